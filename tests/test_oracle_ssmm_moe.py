@@ -1,0 +1,234 @@
+"""Pins for oracle/devlayout.py, oracle/ssmm.py and oracle/moe.py (CPU only)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import bf16, devlayout as D, fmt as F, moe, ssmm
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def bits(a):
+    return synth.f32_to_bf16_bits(np.asarray(a, dtype=np.float32))
+
+
+def make_enc(fmt, rows, cols, seed=11, integer=False):
+    w = synth.weight_bf16(seed, rows, cols, integer=integer)
+    return F.encode(F.prune(w, fmt), fmt)
+
+
+# ----------------------------------------------------------- device layouts
+
+@pytest.mark.parametrize("fmt", [F.SparseFormat(1, 2, 32), F.SparseFormat(1, 2, 16), F.SparseFormat(4, 8, 32)])
+def test_a_image_is_sw128_permutation_of_values(fmt):
+    enc = make_enc(fmt, 192 * fmt.m // fmt.n // 2 * 2, 256)
+    img = D.a_image(enc)
+    g = D.geometry(enc.rows, enc.cols, fmt)
+    # independent formulation of the 128B swizzle: byte offset bits [4,7) ^= bits [7,10)
+    rep = g["rep"]
+    for t in range(g["m_tiles"]):
+        for s in range(g["k_stages"]):
+            blk = img[t, s]
+            for r in (0, 5, 63, 127):
+                cr = t * 128 + r
+                for c in range(64):
+                    lin = r * 128 + c * 2
+                    phys = lin ^ (((lin >> 7) & 7) << 4)
+                    got = blk[phys:phys + 2].view(np.uint16)[0]
+                    vb, slot = s * 4 + c // 16, c % 16
+                    if cr >= g["R"]:
+                        assert got == 0
+                        continue
+                    j, h = vb // rep, vb % rep
+                    if rep == 1 or (slot // 8) == h:
+                        assert got == enc.values[cr, j * 16 + slot]
+                    else:
+                        assert got == 0
+
+
+def test_e_image_matches_cutlass_atom_formula():
+    """The TMEM-image lane order must equal the sm1xx sparse E atom
+    (TensorEAtom_MMA_F16 Shape((8,2,8),(16,2,4)):Stride((128,16,2048),(1,1024,32)),
+    in 8-logical-element bytes) -- an independent derivation."""
+    fmt = F.SparseFormat(1, 2, 32)
+    enc = make_enc(fmt, 256, 256)
+    img = D.e_image(enc)                                   # [mt, ks, 2048]
+    for t in range(img.shape[0]):
+        for s in range(img.shape[1]):
+            blk = img[t, s]
+            for m in range(128):
+                cr = t * 128 + m
+                for k in range(0, 128, 4):                  # logical K within the stage
+                    byte = (256 * (m // 16) + 128 * ((k // 16) % 2) + 16 * (m % 8) + 4 * (k // 32)
+                            + 2 * ((m // 8) % 2) + (k % 16) // 8)
+                    nib = (blk[byte] >> (4 * ((k % 8) // 4))) & 0xF
+                    q = (s * 128 + k) // 4                  # 4-group index along the row
+                    p0, p1 = enc.codes[cr, 2 * q], enc.codes[cr, 2 * q + 1]
+                    assert nib == (p0 | (p1 << 2))
+
+
+def test_planes_bits():
+    fmt = F.SparseFormat(4, 8, 32)
+    enc = make_enc(fmt, 512, 256)
+    P = D.n_planes(fmt)
+    assert P == 3
+    pl = D.planes(enc)
+    mt, ks = pl.shape[:2]
+    words = np.ascontiguousarray(pl).view(np.uint32).reshape(mt, ks, 4, P, 4)
+    for t in range(mt):
+        for s in range(ks):
+            for kb in range(4):
+                for lane in range(128):
+                    v = enc.idx[t * 128 + lane, s * 4 + kb]
+                    got = sum(((int(words[t, s, kb, b, lane // 32]) >> (lane % 32)) & 1) << b for b in range(P))
+                    assert got == v
+    assert D.n_planes(F.SparseFormat(2, 2, 32)) == 0 and D.n_planes(F.SparseFormat(1, 2, 32)) == 1
+
+
+# ---------------------------------------------------------------- SSMM
+
+@pytest.mark.parametrize("fmt", F.TABLE4)
+def test_ssmm_equals_brute_force_masked_matmul(fmt):
+    rows, cols = 2 * fmt.m, 64
+    w = F.prune(synth.weight_bf16(21, rows, cols), fmt)
+    x = synth.activations_bf16(22, 12, cols)
+    sel = np.array([0, 3, 4, 11])
+    enc = F.encode(w, fmt)
+    got = ssmm.ssmm(enc, x, sel)
+    ref = ssmm.masked_dense_reference(w, x, sel)
+    assert np.allclose(got, ref, rtol=1e-12, atol=1e-12)
+
+
+def test_ssmm_identity_pattern_selects_x():
+    fmt = F.SparseFormat(1, 2, 32)
+    rows, cols = 4, 4 * 32
+    w = np.zeros((rows, cols))
+    for o in range(rows):
+        w[o, 32 * o] = 1.0
+    enc = F.encode(bits(w), fmt)
+    x = synth.activations_bf16(3, 9, cols)
+    sel = np.array([1, 2, 8])
+    c = ssmm.ssmm(enc, x, sel)
+    assert np.array_equal(c, bf16.to_f64(x)[sel][:, [0, 32, 64, 96]])
+    assert ssmm.ssmm(enc, x, np.array([], dtype=np.int64)).shape == (0, rows)
+
+
+def test_ssmm_integer_inputs_exact_and_linear():
+    fmt = F.SparseFormat(1, 2, 32)
+    enc = make_enc(fmt, 64, 128, integer=True)
+    x = synth.activations_bf16(5, 16, 128, integer=True)
+    sel = np.arange(16)
+    c = ssmm.ssmm(enc, x, sel)
+    assert np.array_equal(c, np.round(c))
+    x2 = synth.activations_bf16(6, 16, 128, integer=True)
+    xs = bits(bf16.to_f64(x) + bf16.to_f64(x2))
+    assert np.array_equal(ssmm.ssmm(enc, xs, sel), c + ssmm.ssmm(enc, x2, sel))
+
+
+def test_epilogues():
+    fmt = F.SparseFormat(1, 2, 32)
+    g, u = make_enc(fmt, 64, 128, 1), make_enc(fmt, 64, 128, 2)
+    x = synth.activations_bf16(7, 10, 128)
+    sel = np.array([2, 5, 9])
+    cg, cu = ssmm.ssmm(g, x, sel), ssmm.ssmm(u, x, sel)
+    a = ssmm.silu_mul_bf16(cg, cu)
+    ref = cg / (1 + np.exp(-cg)) * cu
+    assert np.all(np.abs(bf16.to_f64(a) - ref) <= np.abs(ref) * 2.0 ** -8 + 1e-30)
+    out = ssmm.scatter_add(np.zeros((10, 64)), cg, sel, [0.5, 2.0, -1.0])
+    assert np.array_equal(out[5], 2.0 * cg[1]) and np.array_equal(out[0], np.zeros(64))
+
+
+# ---------------------------------------------------------------- routing
+
+def test_route_golden_and_invariants():
+    for case in GOLD["route"]["cases"]:
+        ids, w = moe.route(np.array([case["logits"]], dtype=np.float32), case["k"])
+        assert ids[0].tolist() == case["ids"]
+        assert np.allclose(w[0], case["w"])
+    lg = synth.router_logits(2, 50, 8)
+    ids, w = moe.route(lg, 2)
+    assert np.allclose(w.sum(1), 1.0, atol=1e-12)
+    ids2, w2 = moe.route(lg + np.float32(3.0), 2)                    # shift invariance (exact in fp32 here?)
+    assert np.array_equal(ids, ids2)
+    ids3, w3 = moe.route(lg, 2, moe.SOFTMAX_ALL)
+    assert np.array_equal(ids, ids3) and (w3.sum(1) < 1).all()
+
+
+def test_compaction_partition():
+    lg = synth.router_logits(2, 64, 8)
+    ids, w = moe.route(lg, 2)
+    counts, offsets, sel, gw = moe.compact(ids, w, 8)
+    assert counts.sum() == 64 * 2
+    for e in range(8):
+        s = sel[offsets[e]:offsets[e + 1]]
+        assert (np.diff(s) > 0).all()                                # strictly ascending
+        for t in s:
+            assert e in ids[t]
+    pairs = {(int(t), e) for e in range(8) for t in sel[offsets[e]:offsets[e + 1]]}
+    assert pairs == {(t, int(e)) for t in range(64) for e in ids[t]}
+
+
+# ---------------------------------------------------------------- layer
+
+def _experts(fmt, E, d, f, seed0=1000, integer=False):
+    ex = []
+    for e in range(E):
+        ex.append(tuple(make_enc(fmt, *(f, d) if i < 2 else (d, f), seed=seed0 + 3 * e + i, integer=integer)
+                        for i in range(3)))
+    return ex
+
+
+def test_layer_equals_textbook_permute_gemm_unpermute():
+    fmt = F.SparseFormat(1, 2, 32)
+    E, d, f, T, k = 4, 64, 96, 20, 2
+    ex = _experts(fmt, E, d, f)
+    x = synth.activations_bf16(1, T, d)
+    lg = synth.router_logits(2, T, E)
+    out, S = moe.moe_layer(ex, x, lg, k)
+    dense = [tuple(F.dense_f64(w) for w in trip) for trip in ex]
+    ref = moe.moe_layer_textbook(dense, x, lg, k)
+    assert np.allclose(out, ref, rtol=1e-12, atol=1e-12)
+    perm = np.random.default_rng(0).permutation(T)
+    out_p, _ = moe.moe_layer(ex, x[perm], lg[perm], k)
+    assert np.allclose(out_p, out[perm], rtol=1e-12, atol=1e-12)
+    z, _ = moe.moe_layer(ex, np.zeros_like(x), lg, k)
+    assert not z.any()
+    assert (S >= np.abs(out) - 1e-12).all()
+
+
+def test_layer_all_tokens_one_expert_and_shared():
+    fmt = F.SparseFormat(1, 2, 32)
+    E, d, f, T = 2, 64, 64, 6
+    ex = _experts(fmt, E, d, f)
+    x = synth.activations_bf16(1, T, d)
+    lg = np.zeros((T, E), dtype=np.float32)
+    lg[:, 0] = 5.0
+    out, _ = moe.moe_layer(ex, x, lg, 1)
+    y, _, _ = moe.expert_ffn(*ex[0], x, np.arange(T))
+    assert np.allclose(out, y, rtol=1e-12, atol=1e-12)
+    sh = _experts(fmt, 2, d, f, seed0=5000)
+    out2, _ = moe.moe_layer(ex, x, lg, 1, shared=sh)
+    y0, _, _ = moe.expert_ffn(*sh[0], x, np.arange(T))
+    y1, _, _ = moe.expert_ffn(*sh[1], x, np.arange(T))
+    assert np.allclose(out2, y + y0 + y1, rtol=1e-12, atol=1e-12)
+
+
+def test_ep_plan_covers_routing_once():
+    E, P, T, k = 8, 4, 16, 2
+    ids_r, w_r = [], []
+    for s in range(P):
+        ids, w = moe.route(synth.router_logits(100 + s, T, E), k)
+        ids_r.append(ids)
+        w_r.append(w)
+    recv = moe.ep_dispatch_plan(ids_r, w_r, E, P)
+    seen = set()
+    for d in range(P):
+        keys = [(s, t) for s, t, _ in recv[d]]
+        assert keys == sorted(keys) and len(set(keys)) == len(keys)
+        for s, t, tags in recv[d]:
+            for le, _ in tags:
+                seen.add((s, t, d * (E // P) + le))
+    assert seen == {(s, t, int(e)) for s in range(P) for t in range(T) for e in ids_r[s][t]}
