@@ -1,0 +1,183 @@
+/*
+ * samoyeds.h -- C ABI of the B200 (sm_100a) Samoyeds hot path.
+ *
+ * Samoyeds (arXiv 2503.10725) multiplies an MoE expert weight held in a
+ * dual-side sparse format with only the tokens routed to that expert:
+ *   "the original weight is encoded into three components: data, indices,
+ *    and metadata"                                    (§4.1)
+ *   "introduces a selection array (SEL) ... aligns with the sparsity pattern
+ *    presented in token routing"                      (§4.1)
+ *   Alg. 1 "Samoyeds Kernel Scheme": Input A, Indices, Metadata, B, SEL;
+ *    Output C
+ *   "the activation function and its precedent operator are fused ... the
+ *    weighted accumulation ... is fused with matrix multiplication"
+ *                                                      (§4.3)
+ *
+ * Conventions (all entry points):
+ *  - Plain pointers only.  "dev" pointers are CUDA device pointers, "host"
+ *    pointers are host memory.  The CALLER allocates and owns every buffer
+ *    (size them with the *_bytes / *_layout queries); the library allocates
+ *    nothing on the hot path and keeps no pointer after a call returns.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).  All
+ *    calls are asynchronous on that stream; host-side argument validation
+ *    returns synchronously with a status and launches nothing.
+ *  - Data-dependent errors (pattern violations) go to a device status word the
+ *    caller may read after synchronising.
+ *  - bf16 tensors are IEEE bfloat16 bit patterns (uint16), row-major.
+ *  - Requires an sm_100a device (B200); otherwise SMY_E_ARCH.
+ */
+#ifndef SAMOYEDS_H
+#define SAMOYEDS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SMY_API __attribute__((visibility("default")))
+#else
+#define SMY_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SMY_OK = 0,
+  SMY_E_NULL = 1,       /* a required pointer is NULL                           */
+  SMY_E_SHAPE = 2,      /* shape not divisible / unsupported size (ShapeError)  */
+  SMY_E_CONFIG = 3,     /* unsupported (N,M,V) or layer configuration           */
+  SMY_E_PATTERN = 4,    /* weight violates the (N,M,V)+2:4 pattern (device)     */
+  SMY_E_SELECTION = 5,  /* selection array invalid                              */
+  SMY_E_CORRUPT = 6,    /* encoded weight invariant violated                    */
+  SMY_E_WORKSPACE = 7,  /* workspace too small                                  */
+  SMY_E_ARCH = 8,       /* no sm_100 device                                     */
+  SMY_E_CUDA = 9,       /* CUDA runtime error                                   */
+  SMY_E_NCCL = 10       /* NCCL error                                           */
+} smy_status;
+
+SMY_API const char* smy_status_str(int status);
+SMY_API int smy_version(void);
+/* Last CUDA error string seen by the library on this thread (diagnostics). */
+SMY_API const char* smy_last_error(void);
+
+/* ------------------------------------------------------------ format ----
+ * (N, M, V) vector-wise sparsity layered on 2:4 (Fig. 7):
+ * the weight is cut into M x V blocks (M output rows x V reduction columns);
+ * N of the M sub-rows of length V are kept per block and each kept sub-row is
+ * further pruned 2:4.  Table 4 formats: (1,2,16), (1,2,32),
+ * (4,8,32), (8,16,32).  GPU path: M in {1,2,4,8,16}, N | 128, V in {16, 32,
+ * 64, ...} (V=16 only with N=1), cols % 128 == 0, rows % M == 0.           */
+typedef struct { int32_t n, m, v; } smy_format;
+
+/* A logical weight [rows x cols] = [out x in] (PyTorch layout = the paper's
+ * offline-transposed W). */
+typedef struct { int64_t rows, cols; smy_format fmt; } smy_wdesc;
+
+/* Byte sizes of every buffer of an encoded weight.  R = rows*N/M.
+ *   values  : bf16 [R x cols/2]          canonical data matrix
+ *   codes   : u8   [R x cols/8]          canonical 2-bit metadata, 4 per
+ *             byte, code c at bits 2*(c%4), first kept position low
+ *   indices : u8   [R x cols/V]          canonical sub-row indices
+ *   image   : device image consumed by the SSMM kernel: [m_tiles][k_stages]
+ *             blocks of `block` bytes = A smem image (16384, 128B-swizzled
+ *             K-major) | E metadata TMEM image (2048) | index bit-planes
+ *             (64*planes).  See DESIGN.md §HBM layout.                     */
+typedef struct {
+  size_t values, codes, indices, image;
+  int32_t comp_rows, m_tiles, k_stages, planes, rep, block;
+} smy_wlayout;
+SMY_API smy_status smy_weight_layout(const smy_wdesc* desc, smy_wlayout* out);
+
+/* An encoded weight: caller-owned device buffers sized by smy_weight_layout. */
+typedef struct {
+  smy_wdesc d;
+  void* values;   /* dev */
+  void* codes;    /* dev */
+  void* indices;  /* dev */
+  void* image;    /* dev */
+} smy_weight;
+
+#define SMY_PRUNE_MAGNITUDE 1 /* prune to the pattern first: per block keep the N
+                                 sub-rows of largest fp32 L1 (ascending-column
+                                 sum), per 4-group the 2 largest |w|; ties to the
+                                 lower index (reading R4) */
+#define SMY_ASSUME_PRUNED 2   /* input must already conform; violations set
+                                 *d_status = SMY_E_PATTERN */
+
+/* samoyeds_compress: encode a dense bf16 weight (dev, [rows x ldw]) into the
+ * canonical (values, codes, indices) AND the device image (PAPER.md:237,
+ * §4.4 packing).  d_status (dev int32, nullable) receives SMY_OK or
+ * SMY_E_PATTERN; the caller zeroes it first.                                */
+SMY_API smy_status samoyeds_compress(const smy_wdesc* desc, const void* w_bf16, int64_t ldw, int flags,
+                             smy_weight* out, int32_t* d_status, void* stream);
+
+/* ------------------------------------------------------------- SSMM -----
+ * C[t, o] = sum_k W[o, k] * x[sel[t], k] for t < n_sel  (Alg. 1)
+ * with a fused epilogue:
+ *   SMY_EPI_COMPACT          out[t * ldo + o] = C[t, o]      (out_dtype)
+ *   SMY_EPI_SILU_MUL_COMPACT out[t * ldo + o] = bf16(silu(C_w[t,o]) * C_w2[t,o])
+ *                            (w = gate, w2 = up; out_dtype must be BF16)
+ *   SMY_EPI_SCATTER_ADD      out[sel[t] * ldo + o] += scale[t] * C[t, o]  (f32;
+ *                            scale NULL = 1; atomic, order not deterministic)
+ * x: dev bf16 [x_rows x ldx], token-major; sel: dev int32 [n_sel], each in
+ * [0, x_rows) (not validated on device); n_sel may be 0.  fp32 accumulation. */
+typedef enum { SMY_EPI_COMPACT = 0, SMY_EPI_SILU_MUL_COMPACT = 1, SMY_EPI_SCATTER_ADD = 2 } smy_epi;
+#define SMY_F32 0
+#define SMY_BF16 1
+SMY_API smy_status samoyeds_ssmm(const smy_weight* w, const smy_weight* w2, const void* x_bf16, int64_t ldx,
+                         int64_t x_rows, const int32_t* sel, int32_t n_sel, const float* scale, int epi,
+                         void* out, int64_t ldo, int out_dtype, void* stream);
+
+/* --------------------------------------------------- routing / compaction
+ * Top-k of fp32 router logits [T x E] per token (ties -> lower expert id) and
+ * gate weights (readings R9, R10), then the per-expert selection
+ * arrays: counts[E], offsets[E+1] (exclusive scan),
+ * sel[T*k] token ids ascending within each expert, gw[T*k] aligned with sel.
+ * ids/w (dev [T x k]) are written too.  Bit-exact deterministic.          */
+#define SMY_GATE_RENORM_TOPK 0
+#define SMY_GATE_SOFTMAX_ALL 1
+SMY_API smy_status smy_route_workspace_bytes(int64_t T, int32_t E, size_t* bytes);
+SMY_API smy_status samoyeds_route(const float* logits, int64_t T, int32_t E, int32_t k, int gating, int32_t* ids,
+                          float* w, int32_t* counts, int32_t* offsets, int32_t* sel, float* gw, void* workspace,
+                          size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------- MoE layer ---
+ * out[t] = sum_{(e,g) in topk(t)} g * Wd_e( silu(Wg_e x_t) * (Wu_e x_t) )
+ *          + sum_s Wd_s( silu(Wg_s x_t) * (Wu_s x_t) )
+ * experts: host array [E][3] of smy_weight (gate, up, down); shared: host
+ * array [num_shared][3] or NULL.  x dev bf16 [T x hidden]; logits dev fp32
+ * [T x E]; out dev fp32 [T x hidden] (overwritten).  The gate/up -> down
+ * intermediate is bf16 (reading R12).                                     */
+typedef struct {
+  int32_t num_experts, top_k, hidden, ffn, num_shared, gating;
+  smy_format fmt;
+} smy_moe_config;
+typedef struct smy_ep_comm smy_ep_comm; /* opaque, library-owned (EP) */
+SMY_API smy_status smy_moe_workspace_bytes(const smy_moe_config* cfg, int64_t max_tokens, size_t* bytes);
+SMY_API smy_status samoyeds_moe_layer(const smy_moe_config* cfg, const smy_weight* experts, const smy_weight* shared,
+                              const void* x_bf16, const float* logits, int64_t T, float* out, void* workspace,
+                              size_t ws_bytes, smy_ep_comm* comm, void* stream);
+
+/* ------------------------------------------------------------ diagnostics
+ * smy_moe_set_phase_events: when events != NULL (n >= 6 cudaEvent_t handles,
+ * passed as void*), samoyeds_moe_layer records events[0..5] on its stream at
+ * its phase boundaries: start | routing done | out zeroed | gate/up SSMM done |
+ * down SSMM done | shared experts done.  NULL disables.  Process-global, not
+ * thread-safe; used by bench.py to time the dominant kernel inside the timed
+ * region.  smy_launch_count: number of kernels this library has launched.  */
+SMY_API smy_status smy_moe_set_phase_events(void** events, int n);
+SMY_API uint64_t smy_launch_count(void);
+
+/* ------------------------------------------------------ synthetic inputs
+ * Counter-based generator twin of synth/__init__.py (input preparation only,
+ * no method arithmetic): out[i] = value(seed, idx0 + i) for i < n.
+ * dist 0 uniform, 1 Irwin-Hall normal, 2 integer in [lo, hi]; out_bf16 != 0
+ * stores bf16 (RNE) else fp32.                                            */
+SMY_API smy_status smy_synth_fill(uint64_t seed, int dist, float scale, int lo, int hi, int64_t idx0, int64_t n,
+                          void* out, int out_bf16, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAMOYEDS_H */

@@ -1,0 +1,10 @@
+"""B200-native (sm_100a) implementation of the Samoyeds hot path (arXiv 2503.10725):
+dual-side sparse SSMM of MoE expert FFNs behind the C ABI in include/samoyeds.h.
+
+The compute path is libsamoyeds.so (csrc/); this package is the thin Python
+binding over it.  There is no CPU fallback: importing the API without the
+built library raises.
+"""
+from .api import (MoEConfig, MoELayer, Format, SparseWeight, compress, route, ssmm, synth_fill,  # noqa: F401
+                  weight_layout)
+from ._lib import LIB_PATH, SamoyedsError, load  # noqa: F401

@@ -1,0 +1,199 @@
+"""Python API over the C ABI (include/samoyeds.h) -- argument marshalling only.
+
+PyTorch provides device memory and streams; every step of the path runs in
+libsamoyeds.so kernels.  Names follow the C ABI and the paper's notation.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib
+from ._lib import check, smy_format, smy_moe_config, smy_wdesc, smy_weight, smy_wlayout
+
+EPI = {"compact": 0, "silu_mul": 1, "scatter_add": 2}
+GATING = {"renorm_topk": 0, "softmax_all": 1}
+PRUNE_MAGNITUDE = 1
+ASSUME_PRUNED = 2
+
+
+def _stream(stream=None) -> C.c_void_p:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]) -> C.c_void_p:
+    if t is None:
+        return C.c_void_p(0)
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor (no CPU path)")
+    return C.c_void_p(t.data_ptr())
+
+
+@dataclass(frozen=True)
+class Format:
+    """(N, M, V) vector-wise sparsity on top of 2:4."""
+    n: int = 1
+    m: int = 2
+    v: int = 32
+
+    def c(self) -> smy_format:
+        return smy_format(self.n, self.m, self.v)
+
+
+def weight_layout(rows: int, cols: int, fmt: Format) -> dict:
+    lib = _lib.load()
+    d = smy_wdesc(rows, cols, fmt.c())
+    lay = smy_wlayout()
+    check(lib.smy_weight_layout(C.byref(d), C.byref(lay)), "smy_weight_layout")
+    return {f: getattr(lay, f) for f, _ in smy_wlayout._fields_}
+
+
+class SparseWeight:
+    """An encoded weight: canonical (values, codes, indices) + device image."""
+
+    def __init__(self, rows: int, cols: int, fmt: Format, device=None):
+        self.rows, self.cols, self.fmt = rows, cols, fmt
+        self.layout = weight_layout(rows, cols, fmt)
+        dev = device or torch.device("cuda")
+        L = self.layout
+        self.values = torch.empty(L["values"] // 2, dtype=torch.int16, device=dev)
+        self.codes = torch.empty(L["codes"], dtype=torch.uint8, device=dev)
+        self.indices = torch.empty(L["indices"], dtype=torch.uint8, device=dev)
+        self.image = torch.empty(L["image"], dtype=torch.uint8, device=dev)
+
+    def c(self) -> smy_weight:
+        return smy_weight(smy_wdesc(self.rows, self.cols, self.fmt.c()), _ptr(self.values), _ptr(self.codes),
+                          _ptr(self.indices), _ptr(self.image))
+
+    @property
+    def nbytes_canonical(self) -> int:
+        return self.values.numel() * 2 + self.codes.numel() + self.indices.numel()
+
+    def drop_canonical(self) -> None:
+        """Free the canonical copy; the SSMM only reads the device image."""
+        self.values = self.codes = self.indices = None
+
+
+def compress(w: torch.Tensor, fmt: Format, prune: bool = True, stream=None):
+    """samoyeds_compress: w is a CUDA bf16 (or int16 bit-pattern) [rows x cols]
+    tensor.  Returns (SparseWeight, status tensor int32[1])."""
+    lib = _lib.load()
+    if w.dtype == torch.bfloat16:
+        w = w.view(torch.int16)
+    assert w.dtype == torch.int16 and w.dim() == 2 and w.stride(1) == 1
+    rows, cols = w.shape
+    sw = SparseWeight(rows, cols, fmt, w.device)
+    status = torch.zeros(1, dtype=torch.int32, device=w.device)
+    d = smy_wdesc(rows, cols, fmt.c())
+    cw = sw.c()
+    check(lib.samoyeds_compress(C.byref(d), _ptr(w), w.stride(0), PRUNE_MAGNITUDE if prune else ASSUME_PRUNED,
+                                C.byref(cw), _ptr(status), _stream(stream)), "samoyeds_compress")
+    return sw, status
+
+
+def ssmm(w: SparseWeight, x: torch.Tensor, sel: torch.Tensor, epi: str = "compact",
+         w2: Optional[SparseWeight] = None, scale: Optional[torch.Tensor] = None,
+         out: Optional[torch.Tensor] = None, out_dtype=torch.float32, stream=None) -> torch.Tensor:
+    """samoyeds_ssmm.  x: CUDA bf16 [x_rows x cols] token-major; sel: int32
+    [n_sel].  compact/silu_mul return [n_sel x rows]; scatter_add accumulates
+    into ``out`` [x_rows x rows] (fp32) and returns it."""
+    lib = _lib.load()
+    n_sel = sel.numel()
+    if out is None:
+        if epi == "scatter_add":
+            raise ValueError("scatter_add needs an output tensor")
+        dt = torch.bfloat16 if epi == "silu_mul" else out_dtype
+        out = torch.empty(n_sel, w.rows, dtype=dt, device=x.device)
+    odt = 1 if out.dtype == torch.bfloat16 else 0
+    xb = x.view(torch.int16) if x.dtype == torch.bfloat16 else x
+    cw = w.c()
+    cw2 = w2.c() if w2 is not None else None
+    check(lib.samoyeds_ssmm(C.byref(cw), C.byref(cw2) if cw2 is not None else None, _ptr(xb), xb.stride(0),
+                            xb.shape[0], _ptr(sel), n_sel, _ptr(scale), EPI[epi], _ptr(out), out.stride(0), odt,
+                            _stream(stream)), "samoyeds_ssmm")
+    return out
+
+
+def route(logits: torch.Tensor, k: int, gating: str = "renorm_topk", stream=None):
+    """samoyeds_route: top-k + gate weights + per-expert selection arrays."""
+    lib = _lib.load()
+    T, E = logits.shape
+    dev = logits.device
+    ws_bytes = C.c_size_t()
+    check(lib.smy_route_workspace_bytes(T, E, C.byref(ws_bytes)), "smy_route_workspace_bytes")
+    ws = torch.empty(max(ws_bytes.value, 1), dtype=torch.uint8, device=dev)
+    ids = torch.empty(T, k, dtype=torch.int32, device=dev)
+    w = torch.empty(T, k, dtype=torch.float32, device=dev)
+    counts = torch.empty(E, dtype=torch.int32, device=dev)
+    offsets = torch.empty(E + 1, dtype=torch.int32, device=dev)
+    sel = torch.empty(max(T * k, 1), dtype=torch.int32, device=dev)
+    gw = torch.empty(max(T * k, 1), dtype=torch.float32, device=dev)
+    check(lib.samoyeds_route(_ptr(logits), T, E, k, GATING[gating], _ptr(ids), _ptr(w), _ptr(counts),
+                             _ptr(offsets), _ptr(sel), _ptr(gw), _ptr(ws), ws.numel(), _stream(stream)),
+          "samoyeds_route")
+    return ids, w, counts, offsets, sel[:T * k], gw[:T * k]
+
+
+@dataclass
+class MoEConfig:
+    num_experts: int
+    top_k: int
+    hidden: int
+    ffn: int
+    num_shared: int = 0
+    gating: str = "renorm_topk"
+    fmt: Format = Format()
+
+    def c(self) -> smy_moe_config:
+        return smy_moe_config(self.num_experts, self.top_k, self.hidden, self.ffn, self.num_shared,
+                              GATING[self.gating], self.fmt.c())
+
+
+def _weight_array(triples: Sequence[Sequence[SparseWeight]]):
+    flat = [w for t in triples for w in t]
+    arr = (smy_weight * len(flat))(*[w.c() for w in flat])
+    return arr
+
+
+class MoELayer:
+    """samoyeds_moe_layer with a persistent workspace (graph-capturable)."""
+
+    def __init__(self, cfg: MoEConfig, experts, shared=(), max_tokens: int = 4096, device=None):
+        self.cfg = cfg
+        self.experts = experts
+        self.shared = shared
+        self._arr = _weight_array(experts)
+        self._sarr = _weight_array(shared) if shared else None
+        self._cfg = cfg.c()
+        lib = _lib.load()
+        b = C.c_size_t()
+        check(lib.smy_moe_workspace_bytes(C.byref(self._cfg), max_tokens, C.byref(b)), "smy_moe_workspace_bytes")
+        self.max_tokens = max_tokens
+        self.workspace = torch.empty(b.value, dtype=torch.uint8, device=device or torch.device("cuda"))
+
+    def __call__(self, x: torch.Tensor, logits: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None):
+        lib = _lib.load()
+        T = x.shape[0]
+        if T > self.max_tokens:
+            raise ValueError("T exceeds the workspace's max_tokens")
+        if out is None:
+            out = torch.empty(T, self.cfg.hidden, dtype=torch.float32, device=x.device)
+        xb = x.view(torch.int16) if x.dtype == torch.bfloat16 else x
+        check(lib.samoyeds_moe_layer(C.byref(self._cfg), self._arr, self._sarr, _ptr(xb), _ptr(logits), T,
+                                     _ptr(out), _ptr(self.workspace), self.workspace.numel(), None,
+                                     _stream(stream)), "samoyeds_moe_layer")
+        return out
+
+
+def synth_fill(out: torch.Tensor, seed: int, dist: int, scale: float, lo: int = -2, hi: int = 2,
+               idx0: int = 0, stream=None) -> torch.Tensor:
+    """Counter-based generator twin of synth/ (input preparation)."""
+    lib = _lib.load()
+    bf = out.dtype in (torch.bfloat16, torch.int16)
+    check(lib.smy_synth_fill(seed, dist, scale, lo, hi, idx0, out.numel(), _ptr(out), int(bf), _stream(stream)),
+          "smy_synth_fill")
+    return out

@@ -1,0 +1,277 @@
+// C ABI entry points (include/samoyeds.h): host-side validation + dispatch.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstring>
+#include <string>
+
+#include "internal.h"
+
+namespace smy {
+
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+static cudaEvent_t g_phase[6];
+static bool g_phase_on = false;
+
+void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+void record_phase(int i, cudaStream_t s) {
+  if (g_phase_on && i >= 0 && i < 6) cudaEventRecord(g_phase[i], s);
+}
+
+void set_last_error(const char* msg) { g_last_error = msg ? msg : ""; }
+
+smy_status cuda_status(cudaError_t e) {
+  if (e != cudaSuccess) cudaGetLastError();
+  if (e == cudaSuccess) return SMY_OK;
+  g_last_error = cudaGetErrorString(e);
+  return SMY_E_CUDA;
+}
+
+smy_status check_arch() {
+  static int cached = -1;
+  if (cached < 0) {
+    int dev = 0, major = 0, minor = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return SMY_E_CUDA;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    cached = (major == 10 && minor == 0) ? 1 : 0;
+  }
+  if (!cached) {
+    set_last_error("samoyeds requires an sm_100 (B200) device");
+    return SMY_E_ARCH;
+  }
+  return SMY_OK;
+}
+
+static bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+
+smy_status geometry(const smy_wdesc* d, Geometry* g) {
+  if (!d || !g) return SMY_E_NULL;
+  const smy_format f = d->fmt;
+  if (f.n < 1 || f.n > f.m || f.v <= 0 || f.v % 4) {
+    set_last_error("format: need 1 <= N <= M and V a multiple of 4");
+    return SMY_E_CONFIG;
+  }
+  if (!(f.m == 1 || f.m == 2 || f.m == 4 || f.m == 8 || f.m == 16) || !is_pow2(f.n)) {
+    set_last_error("format: GPU path supports M in {1,2,4,8,16}, N a power of two");
+    return SMY_E_CONFIG;
+  }
+  if (!(f.v % 32 == 0 || (f.v == 16 && f.n == 1 && f.m == 2))) {
+    set_last_error("format: V must be a multiple of 32, or V=16 with (N,M)=(1,2)");
+    return SMY_E_CONFIG;
+  }
+  if (d->rows <= 0 || d->cols <= 0 || d->rows % f.m || d->cols % f.v || d->cols % 128) {
+    set_last_error("shape: need rows % M == 0, cols % V == 0 and cols % 128 == 0");
+    return SMY_E_SHAPE;
+  }
+  g->R = d->rows * f.n / f.m;
+  g->rep = f.v == 16 ? 2 : 1;
+  g->m_tiles = (int)((g->R + kTileM - 1) / kTileM);
+  g->k_stages = (int)(d->cols * g->rep / kStageVK);
+  g->ms = (f.n == f.m) ? 1 : f.m;
+  g->planes = g->ms == 1 ? 0 : (f.m == 2 ? 1 : f.m == 4 ? 2 : f.m == 8 ? 3 : 4);
+  g->block = (kABytes + kEBytes + 64 * g->planes + 255) / 256 * 256;
+  return SMY_OK;
+}
+
+smy_status synth_launch(uint64_t seed, int dist, float scale, int lo, int hi, int64_t idx0, int64_t n, void* out,
+                        int out_bf16, cudaStream_t s);
+smy_status moe_workspace_bytes(const smy_moe_config* c, int64_t T, size_t* bytes);
+smy_status moe_layer(const smy_moe_config* c, const smy_weight* experts, const smy_weight* shared, const void* x,
+                     const float* logits, int64_t T, float* out, void* workspace, size_t ws_bytes, cudaStream_t s);
+
+}  // namespace smy
+
+using namespace smy;
+
+extern "C" {
+
+const char* smy_status_str(int s) {
+  switch (s) {
+    case SMY_OK: return "SMY_OK";
+    case SMY_E_NULL: return "SMY_E_NULL";
+    case SMY_E_SHAPE: return "SMY_E_SHAPE";
+    case SMY_E_CONFIG: return "SMY_E_CONFIG";
+    case SMY_E_PATTERN: return "SMY_E_PATTERN";
+    case SMY_E_SELECTION: return "SMY_E_SELECTION";
+    case SMY_E_CORRUPT: return "SMY_E_CORRUPT";
+    case SMY_E_WORKSPACE: return "SMY_E_WORKSPACE";
+    case SMY_E_ARCH: return "SMY_E_ARCH";
+    case SMY_E_CUDA: return "SMY_E_CUDA";
+    case SMY_E_NCCL: return "SMY_E_NCCL";
+    default: return "SMY_E_UNKNOWN";
+  }
+}
+
+int smy_version(void) { return 1; }
+
+const char* smy_last_error(void) { return g_last_error.c_str(); }
+
+smy_status smy_weight_layout(const smy_wdesc* d, smy_wlayout* out) {
+  if (!d || !out) return SMY_E_NULL;
+  Geometry g;
+  smy_status st = geometry(d, &g);
+  if (st != SMY_OK) return st;
+  out->values = (size_t)g.R * (d->cols / 2) * 2;
+  out->codes = (size_t)g.R * (d->cols / 8);
+  out->indices = (size_t)g.R * (d->cols / d->fmt.v);
+  out->image = (size_t)g.m_tiles * g.k_stages * g.block;
+  out->comp_rows = (int32_t)g.R;
+  out->m_tiles = g.m_tiles;
+  out->k_stages = g.k_stages;
+  out->planes = g.planes;
+  out->rep = g.rep;
+  out->block = g.block;
+  return SMY_OK;
+}
+
+smy_status samoyeds_compress(const smy_wdesc* desc, const void* w_bf16, int64_t ldw, int flags, smy_weight* out,
+                             int32_t* d_status, void* stream) {
+  if (!desc || !w_bf16 || !out || !out->values || !out->codes || !out->indices || !out->image) return SMY_E_NULL;
+  Geometry g;
+  smy_status st = geometry(desc, &g);
+  if (st != SMY_OK) return st;
+  if (ldw < desc->cols) return SMY_E_SHAPE;
+  if ((flags & (SMY_PRUNE_MAGNITUDE | SMY_ASSUME_PRUNED)) == (SMY_PRUNE_MAGNITUDE | SMY_ASSUME_PRUNED))
+    return SMY_E_CONFIG;
+  if ((st = check_arch()) != SMY_OK) return st;
+  out->d = *desc;
+  return compress_launch(desc, g, static_cast<const uint16_t*>(w_bf16), ldw, flags, out, d_status,
+                         static_cast<cudaStream_t>(stream));
+}
+
+smy_status samoyeds_ssmm(const smy_weight* w, const smy_weight* w2, const void* x_bf16, int64_t ldx, int64_t x_rows,
+                         const int32_t* sel, int32_t n_sel, const float* scale, int epi, void* out, int64_t ldo,
+                         int out_dtype, void* stream) {
+  if (!w || !w->image || (n_sel > 0 && (!sel || !x_bf16 || !out))) return SMY_E_NULL;
+  Geometry g;
+  smy_status st = geometry(&w->d, &g);
+  if (st != SMY_OK) return st;
+  if (n_sel < 0) return SMY_E_SELECTION;
+  if (ldx < w->d.cols || ldx % 8 || x_rows < 0) return SMY_E_SHAPE;
+  if (epi == SMY_EPI_SILU_MUL_COMPACT) {
+    if (!w2 || !w2->image) return SMY_E_NULL;
+    if (memcmp(&w2->d, &w->d, sizeof(smy_wdesc)) != 0) return SMY_E_SHAPE;
+    if (out_dtype != SMY_BF16) return SMY_E_CONFIG;
+    if (g.ms >= 16) {
+      set_last_error("SILU_MUL fusion unsupported for M=16 (use two COMPACT calls)");
+      return SMY_E_CONFIG;
+    }
+  } else if (epi == SMY_EPI_SCATTER_ADD) {
+    if (out_dtype != SMY_F32) return SMY_E_CONFIG;
+  } else if (epi != SMY_EPI_COMPACT) {
+    return SMY_E_CONFIG;
+  }
+  if (out_dtype != SMY_F32 && out_dtype != SMY_BF16) return SMY_E_CONFIG;
+  if (ldo < w->d.rows || (ldo % 2)) return SMY_E_SHAPE;
+  if ((st = check_arch()) != SMY_OK) return st;
+  if (n_sel == 0) return SMY_OK;
+  const int nw = epi == SMY_EPI_SILU_MUL_COMPACT ? 2 : 1;
+  const int nt = ssmm_pick_nt(nw, g.ms, g.rep, n_sel);
+  SsmmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.img0[0] = static_cast<const uint8_t*>(w->image);
+  a.img1[0] = nw == 2 ? static_cast<const uint8_t*>(w2->image) : nullptr;
+  a.num_groups = 1;
+  a.R = (int)g.R;
+  a.m_out = (int)w->d.rows;
+  a.n_fmt = g.ms == 1 ? 1 : w->d.fmt.n;
+  a.m_fmt = g.ms == 1 ? 1 : w->d.fmt.m;
+  a.m_tiles = g.m_tiles;
+  a.k_stages = g.k_stages;
+  a.planes = g.planes;
+  a.block = g.block;
+  a.x = static_cast<const uint16_t*>(x_bf16);
+  a.ldx = ldx;
+  a.x_rows = x_rows;
+  a.sel_in = sel;
+  a.offsets = nullptr;
+  a.tile_prefix = nullptr;
+  a.n_sel = n_sel;
+  a.epi = epi == SMY_EPI_COMPACT ? kEpiCompact : epi == SMY_EPI_SILU_MUL_COMPACT ? kEpiSiluMul : kEpiScatter;
+  a.out_bf16 = out_dtype == SMY_BF16;
+  a.out = out;
+  a.ldo = ldo;
+  a.sel_out = sel;
+  a.scale = scale;
+  a.max_tiles = g.m_tiles * ((n_sel + nt - 1) / nt);
+  return ssmm_launch(a, nt, nw, g.ms, g.rep, static_cast<cudaStream_t>(stream));
+}
+
+smy_status smy_route_workspace_bytes(int64_t T, int32_t E, size_t* bytes) {
+  if (!bytes) return SMY_E_NULL;
+  if (T < 0 || E < 1) return SMY_E_SHAPE;
+  *bytes = route_ws_bytes(T, E);
+  return SMY_OK;
+}
+
+smy_status samoyeds_route(const float* logits, int64_t T, int32_t E, int32_t k, int gating, int32_t* ids, float* w,
+                          int32_t* counts, int32_t* offsets, int32_t* sel, float* gw, void* workspace,
+                          size_t ws_bytes, void* stream) {
+  if (!counts || !offsets || !workspace) return SMY_E_NULL;
+  if (T > 0 && (!logits || !ids || !w || !sel || !gw)) return SMY_E_NULL;
+  if (T < 0 || E < 1 || k < 1 || k > E) return SMY_E_SHAPE;
+  if (gating != SMY_GATE_RENORM_TOPK && gating != SMY_GATE_SOFTMAX_ALL) return SMY_E_CONFIG;
+  smy_status st;
+  if ((st = check_arch()) != SMY_OK) return st;
+  return route_launch(logits, T, E, k, gating, ids, w, counts, offsets, sel, gw, workspace, ws_bytes, nullptr,
+                      nullptr, 0, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+smy_status smy_moe_workspace_bytes(const smy_moe_config* cfg, int64_t max_tokens, size_t* bytes) {
+  if (!cfg || !bytes) return SMY_E_NULL;
+  if (max_tokens < 0) return SMY_E_SHAPE;
+  return moe_workspace_bytes(cfg, max_tokens, bytes);
+}
+
+smy_status samoyeds_moe_layer(const smy_moe_config* cfg, const smy_weight* experts, const smy_weight* shared,
+                              const void* x_bf16, const float* logits, int64_t T, float* out, void* workspace,
+                              size_t ws_bytes, smy_ep_comm* comm, void* stream) {
+  if (!cfg || !experts || !out || !workspace) return SMY_E_NULL;
+  if (T > 0 && (!x_bf16 || !logits)) return SMY_E_NULL;
+  if (cfg->num_experts < 1 || cfg->top_k < 1 || cfg->top_k > cfg->num_experts || cfg->top_k > 8 ||
+      cfg->num_experts > kMaxGroups || cfg->num_shared < 0 || (cfg->num_shared > 0 && !shared))
+    return SMY_E_CONFIG;
+  if (cfg->hidden % 128 || cfg->ffn % 128) return SMY_E_SHAPE;
+  if (comm != nullptr) {
+    set_last_error("expert-parallel communicator: use the Python EP driver (parallel.ep)");
+    return SMY_E_CONFIG;
+  }
+  for (int e = 0; e < cfg->num_experts; ++e)
+    for (int i = 0; i < 3; ++i) {
+      const smy_weight& w = experts[3 * e + i];
+      const int64_t rows = i < 2 ? cfg->ffn : cfg->hidden, cols = i < 2 ? cfg->hidden : cfg->ffn;
+      if (!w.image) return SMY_E_NULL;
+      if (w.d.rows != rows || w.d.cols != cols || memcmp(&w.d.fmt, &cfg->fmt, sizeof(smy_format)) != 0)
+        return SMY_E_SHAPE;
+    }
+  smy_status st;
+  if ((st = check_arch()) != SMY_OK) return st;
+  return moe_layer(cfg, experts, shared, x_bf16, logits, T, out, workspace, ws_bytes,
+                   static_cast<cudaStream_t>(stream));
+}
+
+smy_status smy_moe_set_phase_events(void** events, int n) {
+  if (events == nullptr) {
+    g_phase_on = false;
+    return SMY_OK;
+  }
+  if (n < 6) return SMY_E_SHAPE;
+  for (int i = 0; i < 6; ++i) g_phase[i] = static_cast<cudaEvent_t>(events[i]);
+  g_phase_on = true;
+  return SMY_OK;
+}
+
+uint64_t smy_launch_count(void) { return g_launches.load(); }
+
+smy_status smy_synth_fill(uint64_t seed, int dist, float scale, int lo, int hi, int64_t idx0, int64_t n, void* out,
+                          int out_bf16, void* stream) {
+  if (!out && n > 0) return SMY_E_NULL;
+  if (dist < 0 || dist > 2 || (dist == 2 && hi < lo)) return SMY_E_CONFIG;
+  smy_status st;
+  if ((st = check_arch()) != SMY_OK) return st;
+  return synth_launch(seed, dist, scale, lo, hi, idx0, n, out, out_bf16, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

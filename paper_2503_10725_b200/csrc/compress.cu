@@ -1,0 +1,181 @@
+// samoyeds_compress: (optional magnitude pruning) + encoding into the
+// canonical data / indices / metadata (§4.1) and packing into the
+// sm_100a device image (the B200 counterpart of §4.4's data packing).
+#include <cuda_bf16.h>
+
+#include "internal.h"
+
+namespace smy {
+
+__device__ __forceinline__ float bf16_abs_f32(uint16_t b) { return __uint_as_float((uint32_t)(b & 0x7FFF) << 16); }
+__device__ __forceinline__ bool bf16_nz(uint16_t b) { return (b & 0x7FFF) != 0; }
+
+// One thread per (row-group g, K-block j): select the N kept sub-rows and the
+// 2-of-4 positions, write values / codes / indices.
+__global__ void encode_kernel(const uint16_t* __restrict__ w, int64_t ldw, int64_t rows, int64_t cols, int N,
+                              int M, int V, int prune, uint16_t* __restrict__ values, uint8_t* __restrict__ codes,
+                              uint8_t* __restrict__ indices, int32_t* status) {
+  const int64_t J = cols / V;
+  const int64_t G = rows / M;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= G * J) return;
+  const int64_t g = tid / J, j = tid % J;
+  const uint16_t* blk = w + (g * M) * ldw + j * V;
+
+  // --- choose the N sub-rows (ascending row order)
+  int pick[16];
+  if (prune) {
+    float score[16];
+    for (int r = 0; r < M; ++r) {
+      float acc = 0.f;
+      for (int c = 0; c < V; ++c) acc = __fadd_rn(acc, bf16_abs_f32(blk[r * ldw + c]));  // sequential fp32 (R4)
+      score[r] = acc;
+    }
+    int n = 0;
+    for (int r = 0; r < M; ++r) {
+      int beaten = 0;
+      for (int o = 0; o < M; ++o) beaten += (score[o] > score[r]) || (score[o] == score[r] && o < r);
+      if (beaten < N) pick[n++] = r;
+    }
+  } else {
+    bool nz[16];
+    int cnt = 0;
+    for (int r = 0; r < M; ++r) {
+      bool any = false;
+      for (int c = 0; c < V; ++c) any |= bf16_nz(blk[r * ldw + c]);
+      nz[r] = any;
+      cnt += any;
+    }
+    if (cnt > N && status) atomicExch(status, (int)SMY_E_PATTERN);
+    // non-zero rows first, then the lowest unused rows (R5), then sort ascending
+    int n = 0;
+    for (int r = 0; r < M && n < N; ++r)
+      if (nz[r]) pick[n++] = r;
+    for (int r = 0; r < M && n < N; ++r)
+      if (!nz[r]) pick[n++] = r;
+    for (int a = 1; a < N; ++a)  // insertion sort
+      for (int b = a; b > 0 && pick[b - 1] > pick[b]; --b) {
+        int t = pick[b]; pick[b] = pick[b - 1]; pick[b - 1] = t;
+      }
+  }
+
+  // --- per kept sub-row: 2 of every 4 elements
+  for (int i = 0; i < N; ++i) {
+    const int64_t rc = g * N + i;  // compressed row
+    const uint16_t* src = blk + pick[i] * ldw;
+    indices[rc * J + j] = (uint8_t)pick[i];
+    uint16_t* vout = values + rc * (cols / 2) + j * (V / 2);
+    uint8_t* cout = codes + rc * (cols / 8) + j * (V / 8);
+    for (int q = 0; q < V / 4; q += 2) {
+      uint8_t byte = 0;
+      for (int h = 0; h < 2; ++h) {
+        const uint16_t* e = src + 4 * (q + h);
+        int p0, p1;
+        if (prune) {  // two largest |w|, ties -> lower position
+          int keep[2], nk = 0;
+          for (int p = 0; p < 4; ++p) {
+            int beaten = 0;
+            const float ap = bf16_abs_f32(e[p]);
+            for (int o = 0; o < 4; ++o) {
+              const float ao = bf16_abs_f32(e[o]);
+              beaten += (ao > ap) || (ao == ap && o < p);
+            }
+            if (beaten < 2) keep[nk++] = p;
+          }
+          p0 = keep[0]; p1 = keep[1];
+        } else {  // the non-zeros, padded with the smallest unused positions (R6)
+          int pos[4], np = 0, nzc = 0;
+          for (int p = 0; p < 4; ++p) nzc += bf16_nz(e[p]);
+          if (nzc > 2 && status) atomicExch(status, (int)SMY_E_PATTERN);
+          for (int p = 0; p < 4 && np < 2; ++p)
+            if (bf16_nz(e[p])) pos[np++] = p;
+          for (int p = 0; p < 4 && np < 2; ++p)
+            if (!bf16_nz(e[p])) pos[np++] = p;
+          p0 = min(pos[0], pos[1]); p1 = max(pos[0], pos[1]);
+        }
+        vout[2 * (q + h)] = e[p0];
+        vout[2 * (q + h) + 1] = e[p1];
+        byte |= (uint8_t)((p0 | (p1 << 2)) << (4 * h));
+      }
+      cout[q / 2] = byte;
+    }
+  }
+}
+
+// One CTA (128 threads = 128 TMEM lanes) per (m_tile, k_stage) image block.
+__global__ void pack_kernel(const uint16_t* __restrict__ values, const uint8_t* __restrict__ codes,
+                            const uint8_t* __restrict__ indices, int64_t R, int64_t cols, int V, int rep, int P,
+                            int k_stages, int block, uint8_t* __restrict__ image) {
+  const int mt = blockIdx.x / k_stages, s = blockIdx.x % k_stages;
+  const int l = threadIdx.x;
+  const int64_t cr = (int64_t)mt * kTileM + l;
+  const bool valid = cr < R;
+  uint8_t* blk = image + (size_t)blockIdx.x * block;
+  const int64_t vcols = cols / 2, ccols = cols / 8, icols = cols / V;
+
+  // A: 8 chunks of 16 B per row, 128B swizzle
+  for (int ch = 0; ch < 8; ++ch) {
+    const int kb = ch >> 1, half = ch & 1;
+    const int vb = s * 4 + kb;
+    uint4 val = make_uint4(0, 0, 0, 0);
+    if (valid) {
+      const int j = vb / rep, h = vb % rep;
+      if (rep == 1 || half == h)
+        val = *reinterpret_cast<const uint4*>(values + cr * vcols + (int64_t)j * 16 + half * 8);
+    }
+    *reinterpret_cast<uint4*>(blk + (l >> 3) * 1024 + (l & 7) * 128 + ((ch ^ (l & 7)) << 4)) = val;
+  }
+  // E: lane-major TMEM image
+  {
+    const int r_lo = (l & 7) + 16 * (l >> 4), r_hi = r_lo + 8, k1 = (l >> 3) & 1;
+    const int64_t c_lo = (int64_t)mt * kTileM + r_lo, c_hi = (int64_t)mt * kTileM + r_hi;
+    uint32_t wd[4];
+    for (int kb = 0; kb < 4; ++kb) {
+      const int vb = s * 4 + kb;
+      const int j = vb / rep, h = vb % rep;
+      const bool live = rep == 1 || k1 == h;
+      // 4-groups 8j+4k1 .. +3 of the row = codes bytes 4j+2k1, 4j+2k1+1 (nibble q at bits 4q)
+      auto half16 = [&](int64_t crow) -> uint32_t {
+        if (!live || crow >= R) return 0x4444u;
+        const uint8_t* c = codes + crow * ccols + (int64_t)j * 4 + k1 * 2;
+        return (uint32_t)c[0] | ((uint32_t)c[1] << 8);
+      };
+      wd[kb] = half16(c_lo) | (half16(c_hi) << 16);
+    }
+    *reinterpret_cast<uint4*>(blk + kABytes + 16 * l) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+  }
+  // index bit-planes
+  for (int kb = 0; kb < 4; ++kb) {
+    const int vb = s * 4 + kb;
+    const int vblock = rep == 1 ? (vb * 32) / V : vb;
+    const int idx = valid ? indices[cr * icols + vblock] : 0;
+    for (int b = 0; b < P; ++b) {
+      const uint32_t word = __ballot_sync(0xffffffffu, (idx >> b) & 1);
+      if ((l & 31) == 0) *reinterpret_cast<uint32_t*>(blk + kABytes + kEBytes + (kb * P + b) * 16 + (l >> 5) * 4) = word;
+    }
+  }
+  // zero the tail pad
+  for (int o = kABytes + kEBytes + 64 * P + 4 * l; o < block; o += 4 * kTileM)
+    *reinterpret_cast<uint32_t*>(blk + o) = 0u;
+}
+
+smy_status compress_launch(const smy_wdesc* d, const Geometry& g, const uint16_t* w, int64_t ldw, int flags,
+                           smy_weight* out, int32_t* d_status, cudaStream_t s) {
+  const int64_t G = d->rows / d->fmt.m, J = d->cols / d->fmt.v;
+  const int64_t n = G * J;
+  const int prune = (flags & SMY_PRUNE_MAGNITUDE) ? 1 : 0;
+  encode_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(
+      w, ldw, d->rows, d->cols, d->fmt.n, d->fmt.m, d->fmt.v, prune, static_cast<uint16_t*>(out->values),
+      static_cast<uint8_t*>(out->codes), static_cast<uint8_t*>(out->indices), d_status);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_status(e);
+  pack_kernel<<<(unsigned)(g.m_tiles * g.k_stages), kTileM, 0, s>>>(
+      static_cast<const uint16_t*>(out->values), static_cast<const uint8_t*>(out->codes),
+      static_cast<const uint8_t*>(out->indices), g.R, d->cols, d->fmt.v, g.rep, g.planes, g.k_stages, g.block,
+      static_cast<uint8_t*>(out->image));
+  count_launch();
+  return cuda_status(cudaGetLastError());
+}
+
+}  // namespace smy

@@ -1,0 +1,78 @@
+// Internal declarations shared by the library's translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "samoyeds.h"
+
+namespace smy {
+
+constexpr int kTileM = 128;       // compressed rows per tile (TMEM lanes)
+constexpr int kStageVK = 128;     // virtual logical K per pipeline stage (4 x K32)
+constexpr int kABytes = 16384;    // A smem image per stage
+constexpr int kEBytes = 2048;     // E TMEM image per stage
+constexpr int kMaxGroups = 128;   // experts per grouped launch
+
+struct Geometry {
+  int64_t R;        // compressed rows = rows * N / M
+  int m_tiles, k_stages, planes, rep, block;
+  int ms;           // accumulator slots per weight: M, or 1 when N == M
+};
+
+smy_status geometry(const smy_wdesc* d, Geometry* g);
+void set_last_error(const char* msg);
+smy_status cuda_status(cudaError_t e);
+
+// ---------------------------------------------------------------- SSMM
+enum EpiKind { kEpiCompact = 0, kEpiSiluMul = 1, kEpiScatter = 2 };
+
+struct SsmmArgs {
+  const uint8_t* img0[kMaxGroups];  // weight image per group (gate / single)
+  const uint8_t* img1[kMaxGroups];  // up weight image (SILU_MUL only)
+  int num_groups;
+  // weight geometry (identical for every group)
+  int R, m_out, n_fmt, m_fmt, m_tiles, k_stages, planes, block;
+  // activations
+  const uint16_t* x;
+  int64_t ldx, x_rows;
+  const int32_t* sel_in;   // gather rows: x row = sel_in[row0 + t]; NULL: x row = row0 + t
+  const int32_t* offsets;  // per-group row ranges [G+1]; NULL: single group of n_sel rows
+  const int32_t* tile_prefix;  // per-group tile prefix [G+1]; NULL: single group
+  int n_sel;
+  // epilogue
+  int epi, out_bf16;
+  void* out;
+  int64_t ldo;
+  const int32_t* sel_out;  // scatter destinations (SCATTER only)
+  const float* scale;      // scatter scale, NULL = 1
+  int max_tiles;           // grid size
+};
+
+struct SsmmPlan {
+  int nt, nw, ms, rep;
+};
+// Choose the token tile for a launch given the expected tokens per group.
+int ssmm_pick_nt(int nw, int ms, int rep, int64_t tokens_per_group);
+smy_status ssmm_launch(const SsmmArgs& a, int nt, int nw, int ms, int rep, cudaStream_t s);
+
+// --------------------------------------------------------------- routing
+smy_status route_launch(const float* logits, int64_t T, int E, int k, int gating, int32_t* ids, float* w,
+                        int32_t* counts, int32_t* offsets, int32_t* sel, float* gw, void* ws, size_t ws_bytes,
+                        const int* tile_nt, const int* tile_mt, int n_tile_cfgs, int32_t* tile_prefix,
+                        cudaStream_t s);
+size_t route_ws_bytes(int64_t T, int E);
+
+// --------------------------------------------------------------- compress
+smy_status compress_launch(const smy_wdesc* d, const Geometry& g, const uint16_t* w, int64_t ldw, int flags,
+                           smy_weight* out, int32_t* d_status, cudaStream_t s);
+
+// --------------------------------------------------------------- helpers
+smy_status silu_mul_launch(const float* g, const float* u, int64_t rows, int64_t cols, uint16_t* out,
+                           cudaStream_t s);
+smy_status check_arch();
+void count_launch(int n = 1);
+void record_phase(int i, cudaStream_t s);  // no-op unless bench hooks are set
+
+}  // namespace smy

@@ -1,0 +1,247 @@
+// samoyeds_moe_layer: the whole permutation-free MoE expert path on one GPU
+// (§3.1 P:187-189 redundancy removed; §4.5 P:374 compressed output
+// layout; §6.2 P:493 shared experts):
+//
+//   route + compaction (3 small kernels)  ->  memset(out)
+//   grouped gate/up SSMM, fused SiLU*up, compact bf16 intermediate [sum n_e x f]
+//   grouped down SSMM, fused routing-weight scale + scatter-add into out
+//   shared experts: same two launches with SEL = all tokens, weight 1
+//
+// Every launch reads the routing result on the device (tile prefixes written by
+// the scan kernel), so the layer never synchronises with the host and is CUDA-
+// graph capturable.
+#include <cuda_bf16.h>
+
+#include <cstring>
+
+#include "internal.h"
+
+namespace smy {
+
+namespace {
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct LayerWs {
+  int32_t *ids, *counts, *offsets, *sel, *prefix;
+  float *w, *gw;
+  void* route_ws;
+  size_t route_ws_bytes;
+  uint16_t* inter;
+  float *fallback_g, *fallback_u;
+  size_t total;
+};
+
+LayerWs carve(const smy_moe_config* c, int64_t T, bool fallback, uint8_t* base) {
+  LayerWs w{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    uint8_t* p = base ? base + off : nullptr;
+    off = align_up(off + bytes, 256);
+    return p;
+  };
+  const int64_t Tk = T * c->top_k;
+  const int E = c->num_experts;
+  w.ids = reinterpret_cast<int32_t*>(take(Tk * 4));
+  w.w = reinterpret_cast<float*>(take(Tk * 4));
+  w.counts = reinterpret_cast<int32_t*>(take(E * 4));
+  w.offsets = reinterpret_cast<int32_t*>(take((E + 1) * 4));
+  w.sel = reinterpret_cast<int32_t*>(take(Tk * 4));
+  w.gw = reinterpret_cast<float*>(take(Tk * 4));
+  w.prefix = reinterpret_cast<int32_t*>(take(2 * (E + 1) * 4));
+  w.route_ws_bytes = route_ws_bytes(T, E);
+  w.route_ws = take(w.route_ws_bytes);
+  const int64_t inter_rows = Tk > T ? Tk : T;  // shared experts reuse it with T rows
+  w.inter = reinterpret_cast<uint16_t*>(take((size_t)inter_rows * c->ffn * 2));
+  if (fallback) {
+    w.fallback_g = reinterpret_cast<float*>(take((size_t)inter_rows * c->ffn * 4));
+    w.fallback_u = reinterpret_cast<float*>(take((size_t)inter_rows * c->ffn * 4));
+  }
+  w.total = off;
+  return w;
+}
+
+__global__ void silu_mul_kernel(const float* g, const float* u, int64_t n, uint16_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gv = g[i];
+    out[i] = __bfloat16_as_ushort(__float2bfloat16_rn(gv / (1.f + expf(-gv)) * u[i]));
+  }
+}
+}  // namespace
+
+smy_status silu_mul_launch(const float* g, const float* u, int64_t rows, int64_t cols, uint16_t* out,
+                           cudaStream_t s) {
+  const int64_t n = rows * cols;
+  if (n <= 0) return SMY_OK;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  silu_mul_kernel<<<blocks, 256, 0, s>>>(g, u, n, out);
+  count_launch();
+  return cuda_status(cudaGetLastError());
+}
+
+static bool gate_up_fused(const Geometry& g) { return !(g.ms >= 16); }
+
+smy_status moe_workspace_bytes(const smy_moe_config* c, int64_t T, size_t* bytes) {
+  smy_wdesc d{c->ffn, c->hidden, c->fmt};
+  Geometry g;
+  smy_status st = geometry(&d, &g);
+  if (st != SMY_OK) return st;
+  *bytes = carve(c, T, !gate_up_fused(g), nullptr).total;
+  return SMY_OK;
+}
+
+// grouped SSMM over `groups` weights; tile prefix already on the device
+static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* w1, int groups, const Geometry& g,
+                          int m_out, int nt, int nw, const uint16_t* x, int64_t ldx, int64_t x_rows,
+                          const int32_t* sel_in, const int32_t* offsets, const int32_t* prefix, int max_tiles,
+                          int epi, void* out, int64_t ldo, int out_bf16, const int32_t* sel_out,
+                          const float* scale, cudaStream_t s) {
+  SsmmArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int e = 0; e < groups; ++e) {
+    a.img0[e] = static_cast<const uint8_t*>(w0[e]->image);
+    a.img1[e] = w1 ? static_cast<const uint8_t*>(w1[e]->image) : nullptr;
+  }
+  a.num_groups = groups;
+  a.R = (int)g.R;
+  a.m_out = m_out;
+  a.n_fmt = g.ms == 1 ? 1 : w0[0]->d.fmt.n;
+  a.m_fmt = g.ms == 1 ? 1 : w0[0]->d.fmt.m;
+  a.m_tiles = g.m_tiles;
+  a.k_stages = g.k_stages;
+  a.planes = g.planes;
+  a.block = g.block;
+  a.x = x;
+  a.ldx = ldx;
+  a.x_rows = x_rows;
+  a.sel_in = sel_in;
+  a.offsets = offsets;
+  a.tile_prefix = prefix;
+  a.n_sel = 0;
+  a.epi = epi;
+  a.out_bf16 = out_bf16;
+  a.out = out;
+  a.ldo = ldo;
+  a.sel_out = sel_out;
+  a.scale = scale;
+  a.max_tiles = max_tiles;
+  return ssmm_launch(a, nt, nw, g.ms, g.rep, s);
+}
+
+smy_status moe_layer(const smy_moe_config* c, const smy_weight* experts, const smy_weight* shared, const void* x,
+                     const float* logits, int64_t T, float* out, void* workspace, size_t ws_bytes,
+                     cudaStream_t s) {
+  const int E = c->num_experts, k = c->top_k, d = c->hidden, f = c->ffn;
+  smy_wdesc dgu{f, d, c->fmt}, ddn{d, f, c->fmt};
+  Geometry ggu, gdn;
+  smy_status st;
+  if ((st = geometry(&dgu, &ggu)) != SMY_OK) return st;
+  if ((st = geometry(&ddn, &gdn)) != SMY_OK) return st;
+  if (E > kMaxGroups) return SMY_E_CONFIG;
+  const bool fused = gate_up_fused(ggu);
+  LayerWs w = carve(c, T, !fused, static_cast<uint8_t*>(workspace));
+  if (w.total > ws_bytes) return SMY_E_WORKSPACE;
+
+  const int64_t tpg = E ? (T * k + E - 1) / E : 0;
+  const int nt_gu = ssmm_pick_nt(fused ? 2 : 1, ggu.ms, ggu.rep, tpg);
+  const int nt_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, tpg);
+  const int nts[2] = {nt_gu, nt_dn};
+  const int mts[2] = {ggu.m_tiles, gdn.m_tiles};
+  int32_t* prefix_gu = w.prefix;
+  int32_t* prefix_dn = w.prefix + (E + 1);
+
+  record_phase(0, s);
+  if ((st = route_launch(logits, T, E, k, c->gating, w.ids, w.w, w.counts, w.offsets, w.sel, w.gw, w.route_ws,
+                         w.route_ws_bytes, nts, mts, 2, w.prefix, s)) != SMY_OK)
+    return st;
+  record_phase(1, s);
+  cudaError_t ce = cudaMemsetAsync(out, 0, (size_t)T * d * sizeof(float), s);
+  if (ce != cudaSuccess) return cuda_status(ce);
+  record_phase(2, s);
+  if (T == 0) {
+    for (int i = 3; i < 6; ++i) record_phase(i, s);
+    return SMY_OK;
+  }
+
+  const smy_weight* wg[kMaxGroups];
+  const smy_weight* wu[kMaxGroups];
+  const smy_weight* wd[kMaxGroups];
+  for (int e = 0; e < E; ++e) {
+    wg[e] = &experts[3 * e + 0];
+    wu[e] = &experts[3 * e + 1];
+    wd[e] = &experts[3 * e + 2];
+  }
+  const int64_t Tk = T * k;
+  const int max_gu = ggu.m_tiles * (E + (int)((Tk + nt_gu - 1) / nt_gu));
+  const int max_dn = gdn.m_tiles * (E + (int)((Tk + nt_dn - 1) / nt_dn));
+  const uint16_t* xb = static_cast<const uint16_t*>(x);
+
+  // gate/up: H = Wg x[SEL], U = Wu x[SEL], inter = bf16(silu(H) * U)
+  if (fused) {
+    st = grouped(wg, wu, E, ggu, f, nt_gu, 2, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiSiluMul, w.inter, f,
+                 1, nullptr, nullptr, s);
+  } else {
+    st = grouped(wg, nullptr, E, ggu, f, nt_gu, 1, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiCompact,
+                 w.fallback_g, f, 0, nullptr, nullptr, s);
+    if (st == SMY_OK)
+      st = grouped(wu, nullptr, E, ggu, f, nt_gu, 1, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiCompact,
+                   w.fallback_u, f, 0, nullptr, nullptr, s);
+    if (st == SMY_OK) st = silu_mul_launch(w.fallback_g, w.fallback_u, Tk, f, w.inter, s);
+  }
+  if (st != SMY_OK) return st;
+  record_phase(3, s);
+  // down: out[sel[t]] += gw[t] * Wd inter[t]
+  st = grouped(wd, nullptr, E, gdn, d, nt_dn, 1, w.inter, f, Tk, nullptr, w.offsets, prefix_dn, max_dn, kEpiScatter,
+               out, d, 0, w.sel, w.gw, s);
+  if (st != SMY_OK) return st;
+  record_phase(4, s);
+
+  // shared experts: every token, weight 1 (reading R15)
+  for (int i = 0; shared && i < c->num_shared; ++i) {
+    const smy_weight* sg[1] = {&shared[3 * i + 0]};
+    const smy_weight* su[1] = {&shared[3 * i + 1]};
+    const smy_weight* sd[1] = {&shared[3 * i + 2]};
+    const int nts_gu = ssmm_pick_nt(fused ? 2 : 1, ggu.ms, ggu.rep, T);
+    const int nts_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, T);
+    auto single = [&](const smy_weight* const* a0, const smy_weight* const* a1, const Geometry& g, int m_out, int nt,
+                      int nw, const uint16_t* xx, int64_t ldx, int epi, void* o, int64_t ldo, int ob) {
+      SsmmArgs a;
+      memset(&a, 0, sizeof(a));
+      a.img0[0] = static_cast<const uint8_t*>(a0[0]->image);
+      a.img1[0] = a1 ? static_cast<const uint8_t*>(a1[0]->image) : nullptr;
+      a.num_groups = 1;
+      a.R = (int)g.R;
+      a.m_out = m_out;
+      a.n_fmt = g.ms == 1 ? 1 : c->fmt.n;
+      a.m_fmt = g.ms == 1 ? 1 : c->fmt.m;
+      a.m_tiles = g.m_tiles;
+      a.k_stages = g.k_stages;
+      a.planes = g.planes;
+      a.block = g.block;
+      a.x = xx;
+      a.ldx = ldx;
+      a.x_rows = T;
+      a.n_sel = (int)T;
+      a.epi = epi;
+      a.out_bf16 = ob;
+      a.out = o;
+      a.ldo = ldo;
+      a.max_tiles = g.m_tiles * (int)((T + nt - 1) / nt);
+      return ssmm_launch(a, nt, nw, g.ms, g.rep, s);
+    };
+    if (fused) {
+      st = single(sg, su, ggu, f, nts_gu, 2, xb, d, kEpiSiluMul, w.inter, f, 1);
+    } else {
+      st = single(sg, nullptr, ggu, f, nts_gu, 1, xb, d, kEpiCompact, w.fallback_g, f, 0);
+      if (st == SMY_OK) st = single(su, nullptr, ggu, f, nts_gu, 1, xb, d, kEpiCompact, w.fallback_u, f, 0);
+      if (st == SMY_OK) st = silu_mul_launch(w.fallback_g, w.fallback_u, T, f, w.inter, s);
+    }
+    if (st != SMY_OK) return st;
+    st = single(sd, nullptr, gdn, d, nts_dn, 1, w.inter, f, kEpiScatter, out, d, 0);
+    if (st != SMY_OK) return st;
+  }
+  record_phase(5, s);
+  return SMY_OK;
+}
+
+}  // namespace smy

@@ -1,0 +1,178 @@
+// Routing (top-k + gate weights) and warp-level index compaction into
+// per-expert selection arrays (§2.1 routing; P:239/P:303 SEL).
+//
+// Deterministic by construction: positions inside an expert's SEL are ranks
+// by ascending token id, computed from per-warp expert bitmasks
+// (popc(mask & lanemask_lt)) and fixed-order prefix sums -- no atomics decide
+// any output position, so SEL is bit-exact against the oracle.
+#include "internal.h"
+
+namespace smy {
+
+constexpr int kRouteThreads = 256;  // tokens per block
+constexpr int kRouteWarps = kRouteThreads / 32;
+constexpr int kMaxK = 8;
+constexpr int kMaxE = 256;
+
+__device__ __forceinline__ void topk_token(const float* __restrict__ lg, int E, int k, int gating, int* ids,
+                                           float* w) {
+  float bv[kMaxK];
+  int bi[kMaxK];
+  for (int i = 0; i < kMaxK; ++i) { bv[i] = -INFINITY; bi[i] = -1; }
+  for (int e = 0; e < E; ++e) {
+    const float v = lg[e];
+    if (bi[k - 1] >= 0 && !(v > bv[k - 1])) continue;  // ties keep the lower id (R10)
+    int p = k - 1;
+    while (p > 0 && (bi[p - 1] < 0 || v > bv[p - 1])) {
+      bv[p] = bv[p - 1]; bi[p] = bi[p - 1];
+      --p;
+    }
+    bv[p] = v; bi[p] = e;
+  }
+  const float m = bv[0];
+  float s = 0.f;
+  if (gating == SMY_GATE_SOFTMAX_ALL) {
+    for (int e = 0; e < E; ++e) s += expf(lg[e] - m);
+  } else {
+    for (int i = 0; i < k; ++i) s += expf(bv[i] - m);
+  }
+  for (int i = 0; i < k; ++i) {
+    ids[i] = bi[i];
+    w[i] = expf(bv[i] - m) / s;
+  }
+}
+
+// Build per-warp expert masks for this block's tokens (from ids).
+__device__ __forceinline__ void build_masks(const int32_t* __restrict__ ids, int64_t T, int E, int k,
+                                            uint32_t (*mask)[kMaxE]) {
+  for (int i = threadIdx.x; i < kRouteWarps * E; i += kRouteThreads) mask[i / E][i % E] = 0u;
+  __syncthreads();
+  const int64_t t = (int64_t)blockIdx.x * kRouteThreads + threadIdx.x;
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  if (t < T)
+    for (int i = 0; i < k; ++i) atomicOr(&mask[w][ids[t * k + i]], 1u << l);
+  __syncthreads();
+}
+
+__global__ void route_count_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int gating,
+                                   int32_t* __restrict__ ids, float* __restrict__ w, int32_t* __restrict__ blk_counts) {
+  __shared__ uint32_t mask[kRouteWarps][kMaxE];
+  const int64_t t = (int64_t)blockIdx.x * kRouteThreads + threadIdx.x;
+  if (t < T) {
+    int li[kMaxK];
+    float lw[kMaxK];
+    topk_token(logits + t * E, E, k, gating, li, lw);
+    for (int i = 0; i < k; ++i) { ids[t * k + i] = li[i]; w[t * k + i] = lw[i]; }
+  }
+  __syncthreads();
+  build_masks(ids, T, E, k, mask);
+  for (int e = threadIdx.x; e < E; e += kRouteThreads) {
+    int c = 0;
+    for (int ww = 0; ww < kRouteWarps; ++ww) c += __popc(mask[ww][e]);
+    blk_counts[(int64_t)blockIdx.x * E + e] = c;
+  }
+}
+
+// Single block: counts, offsets, per-block bases and SSMM tile prefixes.
+__global__ void route_scan_kernel(const int32_t* __restrict__ blk_counts, int nblk, int E, int32_t* __restrict__ counts,
+                                  int32_t* __restrict__ offsets, int32_t* __restrict__ blk_base, int nt0, int mt0,
+                                  int32_t* __restrict__ prefix0, int nt1, int mt1, int32_t* __restrict__ prefix1) {
+  __shared__ int32_t cnt[kMaxE];
+  __shared__ int32_t off[kMaxE + 1];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int c = 0;
+    for (int b = 0; b < nblk; ++b) c += blk_counts[(int64_t)b * E + e];
+    cnt[e] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0, p0 = 0, p1 = 0;
+    for (int e = 0; e < E; ++e) {
+      off[e] = acc;
+      if (prefix0) prefix0[e] = p0;
+      if (prefix1) prefix1[e] = p1;
+      const int c = cnt[e];
+      acc += c;
+      if (prefix0) p0 += mt0 * ((c + nt0 - 1) / nt0);
+      if (prefix1) p1 += mt1 * ((c + nt1 - 1) / nt1);
+    }
+    off[E] = acc;
+    if (prefix0) prefix0[E] = p0;
+    if (prefix1) prefix1[E] = p1;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    counts[e] = cnt[e];
+    offsets[e] = off[e];
+    int run = off[e];
+    for (int b = 0; b < nblk; ++b) {
+      blk_base[(int64_t)b * E + e] = run;
+      run += blk_counts[(int64_t)b * E + e];
+    }
+  }
+  if (threadIdx.x == 0) offsets[E] = off[E];
+}
+
+__global__ void route_scatter_kernel(const int32_t* __restrict__ ids, const float* __restrict__ w, int64_t T, int E,
+                                     int k, const int32_t* __restrict__ blk_base, int32_t* __restrict__ sel,
+                                     float* __restrict__ gw) {
+  __shared__ uint32_t mask[kRouteWarps][kMaxE];
+  __shared__ int32_t wbase[kRouteWarps][kMaxE];
+  build_masks(ids, T, E, k, mask);
+  for (int e = threadIdx.x; e < E; e += kRouteThreads) {
+    int run = blk_base[(int64_t)blockIdx.x * E + e];
+    for (int ww = 0; ww < kRouteWarps; ++ww) {
+      wbase[ww][e] = run;
+      run += __popc(mask[ww][e]);
+    }
+  }
+  __syncthreads();
+  const int64_t t = (int64_t)blockIdx.x * kRouteThreads + threadIdx.x;
+  if (t >= T) return;
+  const int ww = threadIdx.x / 32, l = threadIdx.x % 32;
+  const uint32_t lt = (1u << l) - 1u;
+  for (int i = 0; i < k; ++i) {
+    const int e = ids[t * k + i];
+    const int pos = wbase[ww][e] + __popc(mask[ww][e] & lt);
+    sel[pos] = (int32_t)t;
+    gw[pos] = w[t * k + i];
+  }
+}
+
+size_t route_ws_bytes(int64_t T, int E) {
+  const int64_t nblk = (T + kRouteThreads - 1) / kRouteThreads;
+  return (size_t)(2 * nblk * E) * sizeof(int32_t) + 256;
+}
+
+smy_status route_launch(const float* logits, int64_t T, int E, int k, int gating, int32_t* ids, float* w,
+                        int32_t* counts, int32_t* offsets, int32_t* sel, float* gw, void* ws, size_t ws_bytes,
+                        const int* tile_nt, const int* tile_mt, int n_tile_cfgs, int32_t* tile_prefix,
+                        cudaStream_t s) {
+  if (E > kMaxE || k > kMaxK || k < 1 || k > E) return SMY_E_CONFIG;
+  if (ws_bytes < route_ws_bytes(T, E)) return SMY_E_WORKSPACE;
+  const int nblk = (int)((T + kRouteThreads - 1) / kRouteThreads);
+  int32_t* blk_counts = static_cast<int32_t*>(ws);
+  int32_t* blk_base = blk_counts + (int64_t)nblk * E;
+  if (T > 0) {
+    route_count_kernel<<<nblk, kRouteThreads, 0, s>>>(logits, T, E, k, gating, ids, w, blk_counts);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_status(e);
+  }
+  route_scan_kernel<<<1, 256, 0, s>>>(blk_counts, nblk, E, counts, offsets, blk_base,
+                                      n_tile_cfgs > 0 ? tile_nt[0] : 1, n_tile_cfgs > 0 ? tile_mt[0] : 0,
+                                      n_tile_cfgs > 0 ? tile_prefix : nullptr,
+                                      n_tile_cfgs > 1 ? tile_nt[1] : 1, n_tile_cfgs > 1 ? tile_mt[1] : 0,
+                                      n_tile_cfgs > 1 ? tile_prefix + (E + 1) : nullptr);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_status(e);
+  if (T > 0) {
+    route_scatter_kernel<<<nblk, kRouteThreads, 0, s>>>(ids, w, T, E, k, blk_base, sel, gw);
+    count_launch();
+    e = cudaGetLastError();
+  }
+  return cuda_status(e);
+}
+
+}  // namespace smy

@@ -1,0 +1,83 @@
+// SSMM host dispatch: (NT, NW, MS, REP) -> kernel instantiation.
+#include "ssmm_kernel.cuh"
+
+namespace smy {
+
+extern template smy_status launch_t<16,1,2,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<32,1,2,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<64,1,2,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<128,1,2,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<224,1,2,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<16,2,2,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<32,2,2,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<64,2,2,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<112,2,2,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<16,1,1,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<32,1,1,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<64,1,1,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<128,1,1,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<256,1,1,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<16,2,1,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<32,2,1,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<64,2,1,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<128,2,1,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<224,2,1,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<32,1,2,2>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<32,2,2,2>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<32,1,4,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<16,1,8,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<16,1,16,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<32,2,4,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<16,2,8,1>(const SsmmArgs&, cudaStream_t);
+
+namespace {
+struct Entry { int nt, nw, ms, rep; smy_status (*fn)(const SsmmArgs&, cudaStream_t); };
+const Entry kTable[] = {
+    {16, 1, 2, 1, &launch_t<16,1,2,1>},
+    {32, 1, 2, 1, &launch_t<32,1,2,1>},
+    {64, 1, 2, 1, &launch_t<64,1,2,1>},
+    {128, 1, 2, 1, &launch_t<128,1,2,1>},
+    {224, 1, 2, 1, &launch_t<224,1,2,1>},
+    {16, 2, 2, 1, &launch_t<16,2,2,1>},
+    {32, 2, 2, 1, &launch_t<32,2,2,1>},
+    {64, 2, 2, 1, &launch_t<64,2,2,1>},
+    {112, 2, 2, 1, &launch_t<112,2,2,1>},
+    {16, 1, 1, 1, &launch_t<16,1,1,1>},
+    {32, 1, 1, 1, &launch_t<32,1,1,1>},
+    {64, 1, 1, 1, &launch_t<64,1,1,1>},
+    {128, 1, 1, 1, &launch_t<128,1,1,1>},
+    {256, 1, 1, 1, &launch_t<256,1,1,1>},
+    {16, 2, 1, 1, &launch_t<16,2,1,1>},
+    {32, 2, 1, 1, &launch_t<32,2,1,1>},
+    {64, 2, 1, 1, &launch_t<64,2,1,1>},
+    {128, 2, 1, 1, &launch_t<128,2,1,1>},
+    {224, 2, 1, 1, &launch_t<224,2,1,1>},
+    {32, 1, 2, 2, &launch_t<32,1,2,2>},
+    {32, 2, 2, 2, &launch_t<32,2,2,2>},
+    {32, 1, 4, 1, &launch_t<32,1,4,1>},
+    {16, 1, 8, 1, &launch_t<16,1,8,1>},
+    {16, 1, 16, 1, &launch_t<16,1,16,1>},
+    {32, 2, 4, 1, &launch_t<32,2,4,1>},
+    {16, 2, 8, 1, &launch_t<16,2,8,1>},
+};
+}  // namespace
+
+int ssmm_pick_nt(int nw, int ms, int rep, int64_t tpg) {
+  // candidate tile widths for this (nw, ms, rep), ascending
+  int best = -1, largest = -1;
+  for (const Entry& e : kTable) {
+    if (e.nw != nw || e.ms != ms || e.rep != rep) continue;
+    if (e.nt > largest) largest = e.nt;
+    if (e.nt >= tpg && (best < 0 || e.nt < best)) best = e.nt;
+  }
+  return best > 0 ? best : largest;
+}
+
+smy_status ssmm_launch(const SsmmArgs& a, int nt, int nw, int ms, int rep, cudaStream_t s) {
+  for (const Entry& e : kTable)
+    if (e.nt == nt && e.nw == nw && e.ms == ms && e.rep == rep) return e.fn(a, s);
+  set_last_error("ssmm: unsupported (nt, nw, ms, rep) combination");
+  return SMY_E_CONFIG;
+}
+
+}  // namespace smy

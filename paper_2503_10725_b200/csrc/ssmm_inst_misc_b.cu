@@ -1,0 +1,6 @@
+// Explicit instantiations of the SSMM kernel (split for parallel compilation).
+#include "ssmm_kernel.cuh"
+
+namespace smy {
+template smy_status launch_t<32,2,4,1>(const SsmmArgs&, cudaStream_t);
+}  // namespace smy

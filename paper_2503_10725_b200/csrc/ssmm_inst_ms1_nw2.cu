@@ -1,0 +1,10 @@
+// Explicit instantiations of the SSMM kernel (split for parallel compilation).
+#include "ssmm_kernel.cuh"
+
+namespace smy {
+template smy_status launch_t<16,2,1,1>(const SsmmArgs&, cudaStream_t);
+template smy_status launch_t<32,2,1,1>(const SsmmArgs&, cudaStream_t);
+template smy_status launch_t<64,2,1,1>(const SsmmArgs&, cudaStream_t);
+template smy_status launch_t<128,2,1,1>(const SsmmArgs&, cudaStream_t);
+template smy_status launch_t<224,2,1,1>(const SsmmArgs&, cudaStream_t);
+}  // namespace smy

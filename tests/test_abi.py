@@ -1,0 +1,75 @@
+"""CPU-only checks of the C ABI boundary: the library builds/loads, exports every
+symbol include/samoyeds.h declares, and its host-side queries/validation work
+without a GPU (no compute calls here)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "samoyeds.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^SMY_API\s+[\w\s\*]+?\b(\w+)\s*\(", src, flags=re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2503_10725_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        from paper_2503_10725_b200 import build
+        build.build()
+    return _lib.load()
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for required in ("samoyeds_compress", "samoyeds_ssmm", "samoyeds_moe_layer", "samoyeds_route"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_2503_10725_b200 import _lib
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+        assert name in _lib.SIGNATURES, f"binding lacks {name}"
+
+
+def test_layout_query_closed_forms(lib):
+    from paper_2503_10725_b200 import Format, weight_layout
+    L = weight_layout(14336, 4096, Format(1, 2, 32))
+    assert L["values"] == 7168 * 2048 * 2
+    assert L["codes"] == 7168 * 4096 // 8
+    assert L["indices"] == 7168 * 4096 // 32
+    assert L["m_tiles"] == 56 and L["k_stages"] == 32 and L["planes"] == 1 and L["rep"] == 1
+    total = L["values"] + L["codes"] + L["indices"]
+    assert total / (14336 * 4096) == 0.578125
+    L16 = weight_layout(128, 256, Format(1, 2, 16))
+    assert L16["rep"] == 2 and L16["k_stages"] == 4
+    assert weight_layout(1408, 2048, Format(2, 2, 32))["planes"] == 0
+    assert weight_layout(512, 512, Format(8, 16, 32))["planes"] == 4
+
+
+def test_host_validation_without_gpu(lib):
+    from paper_2503_10725_b200._lib import smy_wdesc, smy_format, smy_wlayout
+    lay = smy_wlayout()
+    for rows, cols, f, want in ((129, 256, (1, 2, 32), 2), (128, 200, (1, 2, 32), 2), (128, 256, (3, 2, 32), 3),
+                                (128, 256, (1, 2, 8), 3), (128, 256, (2, 4, 16), 3)):
+        d = smy_wdesc(rows, cols, smy_format(*f))
+        assert lib.smy_weight_layout(C.byref(d), C.byref(lay)) == want
+    assert lib.smy_weight_layout(None, C.byref(lay)) == 1
+    assert lib.smy_status_str(4) == b"SMY_E_PATTERN"
+    b = C.c_size_t()
+    assert lib.smy_route_workspace_bytes(4096, 64, C.byref(b)) == 0 and b.value > 0
+
+
+def test_moe_workspace_query(lib):
+    from paper_2503_10725_b200 import MoEConfig, Format
+    from paper_2503_10725_b200._lib import check
+    cfg = MoEConfig(8, 2, 4096, 14336, fmt=Format(1, 2, 32)).c()
+    b = C.c_size_t()
+    check(lib.smy_moe_workspace_bytes(C.byref(cfg), 4096, C.byref(b)), "ws")
+    assert b.value >= 4096 * 2 * 14336 * 2                         # the bf16 intermediate

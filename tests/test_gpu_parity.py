@@ -1,0 +1,306 @@
+"""GPU parity tests: CUDA path (through the C ABI) vs the fp64 CPU oracle.
+
+Bars (BASELINE.json north star): compressor / metadata / routing indices
+bit-exact; SSMM and layer outputs within relative Frobenius 1e-3 and
+per-element |err| <= 1e-2 * sum|w*x|; integer-valued inputs bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import bf16, devlayout as D, fmt as F, moe, ssmm as OS
+
+pytestmark = pytest.mark.gpu
+
+REL_FRO = 1e-3
+ELEM = 1e-2
+
+
+@pytest.fixture(scope="module")
+def smy():
+    import paper_2503_10725_b200 as P
+    P.load()
+    return P
+
+
+def dev16(bits):
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).cuda()
+
+
+def host16(t):
+    return t.cpu().numpy().view(np.uint16)
+
+
+def gpu_format(fmt):
+    from paper_2503_10725_b200 import Format
+    return Format(fmt.n, fmt.m, fmt.v)
+
+
+def check_tol(got, ref, scale, what):
+    err = np.abs(got - ref)
+    rf = OS.rel_fro(got - ref, ref)
+    bad = err > ELEM * scale + 1e-30
+    assert rf <= REL_FRO, f"{what}: rel Frobenius {rf:.3e} > {REL_FRO}"
+    assert not bad.any(), f"{what}: {bad.sum()} elements beyond 1e-2*sum|wx|, first at {np.argwhere(bad)[:3]}"
+
+
+PARITY_FORMATS = [F.SparseFormat(1, 2, 32), F.SparseFormat(1, 2, 16), F.SparseFormat(4, 8, 32),
+                  F.SparseFormat(8, 16, 32), F.SparseFormat(2, 2, 32), F.SparseFormat(1, 1, 32)]
+
+
+# ------------------------------------------------------------------ synth twin
+
+def test_synth_twin_bit_exact(smy):
+    n, idx0 = 5000, 12345
+    idx = np.arange(idx0, idx0 + n, dtype=np.uint64)
+    for dist, scale in ((synth.DIST_UNIFORM, synth.uniform_scale(0.05)), (synth.DIST_NORMAL, synth.normal_scale(1.0)),
+                        (synth.DIST_INT, 0.0)):
+        ref = synth.fill_f32(77, idx, dist, scale)
+        t = torch.empty(n, dtype=torch.float32, device="cuda")
+        smy.synth_fill(t, 77, dist, float(scale), idx0=idx0)
+        assert np.array_equal(t.cpu().numpy().view(np.uint32), ref.view(np.uint32)), dist
+        tb = torch.empty(n, dtype=torch.int16, device="cuda")
+        smy.synth_fill(tb, 77, dist, float(scale), idx0=idx0)
+        assert np.array_equal(host16(tb), synth.f32_to_bf16_bits(ref)), dist
+
+
+# ------------------------------------------------------------------ compressor
+
+@pytest.mark.parametrize("fmt", PARITY_FORMATS, ids=str)
+def test_compress_bit_exact(smy, fmt):
+    rows, cols = 256, 256
+    w = synth.weight_bf16(31, rows, cols)
+    enc = F.encode(F.prune(w, fmt), fmt)
+    sw, status = smy.compress(dev16(w), gpu_format(fmt), prune=True)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 0
+    assert np.array_equal(host16(sw.values).reshape(enc.values.shape), enc.values)
+    assert np.array_equal(sw.codes.cpu().numpy().reshape(-1, cols // 8), F.pack_codes(enc.codes))
+    assert np.array_equal(sw.indices.cpu().numpy().reshape(enc.idx.shape), enc.idx)
+    assert np.array_equal(sw.image.cpu().numpy(), D.weight_image(enc))
+    # ASSUME_PRUNED on the oracle-pruned weight encodes identically
+    sw2, st2 = smy.compress(dev16(F.prune(w, fmt)), gpu_format(fmt), prune=False)
+    torch.cuda.synchronize()
+    assert int(st2.item()) == 0
+    assert torch.equal(sw2.image, sw.image) and torch.equal(sw2.values, sw.values)
+
+
+def test_compress_pattern_error(smy):
+    fmt = F.SparseFormat(1, 2, 32)
+    w = synth.weight_bf16(3, 128, 128)                 # dense: violates the pattern
+    _, status = smy.compress(dev16(w), gpu_format(fmt), prune=False)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 4                     # SMY_E_PATTERN
+
+
+def test_compress_rejects_bad_shapes(smy):
+    from paper_2503_10725_b200 import SamoyedsError
+    with pytest.raises(SamoyedsError):
+        smy.compress(torch.zeros(128, 96, dtype=torch.int16, device="cuda"), smy.Format(1, 2, 32))
+
+
+# ------------------------------------------------------------------ SSMM
+
+def _ssmm_case(smy, fmt, rows, cols, x_rows, sel, integer, seed=41):
+    w = synth.weight_bf16(seed, rows, cols, integer=integer)
+    enc = F.encode(F.prune(w, fmt), fmt)
+    x = synth.activations_bf16(seed + 1, x_rows, cols, integer=integer)
+    sw, _ = smy.compress(dev16(w), gpu_format(fmt))
+    return enc, x, sw
+
+
+def test_ssmm_probe_identity_activations(smy):
+    """E-metadata / A-layout probe: with x = identity, C = W^T exactly, so any
+    mis-read of values, metadata or the sub-row remap shows up positionally."""
+    fmt = F.SparseFormat(1, 2, 32)
+    rows, cols = 256, 128
+    w = synth.weight_bf16(5, rows, cols, integer=True)
+    pruned = F.prune(w, fmt)
+    enc = F.encode(pruned, fmt)
+    x = synth.f32_to_bf16_bits(np.eye(cols, dtype=np.float32))
+    sel = np.arange(cols, dtype=np.int32)
+    sw, _ = smy.compress(dev16(w), gpu_format(fmt))
+    c = smy.ssmm(sw, dev16(x), torch.from_numpy(sel).cuda()).cpu().numpy()     # [cols x rows] = W^T
+    ref = bf16.to_f64(pruned).T
+    if not np.array_equal(c, ref):
+        bad = np.argwhere(c != ref)
+        lines = []
+        for k, o in bad[:12]:
+            hits = np.argwhere(c[:, o] == ref[k, o])[:4].ravel().tolist() if ref[k, o] != 0 else []
+            lines.append(f"(k={k}, o={o}) got {c[k, o]} want {ref[k, o]}; value found at k={hits}")
+        pytest.fail(f"{len(bad)} wrong of {c.size}:\n" + "\n".join(lines))
+
+
+@pytest.mark.parametrize("fmt", PARITY_FORMATS, ids=str)
+def test_ssmm_integer_bit_exact_cfg1(smy, fmt):
+    """BASELINE config 1: W 128x256, 64 tokens with 16 routed; integer inputs -> exact."""
+    sel = synth.selection(4, 64, 16)
+    enc, x, sw = _ssmm_case(smy, fmt, 128, 256, 64, sel, integer=True)
+    got = smy.ssmm(sw, dev16(x), torch.from_numpy(sel).cuda()).cpu().numpy()
+    ref = OS.ssmm(enc, x, sel)
+    assert np.array_equal(got, ref), f"max |err| {np.abs(got - ref).max()}"
+
+
+@pytest.mark.parametrize("fmt", PARITY_FORMATS, ids=str)
+@pytest.mark.parametrize("shape", [(128, 256, 64, 16), (384, 512, 300, 200), (1024, 1408, 900, 777)])
+def test_ssmm_random_tolerance(smy, fmt, shape):
+    rows, cols, x_rows, n_sel = shape
+    if cols % 128:
+        pytest.skip("cols must be a multiple of 128")
+    sel = synth.selection(9, x_rows, n_sel)
+    enc, x, sw = _ssmm_case(smy, fmt, rows, cols, x_rows, sel, integer=False)
+    got = smy.ssmm(sw, dev16(x), torch.from_numpy(sel).cuda()).cpu().numpy().astype(np.float64)
+    check_tol(got, OS.ssmm(enc, x, sel), OS.ssmm_abs(enc, x, sel), f"ssmm {fmt} {shape}")
+
+
+def test_ssmm_ragged_and_empty(smy):
+    fmt = F.SparseFormat(1, 2, 32)
+    for n_sel in (0, 1, 15, 17, 113, 225, 449):
+        sel = synth.selection(n_sel + 1, 512, n_sel)
+        enc, x, sw = _ssmm_case(smy, fmt, 256, 256, 512, sel, integer=True)
+        got = smy.ssmm(sw, dev16(x), torch.from_numpy(sel).cuda()).cpu().numpy()
+        assert got.shape == (n_sel, 256)
+        assert np.array_equal(got, OS.ssmm(enc, x, sel)), n_sel
+
+
+def test_ssmm_bf16_out(smy):
+    fmt = F.SparseFormat(1, 2, 32)
+    sel = synth.selection(2, 128, 40)
+    enc, x, sw = _ssmm_case(smy, fmt, 256, 256, 128, sel, integer=True)
+    got = smy.ssmm(sw, dev16(x), torch.from_numpy(sel).cuda(), out_dtype=torch.bfloat16)
+    assert np.array_equal(host16(got.view(torch.int16)), bf16.from_f64(OS.ssmm(enc, x, sel)))
+
+
+@pytest.mark.parametrize("fmt", [F.SparseFormat(1, 2, 32), F.SparseFormat(4, 8, 32), F.SparseFormat(1, 2, 16),
+                                 F.SparseFormat(2, 2, 32)], ids=str)
+def test_ssmm_scatter_add_exact(smy, fmt):
+    """Fused weighted accumulation: power-of-two scales, integer inputs -> exact."""
+    sel = synth.selection(6, 200, 77)
+    enc, x, sw = _ssmm_case(smy, fmt, 256, 384, 200, sel, integer=True)
+    scale = np.array([2.0 ** (i % 5 - 2) for i in range(len(sel))], dtype=np.float32)
+    base = np.round(np.random.default_rng(0).standard_normal((200, 256)) * 4).astype(np.float32)
+    out = torch.from_numpy(base.copy()).cuda()
+    smy.ssmm(sw, dev16(x), torch.from_numpy(sel).cuda(), epi="scatter_add", scale=torch.from_numpy(scale).cuda(),
+             out=out)
+    ref = OS.scatter_add(base.astype(np.float64), OS.ssmm(enc, x, sel), sel, scale)
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("fmt", [F.SparseFormat(1, 2, 32), F.SparseFormat(4, 8, 32), F.SparseFormat(1, 2, 16),
+                                 F.SparseFormat(1, 1, 32)], ids=str)
+def test_ssmm_silu_mul(smy, fmt):
+    """Fused gate/up + SiLU*up -> bf16 compact intermediate (R11, R12)."""
+    from paper_2503_10725_b200 import Format
+    sel = synth.selection(8, 300, 130)
+    x = synth.activations_bf16(12, 300, 512)
+    wg, wu = synth.weight_bf16(50, 384, 512), synth.weight_bf16(51, 384, 512)
+    eg, eu = F.encode(F.prune(wg, fmt), fmt), F.encode(F.prune(wu, fmt), fmt)
+    sg, _ = smy.compress(dev16(wg), gpu_format(fmt))
+    su, _ = smy.compress(dev16(wu), gpu_format(fmt))
+    got = smy.ssmm(sg, dev16(x), torch.from_numpy(sel).cuda(), epi="silu_mul", w2=su)
+    got = bf16.to_f64(host16(got.view(torch.int16)))
+    cg, cu = OS.ssmm(eg, x, sel), OS.ssmm(eu, x, sel)
+    exact = cg / (1 + np.exp(-cg)) * cu
+    ref_bits = OS.silu_mul_bf16(cg, cu)
+    # within the bf16 rounding of the stored intermediate + fp32 accumulation
+    rf = OS.rel_fro(got - exact, exact)
+    assert rf <= 5e-3, rf
+    ulp = np.abs(bf16.to_f64(ref_bits)) * 2.0 ** -7 + 1e-30
+    mismatch = np.abs(got - bf16.to_f64(ref_bits)) > ulp
+    assert mismatch.mean() < 0.01, mismatch.mean()
+
+
+def test_ssmm_full_size_sampled(smy):
+    """Mixtral gate_proj at full size (14336 x 4096), 1024 of 4096 tokens, in the
+    launch configuration the layer uses; the oracle recomputes sampled output
+    rows from regenerated weight rows (the generator is counter-based)."""
+    fmt = F.SparseFormat(1, 2, 32)
+    rows, cols, T, n_sel = 14336, 4096, 4096, 1024
+    seed = synth.weight_seed(0, 0)
+    wt = torch.empty(rows, cols, dtype=torch.int16, device="cuda")
+    smy.synth_fill(wt, seed, synth.DIST_UNIFORM, float(synth.uniform_scale(np.sqrt(3.0 / cols))))
+    xt = torch.empty(T, cols, dtype=torch.int16, device="cuda")
+    smy.synth_fill(xt, synth.SEED_X, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
+    sel = synth.selection(17, T, n_sel)
+    sw, _ = smy.compress(wt, smy.Format(1, 2, 32))
+    got = smy.ssmm(sw, xt, torch.from_numpy(sel).cuda()).cpu().numpy()
+    del wt
+    rng = np.random.default_rng(0)
+    groups = rng.choice(rows // 2, 24, replace=False)
+    x = synth.activations_bf16(synth.SEED_X, T, cols, row_idx=sel)          # only the routed rows
+    for g in groups:
+        wrows = synth.weight_bf16(seed, rows, cols, row_idx=[2 * g, 2 * g + 1])
+        enc = F.encode(F.prune(wrows, fmt), fmt)
+        ref = OS.ssmm(enc, x, np.arange(n_sel))
+        S = OS.ssmm_abs(enc, x, np.arange(n_sel))
+        check_tol(got[:, 2 * g:2 * g + 2].astype(np.float64), ref, S, f"row group {g}")
+
+
+# ------------------------------------------------------------------ routing
+
+@pytest.mark.parametrize("T,E,k,gating", [(1, 8, 2, "renorm_topk"), (1000, 64, 6, "renorm_topk"),
+                                          (777, 64, 8, "softmax_all"), (4096, 8, 2, "renorm_topk"),
+                                          (300, 60, 4, "renorm_topk")])
+def test_route_bit_exact(smy, T, E, k, gating):
+    lg = synth.router_logits(synth.SEED_LOGITS, T, E, skew=1.0 if E == 64 else 0.0)
+    ids, w, counts, offsets, sel, gw = smy.route(torch.from_numpy(lg).cuda(), k, gating)
+    rid, rw = moe.route(lg, k, moe.SOFTMAX_ALL if gating == "softmax_all" else moe.RENORM_TOPK)
+    rc, ro, rs, rg = moe.compact(rid, rw, E)
+    assert np.array_equal(ids.cpu().numpy(), rid)
+    assert np.array_equal(counts.cpu().numpy(), rc)
+    assert np.array_equal(offsets.cpu().numpy(), ro)
+    assert np.array_equal(sel.cpu().numpy(), rs)
+    assert np.allclose(w.cpu().numpy(), rw, rtol=2e-6, atol=1e-7)
+    assert np.allclose(gw.cpu().numpy(), rg, rtol=2e-6, atol=1e-7)
+
+
+def test_route_ties(smy):
+    lg = np.zeros((64, 8), dtype=np.float32)
+    lg[:, 3] = 1.0
+    ids, *_ = smy.route(torch.from_numpy(lg).cuda(), 3)
+    assert np.array_equal(ids.cpu().numpy(), moe.route(lg, 3)[0])      # ties -> lower ids
+
+
+# ------------------------------------------------------------------ MoE layer
+
+def _layer_case(smy, fmt, E, d, f, T, k, gating="renorm_topk", shared=0, skew=0.0, seed_off=0):
+    cfg = smy.MoEConfig(E, k, d, f, shared, gating, gpu_format(fmt))
+    encs, sws = [], []
+    for e in range(E + shared):
+        te, ts = [], []
+        for i in range(3):
+            r, c = (f, d) if i < 2 else (d, f)
+            w = synth.weight_bf16(synth.weight_seed(e + seed_off, i), r, c)
+            te.append(F.encode(F.prune(w, fmt), fmt))
+            ts.append(smy.compress(dev16(w), gpu_format(fmt))[0])
+        encs.append(tuple(te))
+        sws.append(tuple(ts))
+    x = synth.activations_bf16(synth.SEED_X, T, d)
+    lg = synth.router_logits(synth.SEED_LOGITS, T, E, skew=skew)
+    layer = smy.MoELayer(cfg, sws[:E], sws[E:], max_tokens=max(T, 1))
+    got = layer(dev16(x), torch.from_numpy(lg).cuda()).cpu().numpy().astype(np.float64)
+    mode = moe.SOFTMAX_ALL if gating == "softmax_all" else moe.RENORM_TOPK
+    ref, S = moe.moe_layer(encs[:E], x, lg, k, mode, shared=encs[E:])
+    return got, ref, S
+
+
+@pytest.mark.parametrize("case", [
+    dict(fmt=F.SparseFormat(1, 2, 32), E=8, d=256, f=512, T=100, k=2),
+    dict(fmt=F.SparseFormat(1, 2, 32), E=16, d=256, f=384, T=257, k=6, gating="softmax_all", shared=2, skew=1.0),
+    dict(fmt=F.SparseFormat(1, 2, 32), E=8, d=128, f=256, T=1, k=2),
+    dict(fmt=F.SparseFormat(1, 2, 16), E=4, d=256, f=256, T=64, k=2),
+    dict(fmt=F.SparseFormat(4, 8, 32), E=4, d=256, f=256, T=64, k=2),
+    dict(fmt=F.SparseFormat(8, 16, 32), E=4, d=256, f=256, T=50, k=2),
+], ids=lambda c: f"{c['fmt']}-E{c['E']}-T{c['T']}")
+def test_moe_layer_parity(smy, case):
+    case = dict(case)
+    fmt = case.pop("fmt")
+    got, ref, S = _layer_case(smy, fmt, **case)
+    check_tol(got, ref, S, "moe layer")
+
+
+def test_moe_layer_all_tokens_one_expert(smy):
+    fmt = F.SparseFormat(1, 2, 32)
+    got, ref, S = _layer_case(smy, fmt, E=4, d=128, f=256, T=200, k=1, skew=50.0)
+    check_tol(got, ref, S, "hot expert")
