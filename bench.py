@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""Benchmark: Samoyeds MoE layer on B200 (BASELINE.json metric:
+"SSMM TFLOPS vs B200 2:4-sparse peak; MoE-layer tokens/s at 1/2/4/8 B200").
+
+One step = one call of samoyeds_moe_layer (route + compaction, gate/up SSMM with
+fused SiLU*up, down SSMM with fused routing-weight scale + scatter-add) over one
+batch of T synthetic tokens per GPU, on a random-init layer of the named shape
+in the (1,2,32) format (75% weight sparsity).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--model mixtral|deepseek|qwen2] [--tokens T]
+
+N > 1 is launched by torchrun; every rank runs its own token batch on a full
+replica of the experts ("scaling": "weak"; no data-path collective yet).
+Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MODELS = {
+    # name: (hidden, ffn, experts, top_k, gating)
+    "mixtral": (4096, 14336, 8, 2, "renorm_topk"),
+    "deepseek": (2048, 1408, 64, 6, "softmax_all"),
+    "qwen2": (3584, 2560, 64, 8, "softmax_all"),
+}
+WORKLOAD = {
+    "mixtral": "mixtral-8x7b-moe-layer",
+    "deepseek": "deepseek-moe-16b-moe-layer",
+    "qwen2": "qwen2-57b-a14b-moe-layer",
+}
+FMT = (1, 2, 32)
+BYTES_PER_ELEM = 0.578125     # canonical (1,2,32) bf16 weight bytes per logical element
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained"), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.4)
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def stop(self, t0, t1):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = [ln for ts, ln in self.lines if t0 - 0.05 <= ts <= t1 + 0.05] or [ln for _, ln in self.lines[-3:]]
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in rows:
+            parts = [x.strip() for x in ln.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU oracle
+
+def oracle_sample(model: str, tokens: int, f_slice: int, rank: int = 0):
+    """A bounded sample of the same workload for the CPU oracle: the first
+    `tokens` tokens, all experts, and the first `f_slice` FFN channels of every
+    expert (gate/up rows and down columns [0, f_slice)).  The FFN is a sum over
+    its channels, so oracle time scales linearly with f: full-layer tokens/s =
+    sample tokens/s * f_slice / ffn."""
+    import numpy as np
+
+    import synth
+    from oracle import fmt as F
+    d, f, E, k, gating = MODELS[model]
+    fmt = F.SparseFormat(*FMT)
+    experts = []
+    for e in range(E):
+        trip = []
+        for i in range(3):
+            if i < 2:   # gate/up rows [0, f_slice) of [f x d]
+                w = synth.weight_bf16(synth.weight_seed(e, i), f, d, row_idx=np.arange(f_slice))
+            else:       # down columns [0, f_slice) of [d x f]
+                idx = (np.arange(d, dtype=np.uint64)[:, None] * np.uint64(f)
+                       + np.arange(f_slice, dtype=np.uint64)[None, :])
+                v = synth.fill_f32(synth.weight_seed(e, i), idx, synth.DIST_UNIFORM,
+                                   synth.uniform_scale(np.sqrt(3.0 / f)))
+                w = synth.f32_to_bf16_bits(v)
+            trip.append(F.encode(F.prune(w, fmt), fmt))
+        experts.append(tuple(trip))
+    x = synth.activations_bf16(synth.SEED_X + 100 * rank, tokens, d)
+    lg = synth.router_logits(synth.SEED_LOGITS + 100 * rank, tokens, E)
+    return experts, x, lg, (0 if gating == "renorm_topk" else 1)
+
+
+def time_oracle(model, tokens, f_slice, reps=1):
+    from oracle import moe
+    experts, x, lg, mode = oracle_sample(model, tokens, f_slice)
+    d, f, E, k, _ = MODELS[model]
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        moe.moe_layer(experts, x, lg, k, mode)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(model, tokens=128, f_slice=512):
+    d, f, E, k, _ = MODELS[model]
+    t = time_oracle(model, tokens, f_slice)[0]
+    return {"value": tokens / t * f_slice / f, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
+            "sample": f"{model} layer, {tokens} tokens, all {E} experts, FFN channels [0,{f_slice}) of {f} "
+                      f"(time x {f}/{f_slice}); oracle fp64 NumPy; {t:.2f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    os.environ.setdefault("OMP_NUM_THREADS", str(cpu_cores()))
+    model = args.model
+    d, f, E, k, _ = MODELS[model]
+    tokens, f_slice = 32, 128
+    from oracle import moe
+    experts, x, lg, mode = oracle_sample(model, tokens, f_slice)
+    for _ in range(args.warmup):
+        moe.moe_layer(experts, x, lg, k, mode)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        moe.moe_layer(experts, x, lg, k, mode)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = tokens / dt * f_slice / f
+    line = {"impl": "reference", "metric": "moe_layer_tokens_per_s", "value": value, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD[model], "tokens_per_gpu": args.tokens, "format": "(1,2,32)",
+                       "sample_tokens": tokens, "sample_ffn_channels": f_slice},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
+                             "sample": f"each step: {tokens} tokens, {E} experts, FFN channels [0,{f_slice}) "
+                                       f"of {f}, scaled x {f}/{f_slice}"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def build_layer(P, model, device):
+    import numpy as np
+    import torch
+
+    import synth
+    d, f, E, k, gating = MODELS[model]
+    fmt = P.Format(*FMT)
+    experts = []
+    for e in range(E):
+        trip = []
+        for i in range(3):
+            rows, cols = (f, d) if i < 2 else (d, f)
+            dense = torch.empty(rows, cols, dtype=torch.int16, device=device)
+            P.synth_fill(dense, synth.weight_seed(e, i), synth.DIST_UNIFORM,
+                         float(synth.uniform_scale(np.sqrt(3.0 / cols))))
+            sw, status = P.compress(dense, fmt, prune=True)
+            del dense
+            sw.drop_canonical()
+            trip.append(sw)
+        experts.append(tuple(trip))
+    torch.cuda.synchronize()
+    return experts
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_2503_10725_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    lib = P.load()
+    model = args.model
+    d, f, E, k, gating = MODELS[model]
+    T = args.tokens
+    experts = build_layer(P, model, device)
+    layer = P.MoELayer(P.MoEConfig(E, k, d, f, 0, gating, P.Format(*FMT)), experts, max_tokens=T, device=device)
+
+    x = torch.empty(T, d, dtype=torch.int16, device=device)
+    P.synth_fill(x, synth.SEED_X + 100 * rank, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
+    lg = torch.empty(T, E, dtype=torch.float32, device=device)
+    P.synth_fill(lg, synth.SEED_LOGITS + 100 * rank, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
+    out = torch.empty(T, d, dtype=torch.float32, device=device)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---------------- warm-up
+    for _ in range(args.warmup):
+        layer(x, lg, out)
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (inputs resident in HBM)
+    K = args.steps
+    phase = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(K)]
+    for evs in phase:           # torch creates the cudaEvent_t lazily on first record
+        for ev in evs:
+            ev.record(stream)
+    torch.cuda.synchronize()
+    handles = [(C_void_p_array(ev)) for ev in phase]
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.smy_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_wall0 = time.time()
+    ev0.record(stream)
+    for s in range(K):
+        lib.smy_moe_set_phase_events(handles[s], 6)
+        layer(x, lg, out)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    t_wall1 = time.time()
+    barrier()
+    lib.smy_moe_set_phase_events(None, 0)
+    launches = lib.smy_launch_count() - launches0
+    clk = clocks.stop(t_wall0, t_wall1)
+    ms = ev0.elapsed_time(ev1) / K
+    ph = np.array([[phase[s][i].elapsed_time(phase[s][i + 1]) for i in range(5)] for s in range(K)])
+    ph_ms = ph.mean(0)
+    if world > 1:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---------------- end to end: host buffers, copies inside the timed region
+    x_h = x.cpu().pin_memory()
+    lg_h = lg.cpu().pin_memory()
+    out_h = torch.empty(T, d, dtype=torch.float32).pin_memory()
+    for _ in range(max(2, args.warmup // 2)):
+        x.copy_(x_h, non_blocking=True)
+        lg.copy_(lg_h, non_blocking=True)
+        layer(x, lg, out)
+        out_h.copy_(out, non_blocking=True)
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(K):
+        x.copy_(x_h, non_blocking=True)
+        lg.copy_(lg_h, non_blocking=True)
+        layer(x, lg, out)
+        out_h.copy_(out, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_e2e = e0.elapsed_time(e1) / K
+    if world > 1:
+        t = torch.tensor([ms_e2e], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+
+    # ---------------- roofline of the dominant kernel (gate/up SSMM)
+    hbm, bf16_burst, bf16_sust, src = peaks()
+    sparse_peak = 2.0 * bf16_burst          # 2:4 sparse bf16 = 2 x dense (nominal ratio)
+    Tk = T * k
+    flops_gu = 2 * 2 * (f // 2) * d * Tk     # 2 weights x 2 * (f*N/M) * d * tokens
+    counts = torch.bincount(P.route(lg, k, gating)[0].flatten().long(), minlength=E).cpu().numpy()
+    active = int((counts > 0).sum())
+    bytes_gu = (2 * active * f * d * BYTES_PER_ELEM + Tk * d * 2 + Tk * 4 + Tk * f * 2)
+    t_gu = ph_ms[2] * 1e-3
+    ach_tf = flops_gu / t_gu / 1e12
+    ach_gbs = bytes_gu / t_gu / 1e9
+    ridge = sparse_peak * 1e12 / (hbm * 1e9)
+    tensor_bound = flops_gu / bytes_gu >= ridge
+    roof = ({"bound": "tensor", "achieved": ach_tf, "peak": sparse_peak, "unit": "TFLOP/s",
+             "frac": ach_tf / sparse_peak, "traffic": None,
+             "peak_source": f"2 x {src} bf16 dense burst ({bf16_burst} TF/s)"} if tensor_bound else
+            {"bound": "hbm", "achieved": ach_gbs, "peak": hbm, "unit": "GB/s", "frac": ach_gbs / hbm,
+             "traffic": None, "peak_source": f"{src} hbm_gbs"})
+    roof.update({"kernel": "ssmm_kernel gate/up (NW=2, fused SiLU*up)", "per_launch_ms": ph_ms[2],
+                 "algorithmic_flops": flops_gu, "algorithmic_bytes": bytes_gu,
+                 "other_view": ({"achieved_gbs": ach_gbs, "hbm_frac": ach_gbs / hbm} if tensor_bound else
+                                {"achieved_tflops": ach_tf, "sparse_frac": ach_tf / sparse_peak})})
+    flops_layer = 3 * flops_gu / 2
+    line = {
+        "metric": "moe_layer_tokens_per_s", "value": T * world / (ms * 1e-3), "unit": "tokens/s",
+        "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": WORKLOAD[model], "tokens_per_gpu": T, "global_tokens": T * world, "hidden": d,
+                   "ffn": f, "experts": E, "top_k": k, "gating": gating, "format": "(N,M,V)=(1,2,32) + 2:4",
+                   "parallelism": f"dp{world} (experts replicated per GPU)",
+                   "l2": "inputs larger than L2: %.0f MB of compressed expert weights streamed per step"
+                         % (3 * active * f * d * BYTES_PER_ELEM / 1e6),
+                   "weights": "random-init (counter-based synthetic), magnitude-pruned to (1,2,32)"},
+        "layer_tflops": flops_layer / (ms * 1e-3) / 1e12,
+        "phases_ms": {"route_compact": ph_ms[0], "zero_out": ph_ms[1], "gate_up_ssmm": ph_ms[2],
+                      "down_ssmm": ph_ms[3]},
+        "down_ssmm_tflops": (flops_gu / 2) / (ph_ms[3] * 1e-3) / 1e12,
+        "roofline": roof,
+        "e2e": {"value": T * world / (ms_e2e * 1e-3), "unit": "tokens/s",
+                "h2d_bytes_per_step": T * d * 2 + T * E * 4, "d2h_bytes_per_step": T * d * 4},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(model)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def C_void_p_array(events):
+    import ctypes as C
+    arr = (C.c_void_p * len(events))(*[C.c_void_p(ev.cuda_event) for ev in events])
+    return arr
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="mixtral", choices=sorted(MODELS))
+    ap.add_argument("--tokens", type=int, default=4096)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

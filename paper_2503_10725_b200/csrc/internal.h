@@ -1,5 +1,6 @@
 // Internal declarations shared by the library's translation units.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstddef>
@@ -29,6 +30,7 @@ smy_status cuda_status(cudaError_t e);
 enum EpiKind { kEpiCompact = 0, kEpiSiluMul = 1, kEpiScatter = 2 };
 
 struct SsmmArgs {
+  CUtensorMap tmap_x;               // contiguous x rows: 2D TMA box 64 x NT, 128B swizzle
   const uint8_t* img0[kMaxGroups];  // weight image per group (gate / single)
   const uint8_t* img1[kMaxGroups];  // up weight image (SILU_MUL only)
   int num_groups;
@@ -47,8 +49,13 @@ struct SsmmArgs {
   int64_t ldo;
   const int32_t* sel_out;  // scatter destinations (SCATTER only)
   const float* scale;      // scatter scale, NULL = 1
-  int max_tiles;           // grid size
+  int max_tiles;           // tile count (single group) / upper bound (grouped)
+  int weights_stream;      // 1: weights read once per call (decode) -> L2 evict_first
 };
+
+// Tensor map over a token-major bf16 activation matrix [rows x cols] (ld elements):
+// boxes of 64 elements x box_rows rows, 128-byte swizzle (the UMMA K-major atom).
+smy_status make_x_tmap(CUtensorMap* map, const void* x, int64_t cols, int64_t rows, int64_t ld, int box_rows);
 
 struct SsmmPlan {
   int nt, nw, ms, rep;

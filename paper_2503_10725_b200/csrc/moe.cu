@@ -95,7 +95,7 @@ static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* 
                           int m_out, int nt, int nw, const uint16_t* x, int64_t ldx, int64_t x_rows,
                           const int32_t* sel_in, const int32_t* offsets, const int32_t* prefix, int max_tiles,
                           int epi, void* out, int64_t ldo, int out_bf16, const int32_t* sel_out,
-                          const float* scale, cudaStream_t s) {
+                          const float* scale, int64_t k_cols, int stream_w, cudaStream_t s) {
   SsmmArgs a;
   memset(&a, 0, sizeof(a));
   for (int e = 0; e < groups; ++e) {
@@ -125,6 +125,9 @@ static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* 
   a.sel_out = sel_out;
   a.scale = scale;
   a.max_tiles = max_tiles;
+  a.weights_stream = stream_w;
+  smy_status st = make_x_tmap(&a.tmap_x, x, k_cols, x_rows, ldx, nt);
+  if (st != SMY_OK) return st;
   return ssmm_launch(a, nt, nw, g.ms, g.rep, s);
 }
 
@@ -179,20 +182,20 @@ smy_status moe_layer(const smy_moe_config* c, const smy_weight* experts, const s
   // gate/up: H = Wg x[SEL], U = Wu x[SEL], inter = bf16(silu(H) * U)
   if (fused) {
     st = grouped(wg, wu, E, ggu, f, nt_gu, 2, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiSiluMul, w.inter, f,
-                 1, nullptr, nullptr, s);
+                 1, nullptr, nullptr, d, tpg <= nt_gu, s);
   } else {
     st = grouped(wg, nullptr, E, ggu, f, nt_gu, 1, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiCompact,
-                 w.fallback_g, f, 0, nullptr, nullptr, s);
+                 w.fallback_g, f, 0, nullptr, nullptr, d, tpg <= nt_gu, s);
     if (st == SMY_OK)
       st = grouped(wu, nullptr, E, ggu, f, nt_gu, 1, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiCompact,
-                   w.fallback_u, f, 0, nullptr, nullptr, s);
+                   w.fallback_u, f, 0, nullptr, nullptr, d, tpg <= nt_gu, s);
     if (st == SMY_OK) st = silu_mul_launch(w.fallback_g, w.fallback_u, Tk, f, w.inter, s);
   }
   if (st != SMY_OK) return st;
   record_phase(3, s);
   // down: out[sel[t]] += gw[t] * Wd inter[t]
   st = grouped(wd, nullptr, E, gdn, d, nt_dn, 1, w.inter, f, Tk, nullptr, w.offsets, prefix_dn, max_dn, kEpiScatter,
-               out, d, 0, w.sel, w.gw, s);
+               out, d, 0, w.sel, w.gw, f, tpg <= nt_dn, s);
   if (st != SMY_OK) return st;
   record_phase(4, s);
 
@@ -227,6 +230,9 @@ smy_status moe_layer(const smy_moe_config* c, const smy_weight* experts, const s
       a.out = o;
       a.ldo = ldo;
       a.max_tiles = g.m_tiles * (int)((T + nt - 1) / nt);
+      a.weights_stream = T <= nt;
+      smy_status st2 = make_x_tmap(&a.tmap_x, xx, ldx, T, ldx, nt);
+      if (st2 != SMY_OK) return st2;
       return ssmm_launch(a, nt, nw, g.ms, g.rep, s);
     };
     if (fused) {

@@ -4,27 +4,33 @@
 // C[t, o] = sum_k W[o, k] * x[sel[t], k]     (Alg. 1)
 //
 // B200 design:
-//  * one CTA = one tile of 128 compressed weight rows (TMEM lanes) x NT
-//    selected tokens, for one expert (grouped launches decode the expert from
-//    a device-side tile prefix -- no host sync on routing counts);
-//  * warp 0 streams the pre-packed weight image (A smem image | E metadata
-//    TMEM image | index bit-planes) with one cp.async.bulk per stage/weight;
-//  * warps 2-7 gather the routed token rows x[sel[t]] straight from the
-//    token-major activations into a 128B-swizzled K-major tile with cp.async
-//    (the paper's SEL gather; no permuted copy of x is ever made);
-//  * warp 1 (one lane) copies E smem->TMEM (tcgen05.cp) and issues
-//    tcgen05.mma.sp (bf16, K=32 = one V=32 sub-row window per MMA);
-//  * the data-stationary remap of §4.3 ("the output of the SpTC
-//    must be remapped to different rows ... according to the indices") is done
-//    by the tensor core itself: one TMEM accumulator per in-block sub-row slot
-//    p < M, and every MMA carries a 128-bit disable_output_lane mask built from
-//    the index bit-planes so lane r only accumulates into slot idx[r][j];
-//  * warps 4-7 zero the accumulators, then run the fused epilogue
-//    (compact store / SiLU*up -> bf16 / routing-weight scale + scatter-add,
-//    P:337) straight from TMEM (tcgen05.ld).
+//  * persistent CTAs (one per SM) walk a static tile schedule; a tile is 128
+//    compressed weight rows (TMEM lanes) x NT selected tokens of one expert.
+//    Grouped (MoE) launches decode the expert from a device-side tile prefix
+//    written by the routing kernels -- the host never sees the counts;
+//  * warp 4 is the producer: one cp.async.bulk per stage and weight streams the
+//    pre-packed weight image (A smem image | E metadata TMEM image | index
+//    bit-planes).  Token rows: when the expert's rows are contiguous (the
+//    compact intermediate feeding down_proj -- the paper's compressed output
+//    layout) warp 4 also issues one 2D TMA tile per stage; when they are
+//    selected through SEL (gate/up) warps 6-9 gather x[sel[t]] with
+//    cp.async straight from the token-major activations into the 128B-swizzled
+//    K-major tile -- x is never permuted or copied (measured on B200: cp.async
+//    sustains ~27 B/clk/SM of 128-B row gathers vs ~8 for tile::gather4,
+//    probes/gather_bench.cu);
+//  * warp 5 (one lane) copies E smem->TMEM (tcgen05.cp) and issues
+//    tcgen05.mma.sp (bf16 -> fp32, K=32 = one V=32 sub-row window per MMA);
+//  * the data-stationary remap of §4.3 ("the output of the SpTC must
+//    be remapped to different rows ... according to the indices matrix") is done
+//    by the tensor core: one TMEM accumulator per in-block sub-row slot p < M;
+//    every MMA carries a 128-bit disable_output_lane mask built from the index
+//    bit-planes so lane r only accumulates into slot idx[r][j];
+//  * warps 0-3 run the fused epilogue straight from TMEM (compact store /
+//    SiLU(gate)*up -> bf16 / routing-weight scale + scatter-add) and then
+//    re-zero the accumulators for the next tile, while the producer is already
+//    streaming that tile's operands.
+#include <cuda.h>
 #include <cuda_bf16.h>
-
-#include <cstdio>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -44,20 +50,60 @@ struct Cfg {
                                    : kColsNeeded <= 128 ? 128
                                    : kColsNeeded <= 256 ? 256
                                                         : 512;
-  static constexpr int kAux = 2048;                        // barriers + row ids
+  static constexpr int kAux = 2048;                        // barriers + gather row ids
   static constexpr int kSmemCap = 232448 - 1024 - kAux;
   static constexpr int kStagesRaw = kSmemCap / kStageBytes;
-  static constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
+  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + kAux;
   static constexpr int kPlanes = MS == 1 ? 0 : MS == 2 ? 1 : MS == 4 ? 2 : MS == 8 ? 3 : 4;
-  static constexpr int kLag = kStages >= 3 ? 2 : 1;
   static_assert(kColsNeeded <= 512, "TMEM budget");
   static_assert(kStages >= 2, "smem budget");
   static_assert(NT % 16 == 0 && NT >= 16 && NT <= 256, "UMMA N");
 };
 
-constexpr int kThreads = 256;
-constexpr int kLoaderThreads = 192;  // warps 2..7
+constexpr int kThreads = 320;  // warps 0-3 epilogue, 4 producer, 5 MMA, 6-9 gather
+constexpr int kGatherThreads = 128;
+
+struct TileInfo {
+  int g, m_tile, t0, n_local, row0;
+};
+
+// Static schedule: tile index -> (expert, m_tile, n_tile).  n is the fastest
+// index so CTAs running concurrently share the weight tile in L2.
+__device__ __forceinline__ bool decode_tile(const SsmmArgs& a, int nt, int tile, TileInfo& ti) {
+  int g = 0, local = tile;
+  if (a.tile_prefix != nullptr) {
+    if (tile >= a.tile_prefix[a.num_groups]) return false;
+    int lo = 0, hi = a.num_groups - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (a.tile_prefix[mid] <= tile) lo = mid; else hi = mid - 1;
+    }
+    g = lo;
+    local = tile - a.tile_prefix[g];
+  } else if (tile >= a.max_tiles) {
+    return false;
+  }
+  const int row0 = a.offsets ? a.offsets[g] : 0;
+  const int n_g = a.offsets ? a.offsets[g + 1] - row0 : a.n_sel;
+  const int n_tiles = (n_g + nt - 1) / nt;
+  ti.g = g;
+  ti.m_tile = local / n_tiles;
+  const int n_tile = local % n_tiles;
+  ti.t0 = n_tile * nt;
+  ti.n_local = min(nt, n_g - ti.t0);
+  ti.row0 = row0;
+  return true;
+}
+
+__device__ __forceinline__ void tma_tile2d(void* dst, const CUtensorMap* map, int col, int row, uint64_t* bar,
+                                           uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(col), "r"(row), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 
 template <int NT, int NW, int MS, int REP>
 __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant__ SsmmArgs a) {
@@ -69,43 +115,22 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
   uint64_t* full = reinterpret_cast<uint64_t*>(aux);
   uint64_t* empty = full + S;
   uint64_t* acc_full = empty + S;
-  uint64_t* tmem_ready = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_ready + 1);
-  int32_t* rows = reinterpret_cast<int32_t*>(aux + 1024);
-
-  // ---- tile -> (group, m_tile, n_tile)
-  int g = 0, local = blockIdx.x;
-  if (a.tile_prefix != nullptr) {
-    if (local >= a.tile_prefix[a.num_groups]) return;
-    int lo = 0, hi = a.num_groups - 1;
-    while (lo < hi) {  // last g with prefix[g] <= local
-      int mid = (lo + hi + 1) >> 1;
-      if (a.tile_prefix[mid] <= local) lo = mid; else hi = mid - 1;
-    }
-    g = lo;
-    local -= a.tile_prefix[g];
-  }
-  const int m_tile = local % a.m_tiles;
-  const int n_tile = local / a.m_tiles;
-  const int row0 = a.offsets ? a.offsets[g] : 0;
-  const int n_g = a.offsets ? a.offsets[g + 1] - row0 : a.n_sel;
-  const int t0 = n_tile * NT;
-  const int n_local = min(NT, n_g - t0);
-  if (n_local <= 0) return;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  int32_t* rows = reinterpret_cast<int32_t*>(aux + 1024);  // gather row ids of the current tile
+  const bool gather = a.sel_in != nullptr;
 
   const int warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1 + kLoaderThreads / 32);
+      mbar_init(&full[s], gather ? 1 + kGatherThreads / 32 : 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(acc_full, 1);
-    mbar_init(tmem_ready, 4);
+    mbar_init(acc_empty, 4);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
-  for (int i = threadIdx.x; i < NT; i += kThreads)
-    rows[i] = (i < n_local) ? (a.sel_in ? a.sel_in[row0 + t0 + i] : row0 + t0 + i) : -1;
+  if (warp == 5) tmem_alloc(tmem_slot, C::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -113,122 +138,144 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
   auto wsm = [&](int st, int w) { return smem + st * C::kStageBytes + w * C::kWStride; };
   auto bsm = [&](int st) { return smem + st * C::kStageBytes + NW * C::kWStride; };
   const int ks = a.k_stages;
+  const int tile0 = blockIdx.x, tstep = gridDim.x;
 
-  if (warp == 0) {
-    // ======================= weight-image producer =======================
+  if (warp == 4) {
+    // ========== producer: weight image (bulk) + contiguous token tile (2D TMA) ==========
     if (lane == 0) {
-      const uint32_t bytes = kABytes + kEBytes + 64 * C::kPlanes;
-      const uint64_t pol = policy_evict_last();
-      const uint8_t* src0 = a.img0[g] + (size_t)m_tile * ks * a.block;
-      const uint8_t* src1 = NW == 2 ? a.img1[g] + (size_t)m_tile * ks * a.block : nullptr;
-      for (int it = 0; it < ks; ++it) {
-        const int st = it % S;
-        mbar_wait(&empty[st], ((it / S) & 1) ^ 1);
-        mbar_arrive_expect_tx(&full[st], NW * bytes);
-        bulk_g2s(wsm(st, 0), src0 + (size_t)it * a.block, bytes, &full[st], pol);
-        if (NW == 2) bulk_g2s(wsm(st, 1), src1 + (size_t)it * a.block, bytes, &full[st], pol);
+      const uint32_t wbytes = kABytes + kEBytes + 64 * C::kPlanes;
+      const uint32_t stage_bytes = NW * wbytes + (gather ? 0u : (uint32_t)C::kBBytes);
+      const uint64_t pol_w = a.weights_stream ? policy_evict_first() : policy_evict_normal();
+      const uint64_t pol_x = policy_evict_last();
+      uint32_t it = 0;
+      TileInfo ti;
+      for (int tile = tile0; decode_tile(a, NT, tile, ti); tile += tstep) {
+        const uint8_t* src0 = a.img0[ti.g] + (size_t)ti.m_tile * ks * a.block;
+        const uint8_t* src1 = NW == 2 ? a.img1[ti.g] + (size_t)ti.m_tile * ks * a.block : nullptr;
+        const int xrow = ti.row0 + ti.t0;
+        for (int k = 0; k < ks; ++k, ++it) {
+          const int st = it % S;
+          mbar_wait(&empty[st], ((it / S) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[st], stage_bytes);
+          bulk_g2s(wsm(st, 0), src0 + (size_t)k * a.block, wbytes, &full[st], pol_w);
+          if (NW == 2) bulk_g2s(wsm(st, 1), src1 + (size_t)k * a.block, wbytes, &full[st], pol_w);
+          if (!gather) {
+#pragma unroll
+            for (int atom = 0; atom < 2 / REP; ++atom)
+              tma_tile2d(bsm(st) + atom * (NT * 128), &a.tmap_x, k * (128 / REP) + atom * 64, xrow, &full[st], pol_x);
+          }
+        }
       }
     }
-  } else if (warp == 1) {
-    // ============================ MMA issuer =============================
+  } else if (warp == 5) {
+    // ================================ MMA issuer ================================
     if (lane == 0) {
       constexpr uint32_t idesc = (1u << 2) | (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NT >> 3) << 17) |
                                  ((uint32_t)(128 >> 4) << 24);
-      mbar_wait(tmem_ready, 0);
-      tc_fence_after();
-      for (int it = 0; it < ks; ++it) {
-        const int st = it % S;
-        mbar_wait(&full[st], (it / S) & 1);
+      uint32_t it = 0, tcount = 0;
+      TileInfo ti;
+      for (int tile = tile0; decode_tile(a, NT, tile, ti); tile += tstep, ++tcount) {
+        mbar_wait(acc_empty, tcount & 1);  // accumulators drained and re-zeroed
         tc_fence_after();
+        for (int k = 0; k < ks; ++k, ++it) {
+          const int st = it % S;
+          mbar_wait(&full[st], (it / S) & 1);
+          tc_fence_after();
 #pragma unroll
-        for (int w = 0; w < NW; ++w)
-          tc_cp_128x128b(tmem + C::kECol + 4 * w, desc_interleave(smem_u32(wsm(st, w) + kABytes)));
+          for (int w = 0; w < NW; ++w)
+            tc_cp_128x128b(tmem + C::kECol + 4 * w, desc_interleave(smem_u32(wsm(st, w) + kABytes)));
 #pragma unroll
-        for (int kb = 0; kb < 4; ++kb) {
-          const int e0 = (kb / REP) * 32;  // first B element of this K=32 window
-          const uint64_t bdesc =
-              desc_sw128(smem_u32(bsm(st)) + (e0 / 64) * (NT * 128) + (e0 % 64) * 2);
+          for (int kb = 0; kb < 4; ++kb) {
+            const int e0 = (kb / REP) * 32;  // first B element of this K=32 window
+            const uint64_t bdesc = desc_sw128(smem_u32(bsm(st)) + (e0 / 64) * (NT * 128) + (e0 % 64) * 2);
 #pragma unroll
-          for (int w = 0; w < NW; ++w) {
-            const uint64_t adesc = desc_sw128(smem_u32(wsm(st, w)) + kb * 32);
-            uint32_t pl[C::kPlanes > 0 ? C::kPlanes : 1][4];
+            for (int w = 0; w < NW; ++w) {
+              const uint64_t adesc = desc_sw128(smem_u32(wsm(st, w)) + kb * 32);
+              uint32_t pl[C::kPlanes > 0 ? C::kPlanes : 1][4];
 #pragma unroll
-            for (int b = 0; b < C::kPlanes; ++b) {
-              const uint4 v = *reinterpret_cast<const uint4*>(wsm(st, w) + kABytes + kEBytes + (kb * C::kPlanes + b) * 16);
-              pl[b][0] = v.x; pl[b][1] = v.y; pl[b][2] = v.z; pl[b][3] = v.w;
-            }
-#pragma unroll
-            for (int p = 0; p < MS; ++p) {
-              uint32_t mask[4];
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                uint32_t en = 0xffffffffu;
-#pragma unroll
-                for (int b = 0; b < C::kPlanes; ++b) en &= ((p >> b) & 1) ? pl[b][q] : ~pl[b][q];
-                mask[q] = MS == 1 ? 0u : ~en;
+              for (int b = 0; b < C::kPlanes; ++b) {
+                const uint4 v =
+                    *reinterpret_cast<const uint4*>(wsm(st, w) + kABytes + kEBytes + (kb * C::kPlanes + b) * 16);
+                pl[b][0] = v.x; pl[b][1] = v.y; pl[b][2] = v.z; pl[b][3] = v.w;
               }
-              // metadata column of this K=32 window: even part in the address, the
-              // odd bit in idesc.sparse_id2 (bits [0,2))
-              tc_mma_sp(tmem + (w * MS + p) * NT, adesc, bdesc, idesc | (uint32_t)(kb & 1), 1u, mask,
-                        tmem + C::kECol + 4 * w + (kb & 2));
+#pragma unroll
+              for (int p = 0; p < MS; ++p) {
+                uint32_t mask[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  uint32_t en = 0xffffffffu;
+#pragma unroll
+                  for (int b = 0; b < C::kPlanes; ++b) en &= ((p >> b) & 1) ? pl[b][q] : ~pl[b][q];
+                  mask[q] = MS == 1 ? 0u : ~en;
+                }
+                // metadata column of this K=32 window: even part in the address,
+                // the odd bit in idesc.sparse_id2 (bits [0,2))
+                tc_mma_sp(tmem + (w * MS + p) * NT, adesc, bdesc, idesc | (uint32_t)(kb & 1), 1u, mask,
+                          tmem + C::kECol + 4 * w + (kb & 2));
+              }
             }
           }
+          tc_commit(&empty[st]);
         }
-        tc_commit(&empty[st]);
+        tc_commit(acc_full);
       }
-      tc_commit(acc_full);
+    }
+  } else if (warp >= 6) {
+    // ================== SEL gather of token rows (warps 6-9, cp.async) ==================
+    if (gather) {
+      const int tb = threadIdx.x - 6 * 32;
+      constexpr int CPR = 16 / REP;  // 16-byte chunks per token row per stage
+      constexpr int CHUNKS = NT * CPR;
+      uint32_t it = 0;
+      TileInfo ti;
+      for (int tile = tile0; decode_tile(a, NT, tile, ti); tile += tstep) {
+        named_bar_sync(1, kGatherThreads);  // previous tile's rows no longer read
+        for (int i = tb; i < NT; i += kGatherThreads)
+          rows[i] = i < ti.n_local ? a.sel_in[ti.row0 + ti.t0 + i] : -1;
+        named_bar_sync(1, kGatherThreads);
+        for (int k = 0; k < ks; ++k, ++it) {
+          const int st = it % S;
+          mbar_wait(&empty[st], ((it / S) & 1) ^ 1);
+          const int64_t kcol0 = (int64_t)k * (128 / REP);
+          uint8_t* bs = bsm(st);
+          for (int idx = tb; idx < CHUNKS; idx += kGatherThreads) {
+            const int row = idx / CPR, ch = idx % CPR;
+            const int atom = ch >> 3, c8 = ch & 7;
+            const int rid = rows[row];
+            const uint16_t* src = rid >= 0 ? a.x + (int64_t)rid * a.ldx + kcol0 + ch * 8 : a.x;
+            uint8_t* dst = bs + atom * (NT * 128) + (row >> 3) * 1024 + (row & 7) * 128 + ((c8 ^ (row & 7)) << 4);
+            cp_async16(dst, src, rid >= 0 ? 16u : 0u);
+          }
+          cp_async_commit();
+          cp_async_wait<0>();
+          fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[st]);
+        }
+      }
     }
   } else {
-    // ============== token gather (warps 2-7) + epilogue (warps 4-7) ==============
-    const int tb = threadIdx.x - 64;
-    if (warp >= 4) {
-      const uint32_t lane_base = (uint32_t)(32 * (warp - 4)) << 16;
+    // ============ epilogue (warps 0-3): TMEM -> fused epilogue -> re-zero ============
+    const int q = warp;  // TMEM lane quarter
+    const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+    const int nf = a.n_fmt;
+    auto zero_acc = [&]() {
       for (int c = 0; c < C::kAccCols; c += 16) tmem_st16_zero(tmem + lane_base + c);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tmem_ready);
-    }
-    constexpr int CPR = 16 / REP;  // 16-byte chunks per token row per stage
-    constexpr int CHUNKS = NT * CPR;
-    constexpr int LAG = C::kLag;
-    for (int it = 0; it < ks; ++it) {
-      const int st = it % S;
-      mbar_wait(&empty[st], ((it / S) & 1) ^ 1);
-      const int64_t kcol0 = (int64_t)it * (128 / REP);
-      uint8_t* bs = bsm(st);
-      for (int idx = tb; idx < CHUNKS; idx += kLoaderThreads) {
-        const int row = idx / CPR, ch = idx % CPR;
-        const int atom = ch >> 3, c8 = ch & 7;
-        const int rid = rows[row];
-        const uint16_t* src = rid >= 0 ? a.x + (int64_t)rid * a.ldx + kcol0 + ch * 8 : a.x;
-        uint8_t* dst = bs + atom * (NT * 128) + (row >> 3) * 1024 + (row & 7) * 128 + ((c8 ^ (row & 7)) << 4);
-        cp_async16(dst, src, rid >= 0 ? 16u : 0u);
-      }
-      cp_async_commit();
-      if (it >= LAG) {
-        cp_async_wait<LAG>();
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[(it - LAG) % S]);
-      }
-    }
-    cp_async_wait<0>();
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0)
-      for (int it = ks - LAG < 0 ? 0 : ks - LAG; it < ks; ++it) mbar_arrive(&full[it % S]);
-
-    if (warp >= 4) {
-      // =============================== epilogue ===============================
-      const int q = warp - 4;
-      const uint32_t lane_base = (uint32_t)(32 * q) << 16;
-      const int cr = m_tile * kTileM + 32 * q + lane;  // compressed row of this lane
+      if (lane == 0) mbar_arrive(acc_empty);
+    };
+    zero_acc();
+    uint32_t tcount = 0;
+    TileInfo ti;
+    for (int tile = tile0; decode_tile(a, NT, tile, ti); tile += tstep, ++tcount) {
+      const int cr = ti.m_tile * kTileM + 32 * q + lane;  // compressed row of this lane
       const bool valid = cr < a.R;
-      const int nf = a.n_fmt;
-      mbar_wait(acc_full, 0);
+      const int grp = cr / nf;
+      mbar_wait(acc_full, tcount & 1);
       tc_fence_after();
-      for (int c0 = 0; c0 < n_local; c0 += 16) {
+      for (int c0 = 0; c0 < ti.n_local; c0 += 16) {
         float v[NW][MS][16];
 #pragma unroll
         for (int w = 0; w < NW; ++w)
@@ -245,12 +292,11 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
                 for (int off = nf >> 1; off > 0; off >>= 1) v[w][p][j] += __shfl_xor_sync(0xffffffffu, v[w][p][j], off);
         }
         if (!valid) continue;
-        const int grp = cr / nf;
-        const int jmax = min(16, n_local - c0);
+        const int jmax = min(16, ti.n_local - c0);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           if (j >= jmax) break;
-          const int r = row0 + t0 + c0 + j;  // compact row of this token
+          const int r = ti.row0 + ti.t0 + c0 + j;  // compact row of this token
           if (a.epi == kEpiScatter) {
             const int dst = a.sel_out ? a.sel_out[r] : r;
             const float s = a.scale ? a.scale[r] : 1.f;
@@ -266,21 +312,30 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
             }
           } else if (NW == 2) {  // SiLU(gate) * up -> bf16
             uint16_t* o = static_cast<uint16_t*>(a.out) + (int64_t)r * a.ldo;
+            if (MS == 2 && nf == 1) {
+              float act[2];
 #pragma unroll
-            for (int p = 0; p < MS; ++p) {
-              if (MS > 1 && nf > 1 && (p % nf) != (cr % nf)) continue;
-              const float gv = v[0][p][j], uv = v[NW - 1][p][j];
-              const float act = gv / (1.f + expf(-gv)) * uv;
-              const int orow = MS == 1 ? cr : grp * MS + p;
-              o[orow] = __bfloat16_as_ushort(__float2bfloat16_rn(act));
+              for (int p = 0; p < 2; ++p) {
+                const float gv = v[0][p % MS][j], uv = v[NW - 1][p % MS][j];
+                act[p] = __fdividef(gv, 1.f + __expf(-gv)) * uv;
+              }
+              const __nv_bfloat162 h = __floats2bfloat162_rn(act[0], act[1]);
+              *reinterpret_cast<__nv_bfloat162*>(o + 2 * grp) = h;
+            } else {
+#pragma unroll
+              for (int p = 0; p < MS; ++p) {
+                if (MS > 1 && nf > 1 && (p % nf) != (cr % nf)) continue;
+                const float gv = v[0][p][j], uv = v[NW - 1][p][j];
+                const float act = __fdividef(gv, 1.f + __expf(-gv)) * uv;
+                o[MS == 1 ? cr : grp * MS + p] = __bfloat16_as_ushort(__float2bfloat16_rn(act));
+              }
             }
           } else if (a.out_bf16) {
             uint16_t* o = static_cast<uint16_t*>(a.out) + (int64_t)r * a.ldo;
 #pragma unroll
             for (int p = 0; p < MS; ++p) {
               if (MS > 1 && nf > 1 && (p % nf) != (cr % nf)) continue;
-              const int orow = MS == 1 ? cr : grp * MS + p;
-              o[orow] = __bfloat16_as_ushort(__float2bfloat16_rn(v[0][p][j]));
+              o[MS == 1 ? cr : grp * MS + p] = __bfloat16_as_ushort(__float2bfloat16_rn(v[0][p][j]));
             }
           } else {
             float* o = static_cast<float*>(a.out) + (int64_t)r * a.ldo;
@@ -296,12 +351,14 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
           }
         }
       }
+      tc_fence_before();
+      zero_acc();  // hand the accumulators back for the next tile
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem, C::kTmemCols);
+  if (warp == 5) tmem_dealloc(tmem, C::kTmemCols);
 }
 
 // ------------------------------------------------------------------ host side
@@ -310,14 +367,19 @@ template <int NT, int NW, int MS, int REP>
 smy_status launch_t(const SsmmArgs& a, cudaStream_t s) {
   using C = Cfg<NT, NW, MS, REP>;
   static bool configured = false;
+  static int num_sms = 0;
   auto kern = ssmm_kernel<NT, NW, MS, REP>;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return cuda_status(e);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     configured = true;
   }
   if (a.max_tiles <= 0) return SMY_OK;
-  kern<<<a.max_tiles, kThreads, C::kSmemBytes, s>>>(a);
+  const int grid = a.max_tiles < num_sms ? a.max_tiles : num_sms;
+  kern<<<grid, kThreads, C::kSmemBytes, s>>>(a);
   count_launch();
   return cuda_status(cudaGetLastError());
 }
