@@ -197,6 +197,8 @@ smy_status samoyeds_ssmm(const smy_weight* w, const smy_weight* w2, const void* 
   a.scale = scale;
   a.max_tiles = g.m_tiles * ((n_sel + nt - 1) / nt);
   a.weights_stream = n_sel <= nt;
+  a.k_splits = a.epi == kEpiScatter ? ssmm_pick_ksplit(a.max_tiles, g.k_stages) : 1;
+  a.max_tiles *= a.k_splits;
   if ((st = make_x_tmap(&a.tmap_x, x_bf16, w->d.cols, x_rows, ldx, nt)) != SMY_OK) return st;
   return ssmm_launch(a, nt, nw, g.ms, g.rep, static_cast<cudaStream_t>(stream));
 }

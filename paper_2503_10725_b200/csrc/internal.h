@@ -51,7 +51,11 @@ struct SsmmArgs {
   const float* scale;      // scatter scale, NULL = 1
   int max_tiles;           // tile count (single group) / upper bound (grouped)
   int weights_stream;      // 1: weights read once per call (decode) -> L2 evict_first
+  int k_splits;            // >1: split K across tiles (SCATTER epilogue only; partial sums add)
 };
+
+// K-split count for a scatter-add launch with `tiles` (expert, m, n) tiles.
+int ssmm_pick_ksplit(int64_t tiles, int k_stages);
 
 // Tensor map over a token-major bf16 activation matrix [rows x cols] (ld elements):
 // boxes of 64 elements x box_rows rows, 128-byte swizzle (the UMMA K-major atom).

@@ -95,7 +95,7 @@ static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* 
                           int m_out, int nt, int nw, const uint16_t* x, int64_t ldx, int64_t x_rows,
                           const int32_t* sel_in, const int32_t* offsets, const int32_t* prefix, int max_tiles,
                           int epi, void* out, int64_t ldo, int out_bf16, const int32_t* sel_out,
-                          const float* scale, int64_t k_cols, int stream_w, cudaStream_t s) {
+                          const float* scale, int64_t k_cols, int stream_w, int k_splits, cudaStream_t s) {
   SsmmArgs a;
   memset(&a, 0, sizeof(a));
   for (int e = 0; e < groups; ++e) {
@@ -124,8 +124,9 @@ static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* 
   a.ldo = ldo;
   a.sel_out = sel_out;
   a.scale = scale;
-  a.max_tiles = max_tiles;
+  a.max_tiles = max_tiles * k_splits;
   a.weights_stream = stream_w;
+  a.k_splits = k_splits;
   smy_status st = make_x_tmap(&a.tmap_x, x, k_cols, x_rows, ldx, nt);
   if (st != SMY_OK) return st;
   return ssmm_launch(a, nt, nw, g.ms, g.rep, s);
@@ -148,8 +149,12 @@ smy_status moe_layer(const smy_moe_config* c, const smy_weight* experts, const s
   const int64_t tpg = E ? (T * k + E - 1) / E : 0;
   const int nt_gu = ssmm_pick_nt(fused ? 2 : 1, ggu.ms, ggu.rep, tpg);
   const int nt_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, tpg);
+  // expected down tiles -> K split (the scatter-add epilogue makes partial sums free)
+  const int64_t act = E < T * k ? E : T * k;
+  const int ks_dn = ssmm_pick_ksplit((int64_t)gdn.m_tiles * act * ((tpg + nt_dn - 1) / (nt_dn > 0 ? nt_dn : 1)),
+                                     gdn.k_stages);
   const int nts[2] = {nt_gu, nt_dn};
-  const int mts[2] = {ggu.m_tiles, gdn.m_tiles};
+  const int mts[2] = {ggu.m_tiles, gdn.m_tiles * ks_dn};
   int32_t* prefix_gu = w.prefix;
   int32_t* prefix_dn = w.prefix + (E + 1);
 
@@ -182,20 +187,20 @@ smy_status moe_layer(const smy_moe_config* c, const smy_weight* experts, const s
   // gate/up: H = Wg x[SEL], U = Wu x[SEL], inter = bf16(silu(H) * U)
   if (fused) {
     st = grouped(wg, wu, E, ggu, f, nt_gu, 2, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiSiluMul, w.inter, f,
-                 1, nullptr, nullptr, d, tpg <= nt_gu, s);
+                 1, nullptr, nullptr, d, tpg <= nt_gu, 1, s);
   } else {
     st = grouped(wg, nullptr, E, ggu, f, nt_gu, 1, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiCompact,
-                 w.fallback_g, f, 0, nullptr, nullptr, d, tpg <= nt_gu, s);
+                 w.fallback_g, f, 0, nullptr, nullptr, d, tpg <= nt_gu, 1, s);
     if (st == SMY_OK)
       st = grouped(wu, nullptr, E, ggu, f, nt_gu, 1, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiCompact,
-                   w.fallback_u, f, 0, nullptr, nullptr, d, tpg <= nt_gu, s);
+                   w.fallback_u, f, 0, nullptr, nullptr, d, tpg <= nt_gu, 1, s);
     if (st == SMY_OK) st = silu_mul_launch(w.fallback_g, w.fallback_u, Tk, f, w.inter, s);
   }
   if (st != SMY_OK) return st;
   record_phase(3, s);
   // down: out[sel[t]] += gw[t] * Wd inter[t]
   st = grouped(wd, nullptr, E, gdn, d, nt_dn, 1, w.inter, f, Tk, nullptr, w.offsets, prefix_dn, max_dn, kEpiScatter,
-               out, d, 0, w.sel, w.gw, f, tpg <= nt_dn, s);
+               out, d, 0, w.sel, w.gw, f, tpg <= nt_dn, ks_dn, s);
   if (st != SMY_OK) return st;
   record_phase(4, s);
 
@@ -231,6 +236,8 @@ smy_status moe_layer(const smy_moe_config* c, const smy_weight* experts, const s
       a.ldo = ldo;
       a.max_tiles = g.m_tiles * (int)((T + nt - 1) / nt);
       a.weights_stream = T <= nt;
+      a.k_splits = epi == kEpiScatter ? ssmm_pick_ksplit(a.max_tiles, g.k_stages) : 1;
+      a.max_tiles *= a.k_splits;
       smy_status st2 = make_x_tmap(&a.tmap_x, xx, ldx, T, ldx, nt);
       if (st2 != SMY_OK) return st2;
       return ssmm_launch(a, nt, nw, g.ms, g.rep, s);

@@ -73,6 +73,15 @@ int ssmm_pick_nt(int nw, int ms, int rep, int64_t tpg) {
   return best > 0 ? best : largest;
 }
 
+int ssmm_pick_ksplit(int64_t tiles, int k_stages) {
+  // aim for >= 4 tiles per SM while keeping >= 8 K-stages per tile
+  const int64_t want = 4 * 148;
+  if (tiles >= want || k_stages < 16) return 1;
+  int64_t ks = (want + tiles - 1) / tiles;
+  if (ks > k_stages / 8) ks = k_stages / 8;
+  return ks < 1 ? 1 : (int)ks;
+}
+
 smy_status ssmm_launch(const SsmmArgs& a, int nt, int nw, int ms, int rep, cudaStream_t s) {
   for (const Entry& e : kTable)
     if (e.nt == nt && e.nw == nw && e.ms == ms && e.rep == rep) return e.fn(a, s);

@@ -65,7 +65,7 @@ constexpr int kThreads = 320;  // warps 0-3 epilogue, 4 producer, 5 MMA, 6-9 gat
 constexpr int kGatherThreads = 128;
 
 struct TileInfo {
-  int g, m_tile, t0, n_local, row0;
+  int g, m_tile, t0, n_local, row0, k0, k1;  // k-stage range [k0, k1)
 };
 
 // Static schedule: tile index -> (expert, m_tile, n_tile).  n is the fastest
@@ -88,8 +88,14 @@ __device__ __forceinline__ bool decode_tile(const SsmmArgs& a, int nt, int tile,
   const int n_g = a.offsets ? a.offsets[g + 1] - row0 : a.n_sel;
   const int n_tiles = (n_g + nt - 1) / nt;
   ti.g = g;
-  ti.m_tile = local / n_tiles;
+  const int mk = local / n_tiles;              // (m_tile, k_split), k_split fastest
   const int n_tile = local % n_tiles;
+  const int ksplits = a.k_splits > 1 ? a.k_splits : 1;
+  ti.m_tile = mk / ksplits;
+  const int kspl = mk % ksplits;
+  const int per = (a.k_stages + ksplits - 1) / ksplits;
+  ti.k0 = kspl * per;
+  ti.k1 = min(a.k_stages, ti.k0 + per);
   ti.t0 = n_tile * nt;
   ti.n_local = min(nt, n_g - ti.t0);
   ti.row0 = row0;
@@ -123,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
   const int warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], gather ? 1 + kGatherThreads / 32 : 1);
+      mbar_init(&full[s], gather ? 1 + kGatherThreads : 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(acc_full, 1);
@@ -153,7 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
         const uint8_t* src0 = a.img0[ti.g] + (size_t)ti.m_tile * ks * a.block;
         const uint8_t* src1 = NW == 2 ? a.img1[ti.g] + (size_t)ti.m_tile * ks * a.block : nullptr;
         const int xrow = ti.row0 + ti.t0;
-        for (int k = 0; k < ks; ++k, ++it) {
+        for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % S;
           mbar_wait(&empty[st], ((it / S) & 1) ^ 1);
           mbar_arrive_expect_tx(&full[st], stage_bytes);
@@ -168,57 +174,63 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
       }
     }
   } else if (warp == 5) {
-    // ================================ MMA issuer ================================
-    if (lane == 0) {
-      constexpr uint32_t idesc = (1u << 2) | (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NT >> 3) << 17) |
-                                 ((uint32_t)(128 >> 4) << 24);
-      uint32_t it = 0, tcount = 0;
-      TileInfo ti;
-      for (int tile = tile0; decode_tile(a, NT, tile, ti); tile += tstep, ++tcount) {
-        mbar_wait(acc_empty, tcount & 1);  // accumulators drained and re-zeroed
+    // ======================= MMA issuer (whole warp, one elected lane) =======================
+    constexpr uint32_t idesc = (1u << 2) | (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NT >> 3) << 17) |
+                               ((uint32_t)(128 >> 4) << 24);
+    const uint32_t smem_base = smem_u32(smem);
+    uint32_t it = 0, tcount = 0;
+    TileInfo ti;
+    for (int tile = tile0; decode_tile(a, NT, tile, ti); tile += tstep, ++tcount) {
+      mbar_wait(acc_empty, tcount & 1);  // accumulators drained and re-zeroed
+      tc_fence_after();
+      for (int k = ti.k0; k < ti.k1; ++k, ++it) {
+        const int st = it % S;
+        mbar_wait(&full[st], (it / S) & 1);
         tc_fence_after();
-        for (int k = 0; k < ks; ++k, ++it) {
-          const int st = it % S;
-          mbar_wait(&full[st], (it / S) & 1);
-          tc_fence_after();
+        const uint32_t sbase = smem_base + st * C::kStageBytes;
 #pragma unroll
-          for (int w = 0; w < NW; ++w)
-            tc_cp_128x128b(tmem + C::kECol + 4 * w, desc_interleave(smem_u32(wsm(st, w) + kABytes)));
+        for (int w = 0; w < NW; ++w) tc_cp_128x128b_elect(tmem + C::kECol + 4 * w, desc_interleave(sbase + w * C::kWStride + kABytes));
+        // index bit-planes of this stage, made explicitly warp-uniform
+        uint32_t pl[NW][4][C::kPlanes > 0 ? C::kPlanes : 1][4];
 #pragma unroll
-          for (int kb = 0; kb < 4; ++kb) {
-            const int e0 = (kb / REP) * 32;  // first B element of this K=32 window
-            const uint64_t bdesc = desc_sw128(smem_u32(bsm(st)) + (e0 / 64) * (NT * 128) + (e0 % 64) * 2);
+        for (int w = 0; w < NW; ++w)
 #pragma unroll
-            for (int w = 0; w < NW; ++w) {
-              const uint64_t adesc = desc_sw128(smem_u32(wsm(st, w)) + kb * 32);
-              uint32_t pl[C::kPlanes > 0 ? C::kPlanes : 1][4];
+          for (int kb = 0; kb < 4; ++kb)
 #pragma unroll
-              for (int b = 0; b < C::kPlanes; ++b) {
-                const uint4 v =
-                    *reinterpret_cast<const uint4*>(wsm(st, w) + kABytes + kEBytes + (kb * C::kPlanes + b) * 16);
-                pl[b][0] = v.x; pl[b][1] = v.y; pl[b][2] = v.z; pl[b][3] = v.w;
+            for (int b = 0; b < C::kPlanes; ++b) {
+              const uint4 v = *reinterpret_cast<const uint4*>(wsm(st, w) + kABytes + kEBytes + (kb * C::kPlanes + b) * 16);
+              pl[w][kb][b][0] = __shfl_sync(0xffffffffu, v.x, 0);
+              pl[w][kb][b][1] = __shfl_sync(0xffffffffu, v.y, 0);
+              pl[w][kb][b][2] = __shfl_sync(0xffffffffu, v.z, 0);
+              pl[w][kb][b][3] = __shfl_sync(0xffffffffu, v.w, 0);
+            }
+#pragma unroll
+        for (int kb = 0; kb < 4; ++kb) {
+          const int e0 = (kb / REP) * 32;  // first B element of this K=32 window
+          const uint64_t bdesc = desc_sw128(sbase + NW * C::kWStride + (e0 / 64) * (NT * 128) + (e0 % 64) * 2);
+#pragma unroll
+          for (int w = 0; w < NW; ++w) {
+            const uint64_t adesc = desc_sw128(sbase + w * C::kWStride + kb * 32);
+#pragma unroll
+            for (int p = 0; p < MS; ++p) {
+              uint32_t mask[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                uint32_t en = 0xffffffffu;
+#pragma unroll
+                for (int b = 0; b < C::kPlanes; ++b) en &= ((p >> b) & 1) ? pl[w][kb][b][q] : ~pl[w][kb][b][q];
+                mask[q] = MS == 1 ? 0u : ~en;
               }
-#pragma unroll
-              for (int p = 0; p < MS; ++p) {
-                uint32_t mask[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  uint32_t en = 0xffffffffu;
-#pragma unroll
-                  for (int b = 0; b < C::kPlanes; ++b) en &= ((p >> b) & 1) ? pl[b][q] : ~pl[b][q];
-                  mask[q] = MS == 1 ? 0u : ~en;
-                }
-                // metadata column of this K=32 window: even part in the address,
-                // the odd bit in idesc.sparse_id2 (bits [0,2))
-                tc_mma_sp(tmem + (w * MS + p) * NT, adesc, bdesc, idesc | (uint32_t)(kb & 1), 1u, mask,
-                          tmem + C::kECol + 4 * w + (kb & 2));
-              }
+              // metadata column of this K=32 window: even part in the address,
+              // the odd bit in idesc.sparse_id2 (bits [0,2))
+              tc_mma_sp_elect(tmem + (w * MS + p) * NT, adesc, bdesc, idesc | (uint32_t)(kb & 1), mask[0], mask[1],
+                              mask[2], mask[3], tmem + C::kECol + 4 * w + (kb & 2));
             }
           }
-          tc_commit(&empty[st]);
         }
-        tc_commit(acc_full);
+        tc_commit_elect(&empty[st]);
       }
+      tc_commit_elect(acc_full);
     }
   } else if (warp >= 6) {
     // ================== SEL gather of token rows (warps 6-9, cp.async) ==================
@@ -233,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
         for (int i = tb; i < NT; i += kGatherThreads)
           rows[i] = i < ti.n_local ? a.sel_in[ti.row0 + ti.t0 + i] : -1;
         named_bar_sync(1, kGatherThreads);
-        for (int k = 0; k < ks; ++k, ++it) {
+        for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % S;
           mbar_wait(&empty[st], ((it / S) & 1) ^ 1);
           const int64_t kcol0 = (int64_t)k * (128 / REP);
@@ -246,11 +258,9 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
             uint8_t* dst = bs + atom * (NT * 128) + (row >> 3) * 1024 + (row & 7) * 128 + ((c8 ^ (row & 7)) << 4);
             cp_async16(dst, src, rid >= 0 ? 16u : 0u);
           }
-          cp_async_commit();
-          cp_async_wait<0>();
-          fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&full[st]);
+          // the barrier completes when every gather thread's copies have landed;
+          // the thread moves on to the next stage immediately
+          cp_async_mbar_arrive_noinc(&full[st]);
         }
       }
     }
