@@ -292,6 +292,42 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
+    # ---------------- decode point on the same layer (reported beside the headline)
+    dec = None
+    if args.decode_tokens and args.decode_tokens < T:
+        Td = args.decode_tokens
+        xd, lgd, outd = x[:Td], lg[:Td], out[:Td]
+        for _ in range(5):
+            layer(xd, lgd, outd)
+        torch.cuda.synchronize()
+        Kd = max(20, K)
+        dph = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(Kd)]
+        for evs in dph:
+            for ev in evs:
+                ev.record(stream)
+        torch.cuda.synchronize()
+        dh = [C_void_p_array(ev) for ev in dph]
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record(stream)
+        for s in range(Kd):
+            lib.smy_moe_set_phase_events(dh[s], 6)
+            layer(xd, lgd, outd)
+        d1.record(stream)
+        torch.cuda.synchronize()
+        lib.smy_moe_set_phase_events(None, 0)
+        dms = d0.elapsed_time(d1) / Kd
+        dpm = np.array([[dph[s][i].elapsed_time(dph[s][i + 1]) for i in range(5)] for s in range(Kd)]).mean(0)
+        ids_d = P.route(lgd, k, gating)[0].flatten().long()
+        act_d = int((torch.bincount(ids_d, minlength=E) > 0).sum().item())
+        gu_bytes = 2 * act_d * f * d * BYTES_PER_ELEM + Td * k * d * 2 + Td * k * 4 + Td * k * f * 2
+        dn_bytes = act_d * f * d * BYTES_PER_ELEM + Td * k * f * 2 + Td * k * 8 + Td * k * d * 4
+        hbm_, _, _, _ = peaks()
+        dec = {"tokens_per_gpu": Td, "tokens_per_s": Td * world / (dms * 1e-3), "ms_per_step": dms,
+               "phases_ms": {"route_compact": dpm[0], "zero_out": dpm[1], "gate_up_ssmm": dpm[2], "down_ssmm": dpm[3]},
+               "gate_up_hbm_frac": gu_bytes / (dpm[2] * 1e-3) / 1e9 / hbm_,
+               "down_hbm_frac": dn_bytes / (dpm[3] * 1e-3) / 1e9 / hbm_,
+               "layer_hbm_frac": (gu_bytes + dn_bytes) / (dms * 1e-3) / 1e9 / hbm_}
+
     # ---------------- end to end: host buffers, copies inside the timed region
     x_h = x.cpu().pin_memory()
     lg_h = lg.cpu().pin_memory()
@@ -337,6 +373,7 @@ def run_ours(args):
              "peak_source": f"2 x {src} bf16 dense burst ({bf16_burst} TF/s)"} if tensor_bound else
             {"bound": "hbm", "achieved": ach_gbs, "peak": hbm, "unit": "GB/s", "frac": ach_gbs / hbm,
              "traffic": None, "peak_source": f"{src} hbm_gbs"})
+    roof["traffic"] = ncu_traffic(model, T, "ssmm_kernel<%d, 2, 2, 1>" % nt_gate_up(T * k // E))
     roof.update({"kernel": "ssmm_kernel gate/up (NW=2, fused SiLU*up)", "per_launch_ms": ph_ms[2],
                  "algorithmic_flops": flops_gu, "algorithmic_bytes": bytes_gu,
                  "other_view": ({"achieved_gbs": ach_gbs, "hbm_frac": ach_gbs / hbm} if tensor_bound else
@@ -359,6 +396,7 @@ def run_ours(args):
         "roofline": roof,
         "e2e": {"value": T * world / (ms_e2e * 1e-3), "unit": "tokens/s",
                 "h2d_bytes_per_step": T * d * 2 + T * E * 4, "d2h_bytes_per_step": T * d * 4},
+        "decode": dec,
         "gpu_launches": int(launches),
         "clocks": clk,
     }
@@ -369,6 +407,27 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def nt_gate_up(tokens_per_expert):
+    """Token tile the library picks for the fused gate/up launch (ssmm.cu table)."""
+    for nt in (16, 32, 64, 112):
+        if nt >= tokens_per_expert:
+            return nt
+    return 112
+
+
+def ncu_traffic(model, T, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel from the
+    committed ncu --set full capture (profiles/r1_ncu_summary.json), or None."""
+    p = os.path.join(ROOT, "profiles", "r1_ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    tag = "%s_T%d: void %s" % (model, T, kernel)
+    for k, v in json.load(open(p))["kernels"].items():
+        if k.startswith(tag):
+            return v["dram_read"] + v["dram_write"]
+    return None
 
 
 def C_void_p_array(events):
@@ -386,6 +445,7 @@ def main():
     ap.add_argument("--model", default="mixtral", choices=sorted(MODELS))
     ap.add_argument("--tokens", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--decode-tokens", type=int, default=64, help="extra decode point on the same layer (0: off)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
