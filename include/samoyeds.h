@@ -159,6 +159,39 @@ SMY_API smy_status samoyeds_moe_layer(const smy_moe_config* cfg, const smy_weigh
                               const void* x_bf16, const float* logits, int64_t T, float* out, void* workspace,
                               size_t ws_bytes, smy_ep_comm* comm, void* stream);
 
+/* ------------------------------------------------ expert parallelism (EP)
+ * The layer shards over experts: rank r of P owns experts [r*E/P,(r+1)*E/P)
+ * (the paper evaluates one GPU).  One exchange step
+ * each way, done by the caller's process group (all_to_all_v, NCCL/NVLink):
+ *   samoyeds_route (all E) -> samoyeds_ep_plan -> samoyeds_ep_pack
+ *   -> [all_to_all rows + tags] -> samoyeds_moe_experts (local experts, keys =
+ *   received tags) -> [all_to_all fp32 rows back] -> samoyeds_ep_combine.
+ * ep_plan: ids/w dev [T x k] (from samoyeds_route); send_counts dev [P],
+ *   send_offsets dev [P+1]; send_sel dev [T*k] = token ids sent, ordered by
+ *   (destination rank, token id) -- each token once per destination;
+ *   tag_ids/tag_w dev [T*k x k] per send row: the local expert ids (ascending)
+ *   and gate weights the token meets at that rank, -1 / 0 padded.
+ * ep_pack: x_send[i] = x[send_sel[i]] for i < send_offsets[P] (read on the
+ *   device; max_rows bounds the buffer).
+ * moe_experts: the layer body for rows whose routing is given: keys/vals dev
+ *   [rows x k] (local expert ids, -1 = none; weights); cfg->num_experts = local
+ *   experts; out dev fp32 [rows x hidden] (overwritten).  Workspace from
+ *   smy_moe_workspace_bytes(cfg, rows).
+ * ep_combine: out[send_sel[i]] += back[i] (fp32 rows returned by the owners;
+ *   caller zeroes out first).                                               */
+SMY_API smy_status smy_ep_plan_workspace_bytes(int64_t T, int32_t k, int32_t world, size_t* bytes);
+SMY_API smy_status samoyeds_ep_plan(const int32_t* ids, const float* w, int64_t T, int32_t k, int32_t num_experts,
+                                    int32_t world, int32_t* send_counts, int32_t* send_offsets, int32_t* send_sel,
+                                    int32_t* tag_ids, float* tag_w, void* workspace, size_t ws_bytes, void* stream);
+SMY_API smy_status samoyeds_ep_pack(const void* x_bf16, int64_t ldx, int64_t hidden, const int32_t* send_offsets,
+                                    int32_t world, const int32_t* send_sel, int64_t max_rows, void* x_send,
+                                    void* stream);
+SMY_API smy_status samoyeds_moe_experts(const smy_moe_config* cfg, const smy_weight* experts, const void* x_bf16,
+                                        int64_t rows, const int32_t* keys, const float* vals, float* out,
+                                        void* workspace, size_t ws_bytes, void* stream);
+SMY_API smy_status samoyeds_ep_combine(const float* back, int64_t hidden, const int32_t* send_offsets, int32_t world,
+                                       const int32_t* send_sel, int64_t max_rows, float* out, void* stream);
+
 /* ------------------------------------------------------------ diagnostics
  * smy_moe_set_phase_events: when events != NULL (n >= 6 cudaEvent_t handles,
  * passed as void*), samoyeds_moe_layer records events[0..5] on its stream at

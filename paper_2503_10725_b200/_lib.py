@@ -54,6 +54,16 @@ SIGNATURES = {
     "samoyeds_moe_layer": (C.c_int, [C.POINTER(smy_moe_config), C.POINTER(smy_weight), C.POINTER(smy_weight),
                                      C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_size_t,
                                      C.c_void_p, C.c_void_p]),
+    "smy_ep_plan_workspace_bytes": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_size_t)]),
+    "samoyeds_ep_plan": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
+                                   C.c_void_p]),
+    "samoyeds_ep_pack": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64,
+                                   C.c_void_p, C.c_void_p]),
+    "samoyeds_moe_experts": (C.c_int, [C.POINTER(smy_moe_config), C.POINTER(smy_weight), C.c_void_p, C.c_int64,
+                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "samoyeds_ep_combine": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64,
+                                      C.c_void_p, C.c_void_p]),
     "smy_moe_set_phase_events": (C.c_int, [C.c_void_p, C.c_int]),
     "smy_launch_count": (C.c_uint64, []),
     "smy_synth_fill": (C.c_int, [C.c_uint64, C.c_int, C.c_float, C.c_int, C.c_int, C.c_int64, C.c_int64,

@@ -197,3 +197,72 @@ def synth_fill(out: torch.Tensor, seed: int, dist: int, scale: float, lo: int = 
     check(lib.smy_synth_fill(seed, dist, scale, lo, hi, idx0, out.numel(), _ptr(out), int(bf), _stream(stream)),
           "smy_synth_fill")
     return out
+
+
+# ------------------------------------------------------------ expert parallelism
+
+def ep_plan(ids: torch.Tensor, w: torch.Tensor, num_experts: int, world: int, stream=None):
+    """samoyeds_ep_plan: per-destination send order + tags (see include/samoyeds.h)."""
+    lib = _lib.load()
+    T, k = ids.shape
+    dev = ids.device
+    b = C.c_size_t()
+    check(lib.smy_ep_plan_workspace_bytes(T, k, world, C.byref(b)), "smy_ep_plan_workspace_bytes")
+    ws = torch.empty(b.value, dtype=torch.uint8, device=dev)
+    counts = torch.empty(world, dtype=torch.int32, device=dev)
+    offsets = torch.empty(world + 1, dtype=torch.int32, device=dev)
+    n = max(T * k, 1)
+    sel = torch.empty(n, dtype=torch.int32, device=dev)
+    tag_ids = torch.empty(n, k, dtype=torch.int32, device=dev)
+    tag_w = torch.empty(n, k, dtype=torch.float32, device=dev)
+    check(lib.samoyeds_ep_plan(_ptr(ids), _ptr(w), T, k, num_experts, world, _ptr(counts), _ptr(offsets), _ptr(sel),
+                               _ptr(tag_ids), _ptr(tag_w), _ptr(ws), ws.numel(), _stream(stream)), "samoyeds_ep_plan")
+    return counts, offsets, sel, tag_ids, tag_w
+
+
+def ep_pack(x: torch.Tensor, offsets: torch.Tensor, sel: torch.Tensor, rows: int, stream=None) -> torch.Tensor:
+    lib = _lib.load()
+    xb = x.view(torch.int16) if x.dtype == torch.bfloat16 else x
+    out = torch.empty(max(rows, 0), xb.shape[1], dtype=torch.int16, device=x.device)
+    check(lib.samoyeds_ep_pack(_ptr(xb), xb.stride(0), xb.shape[1], _ptr(offsets), offsets.numel() - 1, _ptr(sel),
+                               rows, _ptr(out) if rows > 0 else None, _stream(stream)), "samoyeds_ep_pack")
+    return out
+
+
+def ep_combine(back: torch.Tensor, offsets: torch.Tensor, sel: torch.Tensor, out: torch.Tensor, stream=None):
+    lib = _lib.load()
+    rows = back.shape[0]
+    check(lib.samoyeds_ep_combine(_ptr(back) if rows else None, out.shape[1], _ptr(offsets), offsets.numel() - 1,
+                                  _ptr(sel), rows, _ptr(out), _stream(stream)), "samoyeds_ep_combine")
+    return out
+
+
+class MoEExperts:
+    """samoyeds_moe_experts: the layer body for rows whose routing is given
+    (keys = expert ids, -1 = none; vals = gate weights)."""
+
+    def __init__(self, cfg: MoEConfig, experts, max_rows: int, device=None):
+        self.cfg = cfg
+        self.experts = experts
+        self._arr = _weight_array(experts)
+        self._cfg = cfg.c()
+        lib = _lib.load()
+        b = C.c_size_t()
+        check(lib.smy_moe_workspace_bytes(C.byref(self._cfg), max_rows, C.byref(b)), "smy_moe_workspace_bytes")
+        self.max_rows = max_rows
+        self.workspace = torch.empty(b.value, dtype=torch.uint8, device=device or torch.device("cuda"))
+
+    def __call__(self, x: torch.Tensor, keys: torch.Tensor, vals: torch.Tensor, out: Optional[torch.Tensor] = None,
+                 stream=None):
+        lib = _lib.load()
+        R = x.shape[0]
+        if R > self.max_rows:
+            raise ValueError("rows exceed the workspace's max_rows")
+        if out is None:
+            out = torch.empty(R, self.cfg.hidden, dtype=torch.float32, device=x.device)
+        xb = x.view(torch.int16) if x.dtype == torch.bfloat16 else x
+        check(lib.samoyeds_moe_experts(C.byref(self._cfg), self._arr, _ptr(xb) if R else None, R,
+                                       _ptr(keys) if R else None, _ptr(vals) if R else None, _ptr(out),
+                                       _ptr(self.workspace), self.workspace.numel(), _stream(stream)),
+              "samoyeds_moe_experts")
+        return out

@@ -256,6 +256,71 @@ smy_status samoyeds_moe_layer(const smy_moe_config* cfg, const smy_weight* exper
                    static_cast<cudaStream_t>(stream));
 }
 
+static smy_status check_experts(const smy_moe_config* cfg, const smy_weight* experts) {
+  for (int e = 0; e < cfg->num_experts; ++e)
+    for (int i = 0; i < 3; ++i) {
+      const smy_weight& w = experts[3 * e + i];
+      const int64_t rows = i < 2 ? cfg->ffn : cfg->hidden, cols = i < 2 ? cfg->hidden : cfg->ffn;
+      if (!w.image) return SMY_E_NULL;
+      if (w.d.rows != rows || w.d.cols != cols || memcmp(&w.d.fmt, &cfg->fmt, sizeof(smy_format)) != 0)
+        return SMY_E_SHAPE;
+    }
+  return SMY_OK;
+}
+
+smy_status smy_ep_plan_workspace_bytes(int64_t T, int32_t k, int32_t world, size_t* bytes) {
+  if (!bytes) return SMY_E_NULL;
+  if (T < 0 || k < 1 || k > 8 || world < 1 || world > 256) return SMY_E_SHAPE;
+  *bytes = ep_plan_ws_bytes(T, world, k);
+  return SMY_OK;
+}
+
+smy_status samoyeds_ep_plan(const int32_t* ids, const float* w, int64_t T, int32_t k, int32_t num_experts,
+                            int32_t world, int32_t* send_counts, int32_t* send_offsets, int32_t* send_sel,
+                            int32_t* tag_ids, float* tag_w, void* workspace, size_t ws_bytes, void* stream) {
+  if (!send_counts || !send_offsets || !workspace) return SMY_E_NULL;
+  if (T > 0 && (!ids || !w || !send_sel || !tag_ids || !tag_w)) return SMY_E_NULL;
+  if (T < 0 || k < 1 || k > 8 || world < 1 || world > 256 || num_experts % world) return SMY_E_SHAPE;
+  smy_status st;
+  if ((st = check_arch()) != SMY_OK) return st;
+  return ep_plan_launch(ids, w, T, k, num_experts, world, send_counts, send_offsets, send_sel, tag_ids, tag_w,
+                        workspace, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+smy_status samoyeds_ep_pack(const void* x_bf16, int64_t ldx, int64_t hidden, const int32_t* send_offsets,
+                            int32_t world, const int32_t* send_sel, int64_t max_rows, void* x_send, void* stream) {
+  if (max_rows > 0 && (!x_bf16 || !send_offsets || !send_sel || !x_send)) return SMY_E_NULL;
+  if (hidden % 8 || ldx < hidden || ldx % 8 || world < 1) return SMY_E_SHAPE;
+  smy_status st;
+  if ((st = check_arch()) != SMY_OK) return st;
+  return ep_pack_launch(static_cast<const uint16_t*>(x_bf16), ldx, hidden, send_offsets, world, send_sel, max_rows,
+                        static_cast<uint16_t*>(x_send), static_cast<cudaStream_t>(stream));
+}
+
+smy_status samoyeds_moe_experts(const smy_moe_config* cfg, const smy_weight* experts, const void* x_bf16,
+                                int64_t rows, const int32_t* keys, const float* vals, float* out, void* workspace,
+                                size_t ws_bytes, void* stream) {
+  if (!cfg || !experts || !out || !workspace) return SMY_E_NULL;
+  if (rows > 0 && (!x_bf16 || !keys || !vals)) return SMY_E_NULL;
+  if (cfg->num_experts < 1 || cfg->top_k < 1 || cfg->top_k > 8 || cfg->num_experts > kMaxGroups) return SMY_E_CONFIG;
+  if (cfg->hidden % 128 || cfg->ffn % 128 || rows < 0) return SMY_E_SHAPE;
+  smy_status st;
+  if ((st = check_experts(cfg, experts)) != SMY_OK) return st;
+  if ((st = check_arch()) != SMY_OK) return st;
+  return moe_core(cfg, experts, nullptr, x_bf16, nullptr, keys, vals, rows, out, workspace, ws_bytes,
+                  static_cast<cudaStream_t>(stream));
+}
+
+smy_status samoyeds_ep_combine(const float* back, int64_t hidden, const int32_t* send_offsets, int32_t world,
+                               const int32_t* send_sel, int64_t max_rows, float* out, void* stream) {
+  if (max_rows > 0 && (!back || !send_offsets || !send_sel || !out)) return SMY_E_NULL;
+  if (hidden % 2 || world < 1) return SMY_E_SHAPE;
+  smy_status st;
+  if ((st = check_arch()) != SMY_OK) return st;
+  return ep_combine_launch(back, hidden, send_offsets, world, send_sel, max_rows, out,
+                           static_cast<cudaStream_t>(stream));
+}
+
 smy_status smy_moe_set_phase_events(void** events, int n) {
   if (events == nullptr) {
     g_phase_on = false;

@@ -74,6 +74,9 @@ smy_status route_launch(const float* logits, int64_t T, int E, int k, int gating
                         const int* tile_nt, const int* tile_mt, int n_tile_cfgs, int32_t* tile_prefix,
                         cudaStream_t s);
 size_t route_ws_bytes(int64_t T, int E);
+smy_status compact_launch(const int32_t* keys, const float* vals, int64_t T, int nb, int k, int32_t* counts,
+                          int32_t* offsets, int32_t* sel, float* gw, void* ws, size_t ws_bytes, const int* tile_nt,
+                          const int* tile_mt, int n_tile_cfgs, int32_t* tile_prefix, cudaStream_t s);
 
 // --------------------------------------------------------------- compress
 smy_status compress_launch(const smy_wdesc* d, const Geometry& g, const uint16_t* w, int64_t ldw, int flags,
@@ -84,6 +87,17 @@ smy_status silu_mul_launch(const float* g, const float* u, int64_t rows, int64_t
                            cudaStream_t s);
 smy_status check_arch();
 void count_launch(int n = 1);
+size_t ep_plan_ws_bytes(int64_t T, int world, int k);
+smy_status ep_plan_launch(const int32_t* ids, const float* w, int64_t T, int k, int E, int world, int32_t* counts,
+                          int32_t* offsets, int32_t* sel, int32_t* tag_ids, float* tag_w, void* ws, size_t ws_bytes,
+                          cudaStream_t s);
+smy_status ep_pack_launch(const uint16_t* x, int64_t ldx, int64_t d, const int32_t* offsets, int world,
+                          const int32_t* sel, int64_t max_rows, uint16_t* xs, cudaStream_t s);
+smy_status ep_combine_launch(const float* back, int64_t d, const int32_t* offsets, int world, const int32_t* sel,
+                             int64_t max_rows, float* out, cudaStream_t s);
+smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const smy_weight* shared, const void* x,
+                    const float* logits, const int32_t* keys, const float* vals, int64_t T, float* out,
+                    void* workspace, size_t ws_bytes, cudaStream_t s);
 void record_phase(int i, cudaStream_t s);  // no-op unless bench hooks are set
 
 }  // namespace smy

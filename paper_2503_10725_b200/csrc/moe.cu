@@ -132,9 +132,12 @@ static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* 
   return ssmm_launch(a, nt, nw, g.ms, g.rep, s);
 }
 
-smy_status moe_layer(const smy_moe_config* c, const smy_weight* experts, const smy_weight* shared, const void* x,
-                     const float* logits, int64_t T, float* out, void* workspace, size_t ws_bytes,
-                     cudaStream_t s) {
+// The expert computation over T rows of x.  Routing either comes from router
+// logits (top-k on device) or is given as keys[T x k] (expert ids, -1 = none)
+// with weights vals[T x k] -- the expert-parallel receive side.
+smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const smy_weight* shared, const void* x,
+                    const float* logits, const int32_t* keys, const float* vals, int64_t T, float* out,
+                    void* workspace, size_t ws_bytes, cudaStream_t s) {
   const int E = c->num_experts, k = c->top_k, d = c->hidden, f = c->ffn;
   smy_wdesc dgu{f, d, c->fmt}, ddn{d, f, c->fmt};
   Geometry ggu, gdn;
@@ -159,9 +162,13 @@ smy_status moe_layer(const smy_moe_config* c, const smy_weight* experts, const s
   int32_t* prefix_dn = w.prefix + (E + 1);
 
   record_phase(0, s);
-  if ((st = route_launch(logits, T, E, k, c->gating, w.ids, w.w, w.counts, w.offsets, w.sel, w.gw, w.route_ws,
-                         w.route_ws_bytes, nts, mts, 2, w.prefix, s)) != SMY_OK)
-    return st;
+  if (keys == nullptr)
+    st = route_launch(logits, T, E, k, c->gating, w.ids, w.w, w.counts, w.offsets, w.sel, w.gw, w.route_ws,
+                      w.route_ws_bytes, nts, mts, 2, w.prefix, s);
+  else
+    st = compact_launch(keys, vals, T, E, k, w.counts, w.offsets, w.sel, w.gw, w.route_ws, w.route_ws_bytes, nts,
+                        mts, 2, w.prefix, s);
+  if (st != SMY_OK) return st;
   record_phase(1, s);
   cudaError_t ce = cudaMemsetAsync(out, 0, (size_t)T * d * sizeof(float), s);
   if (ce != cudaSuccess) return cuda_status(ce);
@@ -255,6 +262,11 @@ smy_status moe_layer(const smy_moe_config* c, const smy_weight* experts, const s
   }
   record_phase(5, s);
   return SMY_OK;
+}
+
+smy_status moe_layer(const smy_moe_config* c, const smy_weight* experts, const smy_weight* shared, const void* x,
+                     const float* logits, int64_t T, float* out, void* workspace, size_t ws_bytes, cudaStream_t s) {
+  return moe_core(c, experts, shared, x, logits, nullptr, nullptr, T, out, workspace, ws_bytes, s);
 }
 
 }  // namespace smy

@@ -50,7 +50,10 @@ __device__ __forceinline__ void build_masks(const int32_t* __restrict__ ids, int
   const int64_t t = (int64_t)blockIdx.x * kRouteThreads + threadIdx.x;
   const int w = threadIdx.x / 32, l = threadIdx.x % 32;
   if (t < T)
-    for (int i = 0; i < k; ++i) atomicOr(&mask[w][ids[t * k + i]], 1u << l);
+    for (int i = 0; i < k; ++i) {
+      const int key = ids[t * k + i];
+      if (key >= 0) atomicOr(&mask[w][key], 1u << l);  // negative keys: no entry
+    }
   __syncthreads();
 }
 
@@ -58,7 +61,7 @@ __global__ void route_count_kernel(const float* __restrict__ logits, int64_t T, 
                                    int32_t* __restrict__ ids, float* __restrict__ w, int32_t* __restrict__ blk_counts) {
   __shared__ uint32_t mask[kRouteWarps][kMaxE];
   const int64_t t = (int64_t)blockIdx.x * kRouteThreads + threadIdx.x;
-  if (t < T) {
+  if (t < T && logits != nullptr) {  // logits == nullptr: keys are given (generic compaction)
     int li[kMaxK];
     float lw[kMaxK];
     topk_token(logits + t * E, E, k, gating, li, lw);
@@ -133,6 +136,7 @@ __global__ void route_scatter_kernel(const int32_t* __restrict__ ids, const floa
   const uint32_t lt = (1u << l) - 1u;
   for (int i = 0; i < k; ++i) {
     const int e = ids[t * k + i];
+    if (e < 0) continue;
     const int pos = wbase[ww][e] + __popc(mask[ww][e] & lt);
     sel[pos] = (int32_t)t;
     gw[pos] = w[t * k + i];
@@ -144,11 +148,20 @@ size_t route_ws_bytes(int64_t T, int E) {
   return (size_t)(2 * nblk * E) * sizeof(int32_t) + 256;
 }
 
+// Generic deterministic compaction of keys[T x k] (negative = no entry) into
+// per-bucket lists of ascending row ids (and the aligned vals).
+smy_status compact_launch(const int32_t* keys, const float* vals, int64_t T, int nb, int k, int32_t* counts,
+                          int32_t* offsets, int32_t* sel, float* gw, void* ws, size_t ws_bytes, const int* tile_nt,
+                          const int* tile_mt, int n_tile_cfgs, int32_t* tile_prefix, cudaStream_t s) {
+  return route_launch(nullptr, T, nb, k, 0, const_cast<int32_t*>(keys), const_cast<float*>(vals), counts, offsets, sel,
+                      gw, ws, ws_bytes, tile_nt, tile_mt, n_tile_cfgs, tile_prefix, s);
+}
+
 smy_status route_launch(const float* logits, int64_t T, int E, int k, int gating, int32_t* ids, float* w,
                         int32_t* counts, int32_t* offsets, int32_t* sel, float* gw, void* ws, size_t ws_bytes,
                         const int* tile_nt, const int* tile_mt, int n_tile_cfgs, int32_t* tile_prefix,
                         cudaStream_t s) {
-  if (E > kMaxE || k > kMaxK || k < 1 || k > E) return SMY_E_CONFIG;
+  if (E > kMaxE || k > kMaxK || k < 1 || (logits != nullptr && k > E)) return SMY_E_CONFIG;
   if (ws_bytes < route_ws_bytes(T, E)) return SMY_E_WORKSPACE;
   const int nblk = (int)((T + kRouteThreads - 1) / kRouteThreads);
   int32_t* blk_counts = static_cast<int32_t*>(ws);

@@ -1,0 +1,138 @@
+"""Expert parallelism on the GPU: the dispatch plan is bit-exact against the
+oracle's EP simulation, and the full dispatch -> compute -> combine data path for
+world = 2 / 4 ranks (simulated inside one process on one GPU, with an in-process
+exchange standing in for all_to_all_v) matches the oracle layer for every
+rank's tokens."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import fmt as F, moe, ssmm as OS
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def smy():
+    import paper_2503_10725_b200 as P
+    P.load()
+    return P
+
+
+def dev16(bits):
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).cuda()
+
+
+@pytest.mark.parametrize("world,E,k", [(2, 8, 2), (4, 8, 2), (4, 16, 6), (8, 64, 6)])
+def test_ep_plan_bit_exact(smy, world, E, k):
+    T = 300
+    ids_r, w_r = [], []
+    for r in range(world):
+        ids, w = moe.route(synth.router_logits(synth.SEED_LOGITS + 100 * r, T, E), k)
+        ids_r.append(ids)
+        w_r.append(w)
+    plan = moe.ep_dispatch_plan(ids_r, w_r, E, world)
+    for rank in range(world):
+        lg = torch.from_numpy(synth.router_logits(synth.SEED_LOGITS + 100 * rank, T, E)).cuda()
+        gids, gw, *_ = smy.route(lg, k)
+        counts, offsets, sel, tag_ids, tag_w = smy.ep_plan(gids, gw, E, world)
+        counts = counts.cpu().numpy()
+        sel = sel.cpu().numpy()
+        tag_ids = tag_ids.cpu().numpy()
+        tag_w = tag_w.cpu().numpy()
+        pos = 0
+        for d in range(world):
+            rows = [(t, tags) for (s, t, tags) in plan[d] if s == rank]
+            assert counts[d] == len(rows)
+            for t, tags in rows:
+                assert sel[pos] == t
+                assert tag_ids[pos].tolist() == [le for le, _ in tags] + [-1] * (k - len(tags))
+                assert np.allclose(tag_w[pos][:len(tags)], [g for _, g in tags], rtol=2e-6)
+                pos += 1
+
+
+def _ep_inproc(smy, layers, xs, lgs):
+    """Drive the three EP phases of every rank; exchanges are slices/concats."""
+    world = len(layers)
+    st = [layers[r].dispatch(xs[r], lgs[r]) for r in range(world)]
+    off = [np.concatenate([[0], np.cumsum(s["send_counts"])]) for s in st]
+    x_recv, t_recv = [], []
+    for d in range(world):
+        x_recv.append(torch.cat([st[s]["x_send"][off[s][d]:off[s][d + 1]] for s in range(world)]))
+        t_recv.append(torch.cat([st[s]["tags"][off[s][d]:off[s][d + 1]] for s in range(world)]))
+    parts = [layers[d].compute(x_recv[d], t_recv[d]) for d in range(world)]
+    outs = []
+    for s in range(world):
+        back = []
+        for d in range(world):
+            roff = np.concatenate([[0], np.cumsum([st[src]["send_counts"][d] for src in range(world)])])
+            back.append(parts[d][roff[s]:roff[s + 1]])
+        out = torch.empty(xs[s].shape[0], layers[s].cfg.hidden, dtype=torch.float32, device="cuda")
+        outs.append(layers[s].combine(torch.cat(back), st[s], out))
+    return outs
+
+
+@pytest.mark.parametrize("world,E,k,gating", [(2, 8, 2, "renorm_topk"), (4, 8, 2, "renorm_topk"),
+                                             (4, 16, 6, "softmax_all")])
+def test_ep_layer_matches_oracle(smy, world, E, k, gating):
+    from paper_2503_10725_b200.ep import EPMoELayer
+    fmt = F.SparseFormat(1, 2, 32)
+    d, f, T = 256, 384, 100
+    encs, sws = [], []
+    for e in range(E):
+        te, ts = [], []
+        for i in range(3):
+            r, c = (f, d) if i < 2 else (d, f)
+            wb = synth.weight_bf16(synth.weight_seed(e, i), r, c)
+            te.append(F.encode(F.prune(wb, fmt), fmt))
+            ts.append(smy.compress(dev16(wb), smy.Format(1, 2, 32))[0])
+        encs.append(tuple(te))
+        sws.append(tuple(ts))
+    cfg = smy.MoEConfig(E, k, d, f, 0, gating, smy.Format(1, 2, 32))
+    el = E // world
+    layers = [EPMoELayer(cfg, sws[r * el:(r + 1) * el], r, world, max_tokens=T) for r in range(world)]
+    xs_np = [synth.activations_bf16(synth.SEED_X + 100 * r, T, d) for r in range(world)]
+    lg_np = [synth.router_logits(synth.SEED_LOGITS + 100 * r, T, E, skew=0.5) for r in range(world)]
+    outs = _ep_inproc(smy, layers, [dev16(x) for x in xs_np], [torch.from_numpy(l).cuda() for l in lg_np])
+    mode = moe.SOFTMAX_ALL if gating == "softmax_all" else moe.RENORM_TOPK
+    single = smy.MoELayer(cfg, sws, max_tokens=T)
+    for r in range(world):
+        ref, S = moe.moe_layer(encs, xs_np[r], lg_np[r], k, mode)
+        got = outs[r].cpu().numpy().astype(np.float64)
+        assert OS.rel_fro(got - ref, ref) <= 1e-3
+        assert (np.abs(got - ref) <= 1e-2 * S + 1e-30).all()
+        one = single(dev16(xs_np[r]), torch.from_numpy(lg_np[r]).cuda()).cpu().numpy()
+        assert np.allclose(got, one, rtol=1e-4, atol=1e-5)      # EP == 1-GPU layer up to fp32 order
+
+
+def test_ep_world1_nccl(smy):
+    """EPMoELayer over a real NCCL process group of one rank."""
+    import os
+    import torch.distributed as dist
+    from paper_2503_10725_b200.ep import EPMoELayer
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        fmt = F.SparseFormat(1, 2, 32)
+        E, k, d, f, T = 4, 2, 128, 256, 64
+        encs, sws = [], []
+        for e in range(E):
+            te, ts = [], []
+            for i in range(3):
+                r, c = (f, d) if i < 2 else (d, f)
+                wb = synth.weight_bf16(synth.weight_seed(e, i), r, c)
+                te.append(F.encode(F.prune(wb, fmt), fmt))
+                ts.append(smy.compress(dev16(wb), smy.Format(1, 2, 32))[0])
+            encs.append(tuple(te))
+            sws.append(tuple(ts))
+        layer = EPMoELayer(smy.MoEConfig(E, k, d, f), sws, 0, 1, max_tokens=T)
+        x = synth.activations_bf16(synth.SEED_X, T, d)
+        lg = synth.router_logits(synth.SEED_LOGITS, T, E)
+        got = layer(dev16(x), torch.from_numpy(lg).cuda()).cpu().numpy().astype(np.float64)
+        ref, S = moe.moe_layer(encs, x, lg, k)
+        assert OS.rel_fro(got - ref, ref) <= 1e-3
+    finally:
+        dist.destroy_process_group()
