@@ -196,15 +196,15 @@ def run_reference(args):
 
 # ------------------------------------------------------------------ GPU arm
 
-def build_layer(P, model, device):
+def build_layer(P, model, device, experts=None):
     import numpy as np
     import torch
 
     import synth
     d, f, E, k, gating = MODELS[model]
     fmt = P.Format(*FMT)
-    experts = []
-    for e in range(E):
+    experts_out = []
+    for e in (range(E) if experts is None else experts):
         trip = []
         for i in range(3):
             rows, cols = (f, d) if i < 2 else (d, f)
@@ -215,9 +215,9 @@ def build_layer(P, model, device):
             del dense
             sw.drop_canonical()
             trip.append(sw)
-        experts.append(tuple(trip))
+        experts_out.append(tuple(trip))
     torch.cuda.synchronize()
-    return experts
+    return experts_out
 
 
 def run_ours(args):
@@ -233,14 +233,26 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+    if world > 1 or args.force_ep:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29541")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=device)
     lib = P.load()
     model = args.model
     d, f, E, k, gating = MODELS[model]
     T = args.tokens
-    experts = build_layer(P, model, device)
-    layer = P.MoELayer(P.MoEConfig(E, k, d, f, 0, gating, P.Format(*FMT)), experts, max_tokens=T, device=device)
+    ep = (world > 1 or args.force_ep) and args.parallel == "ep"
+    cfg = P.MoEConfig(E, k, d, f, 0, gating, P.Format(*FMT))
+    if ep:
+        from paper_2503_10725_b200.ep import EPMoELayer, TorchExchange
+        if E % world:
+            raise SystemExit(f"--parallel ep needs world | num_experts ({E})")
+        el = E // world
+        experts = build_layer(P, model, device, experts=range(rank * el, (rank + 1) * el))
+        layer = EPMoELayer(cfg, experts, rank, world, max_tokens=T, device=device, exchange=TorchExchange())
+    else:
+        experts = build_layer(P, model, device)
+        layer = P.MoELayer(cfg, experts, max_tokens=T, device=device)
 
     x = torch.empty(T, d, dtype=torch.int16, device=device)
     P.synth_fill(x, synth.SEED_X + 100 * rank, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
@@ -294,7 +306,7 @@ def run_ours(args):
 
     # ---------------- decode point on the same layer (reported beside the headline)
     dec = None
-    if args.decode_tokens and args.decode_tokens < T:
+    if args.decode_tokens and args.decode_tokens < T and not ep:
         Td = args.decode_tokens
         xd, lgd, outd = x[:Td], lg[:Td], out[:Td]
         for _ in range(5):
@@ -358,10 +370,18 @@ def run_ours(args):
     # ---------------- roofline of the dominant kernel (gate/up SSMM)
     hbm, bf16_burst, bf16_sust, src = peaks()
     sparse_peak = 2.0 * bf16_burst          # 2:4 sparse bf16 = 2 x dense (nominal ratio)
-    Tk = T * k
+    cnt = torch.bincount(P.route(lg, k, gating)[0].flatten().long(), minlength=E)
+    if world > 1:
+        dist.all_reduce(cnt)                 # assignments per expert over all ranks
+    cnt = cnt.cpu().numpy()
+    if ep:                                   # this rank computes its own experts for every rank's tokens
+        el = E // world
+        cnt = cnt[rank * el:(rank + 1) * el]
+    else:
+        cnt = cnt // max(world, 1) if world > 1 else cnt
+    Tk = int(cnt.sum())                      # (token, expert) pairs this GPU's gate/up SSMM processed
     flops_gu = 2 * 2 * (f // 2) * d * Tk     # 2 weights x 2 * (f*N/M) * d * tokens
-    counts = torch.bincount(P.route(lg, k, gating)[0].flatten().long(), minlength=E).cpu().numpy()
-    active = int((counts > 0).sum())
+    active = int((cnt > 0).sum())
     bytes_gu = (2 * active * f * d * BYTES_PER_ELEM + Tk * d * 2 + Tk * 4 + Tk * f * 2)
     t_gu = ph_ms[2] * 1e-3
     ach_tf = flops_gu / t_gu / 1e12
@@ -385,7 +405,8 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": WORKLOAD[model], "tokens_per_gpu": T, "global_tokens": T * world, "hidden": d,
                    "ffn": f, "experts": E, "top_k": k, "gating": gating, "format": "(N,M,V)=(1,2,32) + 2:4",
-                   "parallelism": f"dp{world} (experts replicated per GPU)",
+                   "parallelism": (f"ep{world} (experts sharded, NCCL all_to_all_v dispatch/combine)" if ep
+                                   else f"dp{world} (experts replicated per GPU)"),
                    "l2": "inputs larger than L2: %.0f MB of compressed expert weights streamed per step"
                          % (3 * active * f * d * BYTES_PER_ELEM / 1e6),
                    "weights": "random-init (counter-based synthetic), magnitude-pruned to (1,2,32)"},
@@ -404,7 +425,7 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_baseline(model)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
     return 0
 
@@ -445,6 +466,8 @@ def main():
     ap.add_argument("--model", default="mixtral", choices=sorted(MODELS))
     ap.add_argument("--tokens", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-ep", action="store_true", help=argparse.SUPPRESS)  # EP code path at world 1 (tests)
+    ap.add_argument("--parallel", default="ep", choices=["ep", "dp"], help="N>1: expert (default) or data parallel")
     ap.add_argument("--decode-tokens", type=int, default=64, help="extra decode point on the same layer (0: off)")
     args = ap.parse_args()
     if args.warmup < 3:
