@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -13,6 +14,15 @@ static thread_local std::string g_last_error;
 static std::atomic<uint64_t> g_launches{0};
 static cudaEvent_t g_phase[6];
 static bool g_phase_on = false;
+
+int debug_flags() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SMY_DEBUG");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
 
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 void record_phase(int i, cudaStream_t s) {

@@ -52,7 +52,10 @@ struct SsmmArgs {
   int max_tiles;           // tile count (single group) / upper bound (grouped)
   int weights_stream;      // 1: weights read once per call (decode) -> L2 evict_first
   int k_splits;            // >1: split K across tiles (SCATTER epilogue only; partial sums add)
+  int debug;               // profiling switches (env SMY_DEBUG): 1 no gather copies, 2 no weight
+                           // copies, 4 no MMAs, 8 no epilogue math/stores -- results are garbage
 };
+int debug_flags();
 
 // K-split count for a scatter-add launch with `tiles` (expert, m, n) tiles.
 int ssmm_pick_ksplit(int64_t tiles, int k_stages);

@@ -82,7 +82,15 @@ int ssmm_pick_ksplit(int64_t tiles, int k_stages) {
   return ks < 1 ? 1 : (int)ks;
 }
 
-smy_status ssmm_launch(const SsmmArgs& a, int nt, int nw, int ms, int rep, cudaStream_t s) {
+smy_status ssmm_launch(const SsmmArgs& a0, int nt, int nw, int ms, int rep, cudaStream_t s) {
+  const SsmmArgs* ap = &a0;
+  SsmmArgs dbg;
+  if (debug_flags()) {
+    dbg = a0;
+    dbg.debug = debug_flags();
+    ap = &dbg;
+  }
+  const SsmmArgs& a = *ap;
   for (const Entry& e : kTable)
     if (e.nt == nt && e.nw == nw && e.ms == ms && e.rep == rep) return e.fn(a, s);
   set_last_error("ssmm: unsupported (nt, nw, ms, rep) combination");

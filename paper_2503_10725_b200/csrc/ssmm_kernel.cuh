@@ -44,7 +44,7 @@ struct Cfg {
   static constexpr int kStageBytes = NW * kWStride + kBBytes;
   static constexpr int kAccCols = NW * MS * NT;
   static constexpr int kECol = (kAccCols + 3) / 4 * 4;
-  static constexpr int kColsNeeded = kECol + 4 * NW;
+  static constexpr int kColsNeeded = kECol + 8 * NW;       // E double-buffered across stages
   static constexpr int kTmemCols = kColsNeeded <= 32    ? 32
                                    : kColsNeeded <= 64  ? 64
                                    : kColsNeeded <= 128 ? 128
@@ -162,9 +162,12 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % S;
           mbar_wait(&empty[st], ((it / S) & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[st], stage_bytes);
-          bulk_g2s(wsm(st, 0), src0 + (size_t)k * a.block, wbytes, &full[st], pol_w);
-          if (NW == 2) bulk_g2s(wsm(st, 1), src1 + (size_t)k * a.block, wbytes, &full[st], pol_w);
+          const bool skip_w = a.debug & 2;
+          mbar_arrive_expect_tx(&full[st], stage_bytes - (skip_w ? NW * wbytes : 0u));
+          if (!skip_w) {
+            bulk_g2s(wsm(st, 0), src0 + (size_t)k * a.block, wbytes, &full[st], pol_w);
+            if (NW == 2) bulk_g2s(wsm(st, 1), src1 + (size_t)k * a.block, wbytes, &full[st], pol_w);
+          }
           if (!gather) {
 #pragma unroll
             for (int atom = 0; atom < 2 / REP; ++atom)
@@ -178,6 +181,9 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
     constexpr uint32_t idesc = (1u << 2) | (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NT >> 3) << 17) |
                                ((uint32_t)(128 >> 4) << 24);
     const uint32_t smem_base = smem_u32(smem);
+    // redux.sync results live in uniform registers: keeps every MMA operand uniform
+    // so the compiler issues UTCHMMA without a per-instruction R2UR waterfall
+    const uint32_t tm = __reduce_or_sync(0xffffffffu, tmem);
     uint32_t it = 0, tcount = 0;
     TileInfo ti;
     for (int tile = tile0; decode_tile(a, NT, tile, ti); tile += tstep, ++tcount) {
@@ -189,7 +195,11 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
         tc_fence_after();
         const uint32_t sbase = smem_base + st * C::kStageBytes;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) tc_cp_128x128b_elect(tmem + C::kECol + 4 * w, desc_interleave(sbase + w * C::kWStride + kABytes));
+        // E double-buffered in TMEM: this stage's copy does not overwrite columns
+        // the previous stage's MMAs may still be reading
+        const uint32_t ecol = C::kECol + (it & 1) * 4 * NW;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) tc_cp_128x128b_elect(tm + ecol + 4 * w, desc_interleave(sbase + w * C::kWStride + kABytes));
         // index bit-planes of this stage, made explicitly warp-uniform
         uint32_t pl[NW][4][C::kPlanes > 0 ? C::kPlanes : 1][4];
 #pragma unroll
@@ -199,10 +209,10 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
 #pragma unroll
             for (int b = 0; b < C::kPlanes; ++b) {
               const uint4 v = *reinterpret_cast<const uint4*>(wsm(st, w) + kABytes + kEBytes + (kb * C::kPlanes + b) * 16);
-              pl[w][kb][b][0] = __shfl_sync(0xffffffffu, v.x, 0);
-              pl[w][kb][b][1] = __shfl_sync(0xffffffffu, v.y, 0);
-              pl[w][kb][b][2] = __shfl_sync(0xffffffffu, v.z, 0);
-              pl[w][kb][b][3] = __shfl_sync(0xffffffffu, v.w, 0);
+              pl[w][kb][b][0] = __reduce_or_sync(0xffffffffu, v.x);
+              pl[w][kb][b][1] = __reduce_or_sync(0xffffffffu, v.y);
+              pl[w][kb][b][2] = __reduce_or_sync(0xffffffffu, v.z);
+              pl[w][kb][b][3] = __reduce_or_sync(0xffffffffu, v.w);
             }
 #pragma unroll
         for (int kb = 0; kb < 4; ++kb) {
@@ -223,8 +233,9 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
               }
               // metadata column of this K=32 window: even part in the address,
               // the odd bit in idesc.sparse_id2 (bits [0,2))
-              tc_mma_sp_elect(tmem + (w * MS + p) * NT, adesc, bdesc, idesc | (uint32_t)(kb & 1), mask[0], mask[1],
-                              mask[2], mask[3], tmem + C::kECol + 4 * w + (kb & 2));
+              if (!(a.debug & 4))
+              tc_mma_sp_elect(tm + (w * MS + p) * NT, adesc, bdesc, idesc | (uint32_t)(kb & 1), mask[0], mask[1],
+                              mask[2], mask[3], tm + ecol + 4 * w + (kb & 2));
             }
           }
         }
@@ -250,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
           mbar_wait(&empty[st], ((it / S) & 1) ^ 1);
           const int64_t kcol0 = (int64_t)k * (128 / REP);
           uint8_t* bs = bsm(st);
-          for (int idx = tb; idx < CHUNKS; idx += kGatherThreads) {
+          for (int idx = tb; idx < ((a.debug & 1) ? 0 : CHUNKS); idx += kGatherThreads) {
             const int row = idx / CPR, ch = idx % CPR;
             const int atom = ch >> 3, c8 = ch & 7;
             const int rid = rows[row];
@@ -301,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
               for (int j = 0; j < 16; ++j)
                 for (int off = nf >> 1; off > 0; off >>= 1) v[w][p][j] += __shfl_xor_sync(0xffffffffu, v[w][p][j], off);
         }
-        if (!valid) continue;
+        if (!valid || (a.debug & 8)) continue;
         const int jmax = min(16, ti.n_local - c0);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
