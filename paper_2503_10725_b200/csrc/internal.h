@@ -70,6 +70,9 @@ struct SsmmPlan {
 // Choose the token tile for a launch given the expected tokens per group.
 int ssmm_pick_nt(int nw, int ms, int rep, int64_t tokens_per_group);
 smy_status ssmm_launch(const SsmmArgs& a, int nt, int nw, int ms, int rep, cudaStream_t s);
+// CTA-pair (cta_group::2) kernel: a.m_tiles / tile prefixes count m-tile PAIRS, tmap box = nt/2 rows
+bool ssmm_pair_ok(int nt, int nw, int ms, int rep, int m_tiles, int64_t tokens_per_group);
+smy_status ssmm_launch_pair(const SsmmArgs& a, int nt, int nw, cudaStream_t s);
 
 // --------------------------------------------------------------- routing
 smy_status route_launch(const float* logits, int64_t T, int E, int k, int gating, int32_t* ids, float* w,

@@ -1,5 +1,5 @@
 // SSMM host dispatch: (NT, NW, MS, REP) -> kernel instantiation.
-#include "ssmm_kernel.cuh"
+#include "ssmm_pair.cuh"
 
 namespace smy {
 
@@ -29,6 +29,11 @@ extern template smy_status launch_t<16,1,8,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<16,1,16,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<32,2,4,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<16,2,8,1>(const SsmmArgs&, cudaStream_t);
+
+extern template smy_status launch_pair_t<64, 2>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<112, 2>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<128, 1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<224, 1>(const SsmmArgs&, cudaStream_t);
 
 namespace {
 struct Entry { int nt, nw, ms, rep; smy_status (*fn)(const SsmmArgs&, cudaStream_t); };
@@ -71,6 +76,23 @@ int ssmm_pick_nt(int nw, int ms, int rep, int64_t tpg) {
     if (e.nt >= tpg && (best < 0 || e.nt < best)) best = e.nt;
   }
   return best > 0 ? best : largest;
+}
+
+bool ssmm_pair_ok(int nt, int nw, int ms, int rep, int m_tiles, int64_t tokens_per_group) {
+  if (debug_flags() & 16) return false;  // SMY_DEBUG=16: force the single-CTA kernel
+  if (ms != 2 || rep != 1 || (m_tiles & 1) || tokens_per_group < 64) return false;
+  return nw == 2 ? (nt == 64 || nt == 112) : (nt == 128 || nt == 224);
+}
+
+smy_status ssmm_launch_pair(const SsmmArgs& a0, int nt, int nw, cudaStream_t s) {
+  SsmmArgs a = a0;
+  a.debug = debug_flags();
+  if (nw == 2 && nt == 64) return launch_pair_t<64, 2>(a, s);
+  if (nw == 2 && nt == 112) return launch_pair_t<112, 2>(a, s);
+  if (nw == 1 && nt == 128) return launch_pair_t<128, 1>(a, s);
+  if (nw == 1 && nt == 224) return launch_pair_t<224, 1>(a, s);
+  set_last_error("ssmm: unsupported pair (nt, nw)");
+  return SMY_E_CONFIG;
 }
 
 int ssmm_pick_ksplit(int64_t tiles, int k_stages) {

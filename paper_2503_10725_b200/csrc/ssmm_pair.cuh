@@ -1,0 +1,379 @@
+#pragma once
+// SSMM on CTA pairs (tcgen05 cta_group::2) -- the prefill path.
+//
+// Same computation and epilogues as ssmm_kernel.cuh, restructured around the
+// measured B200 limits (probes/mma_bench.cu, probes/gather_bench.cu, DESIGN.md
+// §7.1): a sparse M=128 MMA streams its A (4 KB) and B (64 B per token) from
+// shared memory at 128 B/clk, and the SEL gather is re-done for every weight
+// tile.  A CTA pair (one cluster of 2 on a TPC) issues M=256 MMAs: each CTA
+// holds its own 128 compressed rows of A and HALF of the token tile, each half
+// of B is read once for both SMs, and each CTA gathers only half the tokens.
+//
+// Roles per CTA (320 threads): warps 0-3 epilogue, 4 producer (weight-image
+// bulk copies; contiguous B tile via 2D TMA), 5 MMA issuer (leader CTA) or
+// stage relay (peer CTA), 6-9 SEL gather (cp.async).  Stage completion in the
+// peer is relayed to the leader's `pfull` barrier; the leader's MMA commits
+// multicast to both CTAs' `empty` / `acc_full`; both epilogues arrive on the
+// leader's `acc_empty`.
+#include "ssmm_kernel.cuh"
+
+namespace smy {
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar), done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_alloc2(uint32_t* smem_dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tc_cp2_elect(uint32_t taddr, uint64_t sdesc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+      "@p tcgen05.cp.cta_group::2.128x128b [%0], %1;\n\t}" ::"r"(taddr),
+      "l"(sdesc)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_sp2_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                 const uint32_t (&m)[8], uint32_t e_tmem) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "@p tcgen05.mma.sp.cta_group::2.kind::f16 [%0], %1, %2, [%12], %3, {%4, %5, %6, %7, %8, %9, %10, %11}, 1;\n\t}" ::"r"(
+          d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(m[0]), "r"(m[1]), "r"(m[2]), "r"(m[3]), "r"(m[4]), "r"(m[5]), "r"(m[6]),
+      "r"(m[7]), "r"(e_tmem)
+      : "memory");
+}
+// arrive on the same-offset mbarrier in every CTA of `cta_mask` once all prior
+// tcgen05 ops of this thread complete
+__device__ __forceinline__ void tc_commit2_mc_elect(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+      "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"(cta_mask)
+      : "memory");
+}
+
+template <int NT, int NW>
+struct PairCfg {
+  static constexpr int MS = 2;
+  static constexpr int kHalf = NT / 2;                      // tokens per CTA
+  static constexpr int kWStride = 19456;                    // A|E|planes
+  static constexpr int kBBytes = kHalf * 256;               // 2 K-atoms x kHalf rows x 128 B
+  static constexpr int kPeerPl = 128;                       // the peer m-tile's index planes (leader)
+  static constexpr int kStageBytes = (NW * kWStride + kBBytes + kPeerPl + 1023) / 1024 * 1024;
+  static constexpr int kAccCols = NW * MS * NT;
+  static constexpr int kECol = (kAccCols + 3) / 4 * 4;
+  static constexpr int kColsNeeded = kECol + 8 * NW;
+  static constexpr int kTmemCols = kColsNeeded <= 128 ? 128 : kColsNeeded <= 256 ? 256 : 512;
+  static constexpr int kAux = 2048;
+  static constexpr int kSmemCap = 232448 - 1024 - kAux;
+  static constexpr int kStagesRaw = kSmemCap / kStageBytes;
+  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + kAux;
+  static_assert(kColsNeeded <= 512, "TMEM budget");
+  static_assert(kStages >= 2, "smem budget");
+  static_assert(NT % 16 == 0 && (NT / 2) % 8 == 0 && NT >= 32 && NT <= 256, "UMMA N (cta_group::2) / 8-row halves");
+};
+
+template <int NT, int NW>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    ssmm_pair_kernel(const __grid_constant__ SsmmArgs a) {
+  using C = PairCfg<NT, NW>;
+  constexpr int S = C::kStages;
+  constexpr int MS = 2;
+  constexpr int H = C::kHalf;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* aux = smem + S * C::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(aux);
+  uint64_t* empty = full + S;
+  uint64_t* pfull = empty + S;   // leader: the peer's stage is complete
+  uint64_t* acc_full = pfull + S;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  int32_t* rows = reinterpret_cast<int32_t*>(aux + 1024);
+
+  const uint32_t cta = cluster_rank();
+  const bool leader = cta == 0;
+  const bool gather = a.sel_in != nullptr;
+  const int warp = warp_id(), lane = lane_id();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], gather ? 1 + kGatherThreads : 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&pfull[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 8);
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc2(tmem_slot, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // both CTAs' barriers exist before any remote arrive
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  auto wsm = [&](int st, int w) { return smem + st * C::kStageBytes + w * C::kWStride; };
+  auto bsm = [&](int st) { return smem + st * C::kStageBytes + NW * C::kWStride; };
+  auto psm = [&](int st) { return smem + st * C::kStageBytes + NW * C::kWStride + C::kBBytes; };
+  const int ks = a.k_stages;
+  const int pair0 = blockIdx.x >> 1, pstep = gridDim.x >> 1;
+
+  if (warp == 4) {
+    // ========= producer: own weight image + (leader) peer planes + contiguous B half =========
+    if (lane == 0) {
+      const uint32_t wbytes = kABytes + kEBytes + 64;
+      const uint32_t stage_bytes =
+          NW * wbytes + (leader ? NW * 64u : 0u) + (gather ? 0u : (uint32_t)C::kBBytes);
+      const uint64_t pol_w = a.weights_stream ? policy_evict_first() : policy_evict_normal();
+      const uint64_t pol_x = policy_evict_last();
+      uint32_t it = 0;
+      TileInfo ti;
+      for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep) {
+        const int m_own = 2 * ti.m_tile + (int)cta, m_peer = 2 * ti.m_tile + 1;
+        const uint8_t* src[2] = {a.img0[ti.g], NW == 2 ? a.img1[ti.g] : nullptr};
+        const int xrow = ti.row0 + ti.t0 + (int)cta * H;
+        for (int k = ti.k0; k < ti.k1; ++k, ++it) {
+          const int st = it % S;
+          mbar_wait_acq_cluster(&empty[st], ((it / S) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[st], stage_bytes);
+#pragma unroll
+          for (int w = 0; w < NW; ++w) {
+            bulk_g2s(wsm(st, w), src[w] + ((size_t)m_own * ks + k) * a.block, wbytes, &full[st], pol_w);
+            if (leader)
+              bulk_g2s(psm(st) + 64 * w, src[w] + ((size_t)m_peer * ks + k) * a.block + kABytes + kEBytes, 64,
+                       &full[st], pol_w);
+          }
+          if (!gather) {
+#pragma unroll
+            for (int atom = 0; atom < 2; ++atom)
+              tma_tile2d(bsm(st) + atom * (H * 128), &a.tmap_x, k * 128 + atom * 64, xrow, &full[st], pol_x);
+          }
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (leader) {
+      // ========================= MMA issuer (leader CTA) =========================
+      constexpr uint32_t idesc = (1u << 2) | (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NT >> 3) << 17) |
+                                 ((uint32_t)(256 >> 4) << 24);
+      const uint32_t smem_base = smem_u32(smem);
+      const uint32_t tm = __reduce_or_sync(0xffffffffu, tmem);
+      uint32_t it = 0, tcount = 0;
+      TileInfo ti;
+      for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep, ++tcount) {
+        mbar_wait_acq_cluster(acc_empty, tcount & 1);  // both epilogues drained and re-zeroed
+        tc_fence_after();
+        for (int k = ti.k0; k < ti.k1; ++k, ++it) {
+          const int st = it % S;
+          mbar_wait(&full[st], (it / S) & 1);
+          mbar_wait_acq_cluster(&pfull[st], (it / S) & 1);
+          tc_fence_after();
+          const uint32_t sbase = smem_base + st * C::kStageBytes;
+          const uint32_t ecol = C::kECol + (it & 1) * 4 * NW;
+#pragma unroll
+          for (int w = 0; w < NW; ++w)
+            tc_cp2_elect(tm + ecol + 4 * w, desc_interleave(sbase + w * C::kWStride + kABytes));
+          uint32_t pl[NW][4][8];  // lane planes: words 0-3 this CTA's 128 lanes, 4-7 the peer's
+#pragma unroll
+          for (int w = 0; w < NW; ++w)
+#pragma unroll
+            for (int kb = 0; kb < 4; ++kb) {
+              const uint4 v = *reinterpret_cast<const uint4*>(wsm(st, w) + kABytes + kEBytes + kb * 16);
+              const uint4 u = *reinterpret_cast<const uint4*>(psm(st) + 64 * w + kb * 16);
+              pl[w][kb][0] = __reduce_or_sync(0xffffffffu, v.x);
+              pl[w][kb][1] = __reduce_or_sync(0xffffffffu, v.y);
+              pl[w][kb][2] = __reduce_or_sync(0xffffffffu, v.z);
+              pl[w][kb][3] = __reduce_or_sync(0xffffffffu, v.w);
+              pl[w][kb][4] = __reduce_or_sync(0xffffffffu, u.x);
+              pl[w][kb][5] = __reduce_or_sync(0xffffffffu, u.y);
+              pl[w][kb][6] = __reduce_or_sync(0xffffffffu, u.z);
+              pl[w][kb][7] = __reduce_or_sync(0xffffffffu, u.w);
+            }
+#pragma unroll
+          for (int kb = 0; kb < 4; ++kb) {
+            const int e0 = kb * 32;
+            const uint64_t bdesc = desc_sw128(sbase + NW * C::kWStride + (e0 / 64) * (H * 128) + (e0 % 64) * 2);
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+              const uint64_t adesc = desc_sw128(sbase + w * C::kWStride + kb * 32);
+#pragma unroll
+              for (int p = 0; p < MS; ++p) {
+                uint32_t mask[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) mask[q] = p ? ~pl[w][kb][q] : pl[w][kb][q];  // disable lanes idx != p
+                if (!(a.debug & 4))
+                  tc_mma_sp2_elect(tm + (w * MS + p) * NT, adesc, bdesc, idesc | (uint32_t)(kb & 1), mask,
+                                   tm + ecol + 4 * w + (kb & 2));
+              }
+            }
+          }
+          tc_commit2_mc_elect(&empty[st], 0x3);
+        }
+        tc_commit2_mc_elect(acc_full, 0x3);
+      }
+    } else if (lane == 0) {
+      // ============== peer: relay "stage complete" to the leader's pfull ==============
+      const uint32_t pfull_leader = mapa_shared(smem_u32(pfull), 0);
+      uint32_t it = 0;
+      TileInfo ti;
+      for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep)
+        for (int k = ti.k0; k < ti.k1; ++k, ++it) {
+          const int st = it % S;
+          mbar_wait(&full[st], (it / S) & 1);
+          mbar_arrive_cluster(pfull_leader + st * 8);
+        }
+    }
+  } else if (warp >= 6) {
+    // ============ SEL gather of this CTA's half of the token rows (cp.async) ============
+    if (gather) {
+      const int tb = threadIdx.x - 6 * 32;
+      constexpr int CHUNKS = H * 16;
+      uint32_t it = 0;
+      TileInfo ti;
+      for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep) {
+        named_bar_sync(1, kGatherThreads);
+        for (int i = tb; i < H; i += kGatherThreads) {
+          const int t = (int)cta * H + i;
+          rows[i] = t < ti.n_local ? a.sel_in[ti.row0 + ti.t0 + t] : -1;
+        }
+        named_bar_sync(1, kGatherThreads);
+        for (int k = ti.k0; k < ti.k1; ++k, ++it) {
+          const int st = it % S;
+          mbar_wait_acq_cluster(&empty[st], ((it / S) & 1) ^ 1);
+          const int64_t kcol0 = (int64_t)k * 128;
+          uint8_t* bs = bsm(st);
+          for (int idx = tb; idx < ((a.debug & 1) ? 0 : CHUNKS); idx += kGatherThreads) {
+            const int row = idx / 16, ch = idx % 16;
+            const int atom = ch >> 3, c8 = ch & 7;
+            const int rid = rows[row];
+            const uint16_t* srcp = rid >= 0 ? a.x + (int64_t)rid * a.ldx + kcol0 + ch * 8 : a.x;
+            uint8_t* dst = bs + atom * (H * 128) + (row >> 3) * 1024 + (row & 7) * 128 + ((c8 ^ (row & 7)) << 4);
+            cp_async16(dst, srcp, rid >= 0 ? 16u : 0u);
+          }
+          cp_async_mbar_arrive_noinc(&full[st]);
+        }
+      }
+    }
+  } else {
+    // ============ epilogue (warps 0-3): this CTA's 128 lanes x all NT tokens ============
+    const int q = warp;
+    const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+    const uint32_t acc_empty_leader = mapa_shared(smem_u32(acc_empty), 0);
+    auto zero_acc = [&]() {
+      for (int c = 0; c < C::kAccCols; c += 16) tmem_st16_zero(tmem + lane_base + c);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc_empty_leader);
+    };
+    zero_acc();
+    uint32_t tcount = 0;
+    TileInfo ti;
+    for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep, ++tcount) {
+      const int m_own = 2 * ti.m_tile + (int)cta;
+      const int cr = m_own * kTileM + 32 * q + lane;
+      const bool valid = cr < a.R;
+      const int grp = cr;  // (1,2,V): one compressed row per group
+      mbar_wait_acq_cluster(acc_full, tcount & 1);
+      tc_fence_after();
+      for (int c0 = 0; c0 < ti.n_local; c0 += 16) {
+        float v[NW][MS][16];
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+#pragma unroll
+          for (int p = 0; p < MS; ++p) tmem_ld16(tmem + lane_base + (w * MS + p) * NT + c0, v[w][p]);
+        tmem_ld_wait();
+        if (!valid || (a.debug & 8)) continue;
+        const int jmax = min(16, ti.n_local - c0);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (j >= jmax) break;
+          const int r = ti.row0 + ti.t0 + c0 + j;
+          if (a.epi == kEpiScatter) {
+            const int dst = a.sel_out ? a.sel_out[r] : r;
+            const float s = a.scale ? a.scale[r] : 1.f;
+            red_add_v2(static_cast<float*>(a.out) + (int64_t)dst * a.ldo + 2 * grp, s * v[0][0][j], s * v[0][1][j]);
+          } else if (NW == 2) {
+            float act[2];
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+              const float gv = v[0][p][j], uv = v[NW - 1][p][j];
+              act[p] = __fdividef(gv, 1.f + __expf(-gv)) * uv;
+            }
+            *reinterpret_cast<__nv_bfloat162*>(static_cast<uint16_t*>(a.out) + (int64_t)r * a.ldo + 2 * grp) =
+                __floats2bfloat162_rn(act[0], act[1]);
+          } else if (a.out_bf16) {
+            *reinterpret_cast<__nv_bfloat162*>(static_cast<uint16_t*>(a.out) + (int64_t)r * a.ldo + 2 * grp) =
+                __floats2bfloat162_rn(v[0][0][j], v[0][1][j]);
+          } else {
+            *reinterpret_cast<float2*>(static_cast<float*>(a.out) + (int64_t)r * a.ldo + 2 * grp) =
+                make_float2(v[0][0][j], v[0][1][j]);
+          }
+        }
+      }
+      tc_fence_before();
+      zero_acc();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 5) tmem_dealloc2(tmem, C::kTmemCols);
+}
+
+template <int NT, int NW>
+smy_status launch_pair_t(const SsmmArgs& a, cudaStream_t s) {
+  using C = PairCfg<NT, NW>;
+  static bool configured = false;
+  static int num_sms = 0;
+  auto kern = ssmm_pair_kernel<NT, NW>;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e != cudaSuccess) return cuda_status(e);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    configured = true;
+  }
+  if (a.max_tiles <= 0) return SMY_OK;
+  const int pairs = a.max_tiles < num_sms / 2 ? a.max_tiles : num_sms / 2;
+  kern<<<2 * pairs, kThreads, C::kSmemBytes, s>>>(a);
+  count_launch();
+  return cuda_status(cudaGetLastError());
+}
+
+}  // namespace smy

@@ -300,6 +300,17 @@ def test_moe_layer_parity(smy, case):
     check_tol(got, ref, S, "moe layer")
 
 
+@pytest.mark.parametrize("case", [
+    dict(E=4, d=512, f=512, T=512, k=2),                       # tokens/expert >= 64: CTA-pair kernels
+    dict(E=8, d=1024, f=768, T=700, k=2, gating="softmax_all"),
+    dict(E=2, d=512, f=1024, T=300, k=2, skew=2.0),            # unbalanced experts, ragged tiles
+], ids=lambda c: f"E{c['E']}-d{c['d']}-f{c['f']}-T{c['T']}")
+def test_moe_layer_prefill_pair_kernels(smy, case):
+    case = dict(case)
+    got, ref, S = _layer_case(smy, F.SparseFormat(1, 2, 32), **case)
+    check_tol(got, ref, S, "moe layer (pair kernels)")
+
+
 def test_moe_layer_all_tokens_one_expert(smy):
     fmt = F.SparseFormat(1, 2, 32)
     got, ref, S = _layer_case(smy, fmt, E=4, d=128, f=256, T=200, k=1, skew=50.0)
