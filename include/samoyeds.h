@@ -201,6 +201,8 @@ SMY_API smy_status samoyeds_ep_combine(const float* back, int64_t hidden, const 
  * region.  smy_launch_count: number of kernels this library has launched.  */
 SMY_API smy_status smy_moe_set_phase_events(void** events, int n);
 SMY_API uint64_t smy_launch_count(void);
+/* SMY_DEBUG=128 profiling: copy (and reset) role cycle counters [2][ctas][16] (gate/up, scatter launches). */
+SMY_API int smy_debug_prof(unsigned long long* host, int ctas);
 
 /* ------------------------------------------------------ synthetic inputs
  * Counter-based generator twin of synth/__init__.py (input preparation only,

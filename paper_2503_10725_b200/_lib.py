@@ -66,6 +66,7 @@ SIGNATURES = {
                                       C.c_void_p, C.c_void_p]),
     "smy_moe_set_phase_events": (C.c_int, [C.c_void_p, C.c_int]),
     "smy_launch_count": (C.c_uint64, []),
+    "smy_debug_prof": (C.c_int, [C.c_void_p, C.c_int]),
     "smy_synth_fill": (C.c_int, [C.c_uint64, C.c_int, C.c_float, C.c_int, C.c_int, C.c_int64, C.c_int64,
                                  C.c_void_p, C.c_int, C.c_void_p]),
 }

@@ -24,6 +24,18 @@ int debug_flags() {
   return v;
 }
 
+static unsigned long long* g_prof = nullptr;
+static int g_prof_ctas = 0;
+unsigned long long* debug_prof_buffer(int ctas) {
+  if (ctas > g_prof_ctas) {
+    if (g_prof) cudaFree(g_prof);
+    cudaMalloc(&g_prof, sizeof(unsigned long long) * 32 * ctas);
+    cudaMemset(g_prof, 0, sizeof(unsigned long long) * 32 * ctas);
+    g_prof_ctas = ctas;
+  }
+  return g_prof;
+}
+
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 void record_phase(int i, cudaStream_t s) {
   if (g_phase_on && i >= 0 && i < 6) cudaEventRecord(g_phase[i], s);
@@ -343,6 +355,15 @@ smy_status smy_moe_set_phase_events(void** events, int n) {
 }
 
 uint64_t smy_launch_count(void) { return g_launches.load(); }
+
+// SMY_DEBUG & 128: accumulated per-role cycle counters of the last pair-kernel launches
+int smy_debug_prof(unsigned long long* host, int ctas) {
+  if (!g_prof || ctas > g_prof_ctas) return 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, g_prof, sizeof(unsigned long long) * 32 * ctas, cudaMemcpyDeviceToHost);
+  cudaMemset(g_prof, 0, sizeof(unsigned long long) * 32 * g_prof_ctas);
+  return ctas;
+}
 
 smy_status smy_synth_fill(uint64_t seed, int dist, float scale, int lo, int hi, int64_t idx0, int64_t n, void* out,
                           int out_bf16, void* stream) {

@@ -53,8 +53,11 @@ struct SsmmArgs {
   int weights_stream;      // 1: weights read once per call (decode) -> L2 evict_first
   int k_splits;            // >1: split K across tiles (SCATTER epilogue only; partial sums add)
   int debug;               // profiling switches (env SMY_DEBUG): 1 no gather copies, 2 no weight
-                           // copies, 4 no MMAs, 8 no epilogue math/stores -- results are garbage
+                           // copies, 4 no MMAs, 8 no epilogue math/stores -- results are garbage;
+                           // 128: per-role cycle counters into `prof` (results valid)
+  unsigned long long* prof;  // [2 epilogue kinds][148][16] role cycle counters (SMY_DEBUG & 128)
 };
+unsigned long long* debug_prof_buffer(int ctas);
 int debug_flags();
 
 // K-split count for a scatter-add launch with `tiles` (expert, m, n) tiles.
@@ -71,8 +74,9 @@ struct SsmmPlan {
 int ssmm_pick_nt(int nw, int ms, int rep, int64_t tokens_per_group);
 smy_status ssmm_launch(const SsmmArgs& a, int nt, int nw, int ms, int rep, cudaStream_t s);
 // CTA-pair (cta_group::2) kernel: a.m_tiles / tile prefixes count m-tile PAIRS, tmap box = nt/2 rows
-bool ssmm_pair_ok(int nt, int nw, int ms, int rep, int m_tiles, int64_t tokens_per_group);
-smy_status ssmm_launch_pair(const SsmmArgs& a, int nt, int nw, cudaStream_t s);
+// returns the cluster size to use (2: one MMA pair, 4: two pairs sharing weights) or 0 (single CTA)
+int ssmm_pair_cluster(int nt, int nw, int ms, int rep, int m_tiles, int64_t tokens_per_group);
+smy_status ssmm_launch_pair(const SsmmArgs& a, int nt, int nw, int cl, cudaStream_t s);
 
 // --------------------------------------------------------------- routing
 smy_status route_launch(const float* logits, int64_t T, int E, int k, int gating, int32_t* ids, float* w,

@@ -95,7 +95,7 @@ static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* 
                           int m_out, int nt, int nw, const uint16_t* x, int64_t ldx, int64_t x_rows,
                           const int32_t* sel_in, const int32_t* offsets, const int32_t* prefix, int max_tiles,
                           int epi, void* out, int64_t ldo, int out_bf16, const int32_t* sel_out,
-                          const float* scale, int64_t k_cols, int stream_w, int k_splits, bool pair,
+                          const float* scale, int64_t k_cols, int stream_w, int k_splits, int cl,
                           cudaStream_t s) {
   SsmmArgs a;
   memset(&a, 0, sizeof(a));
@@ -128,9 +128,9 @@ static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* 
   a.max_tiles = max_tiles * k_splits;
   a.weights_stream = stream_w;
   a.k_splits = k_splits;
-  smy_status st = make_x_tmap(&a.tmap_x, x, k_cols, x_rows, ldx, pair ? nt / 2 : nt);
+  smy_status st = make_x_tmap(&a.tmap_x, x, k_cols, x_rows, ldx, cl ? nt / 2 : nt);
   if (st != SMY_OK) return st;
-  return pair ? ssmm_launch_pair(a, nt, nw, s) : ssmm_launch(a, nt, nw, g.ms, g.rep, s);
+  return cl ? ssmm_launch_pair(a, nt, nw, cl, s) : ssmm_launch(a, nt, nw, g.ms, g.rep, s);
 }
 
 // The expert computation over T rows of x.  Routing either comes from router
@@ -157,11 +157,12 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   const int64_t act = E < T * k ? E : T * k;
   const int ks_dn = ssmm_pick_ksplit((int64_t)gdn.m_tiles * act * ((tpg + nt_dn - 1) / (nt_dn > 0 ? nt_dn : 1)),
                                      gdn.k_stages);
-  const bool pair_gu = fused && ssmm_pair_ok(nt_gu, 2, ggu.ms, ggu.rep, ggu.m_tiles, tpg);
-  const bool pair_dn = ssmm_pair_ok(nt_dn, 1, gdn.ms, gdn.rep, gdn.m_tiles, tpg);
-  const int mt_gu = pair_gu ? ggu.m_tiles / 2 : ggu.m_tiles;
-  const int mt_dn = pair_dn ? gdn.m_tiles / 2 : gdn.m_tiles;
-  const int nts[2] = {nt_gu, nt_dn};
+  const int cl_gu = fused ? ssmm_pair_cluster(nt_gu, 2, ggu.ms, ggu.rep, ggu.m_tiles, tpg) : 0;
+  const int cl_dn = ssmm_pair_cluster(nt_dn, 1, gdn.ms, gdn.rep, gdn.m_tiles, tpg);
+  const int mt_gu = cl_gu ? ggu.m_tiles / 2 : ggu.m_tiles;
+  const int mt_dn = cl_dn ? gdn.m_tiles / 2 : gdn.m_tiles;
+  // the routing scan counts tiles per expert in units of the launch's token span
+  const int nts[2] = {cl_gu == 4 ? 2 * nt_gu : nt_gu, cl_dn == 4 ? 2 * nt_dn : nt_dn};
   const int mts[2] = {mt_gu, mt_dn * ks_dn};
   int32_t* prefix_gu = w.prefix;
   int32_t* prefix_dn = w.prefix + (E + 1);
@@ -192,27 +193,27 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
     wd[e] = &experts[3 * e + 2];
   }
   const int64_t Tk = T * k;
-  const int max_gu = mt_gu * (E + (int)((Tk + nt_gu - 1) / nt_gu));
-  const int max_dn = mt_dn * (E + (int)((Tk + nt_dn - 1) / nt_dn));
+  const int max_gu = mt_gu * (E + (int)((Tk + nts[0] - 1) / nts[0]));
+  const int max_dn = mt_dn * (E + (int)((Tk + nts[1] - 1) / nts[1]));
   const uint16_t* xb = static_cast<const uint16_t*>(x);
 
   // gate/up: H = Wg x[SEL], U = Wu x[SEL], inter = bf16(silu(H) * U)
   if (fused) {
     st = grouped(wg, wu, E, ggu, f, nt_gu, 2, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiSiluMul, w.inter, f,
-                 1, nullptr, nullptr, d, tpg <= nt_gu, 1, pair_gu, s);
+                 1, nullptr, nullptr, d, tpg <= nt_gu, 1, cl_gu, s);
   } else {
     st = grouped(wg, nullptr, E, ggu, f, nt_gu, 1, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiCompact,
-                 w.fallback_g, f, 0, nullptr, nullptr, d, tpg <= nt_gu, 1, false, s);
+                 w.fallback_g, f, 0, nullptr, nullptr, d, tpg <= nt_gu, 1, 0, s);
     if (st == SMY_OK)
       st = grouped(wu, nullptr, E, ggu, f, nt_gu, 1, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiCompact,
-                   w.fallback_u, f, 0, nullptr, nullptr, d, tpg <= nt_gu, 1, false, s);
+                   w.fallback_u, f, 0, nullptr, nullptr, d, tpg <= nt_gu, 1, 0, s);
     if (st == SMY_OK) st = silu_mul_launch(w.fallback_g, w.fallback_u, Tk, f, w.inter, s);
   }
   if (st != SMY_OK) return st;
   record_phase(3, s);
   // down: out[sel[t]] += gw[t] * Wd inter[t]
   st = grouped(wd, nullptr, E, gdn, d, nt_dn, 1, w.inter, f, Tk, nullptr, w.offsets, prefix_dn, max_dn, kEpiScatter,
-               out, d, 0, w.sel, w.gw, f, tpg <= nt_dn, ks_dn, pair_dn, s);
+               out, d, 0, w.sel, w.gw, f, tpg <= nt_dn, ks_dn, cl_dn, s);
   if (st != SMY_OK) return st;
   record_phase(4, s);
 

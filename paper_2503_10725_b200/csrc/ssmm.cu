@@ -30,10 +30,12 @@ extern template smy_status launch_t<16,1,16,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<32,2,4,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<16,2,8,1>(const SsmmArgs&, cudaStream_t);
 
-extern template smy_status launch_pair_t<64, 2>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<112, 2>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<128, 1>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<224, 1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<64, 2, 2>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<112, 2, 2>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<128, 1, 2>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<224, 1, 2>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<112, 2, 4>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<224, 1, 4>(const SsmmArgs&, cudaStream_t);
 
 namespace {
 struct Entry { int nt, nw, ms, rep; smy_status (*fn)(const SsmmArgs&, cudaStream_t); };
@@ -78,19 +80,26 @@ int ssmm_pick_nt(int nw, int ms, int rep, int64_t tpg) {
   return best > 0 ? best : largest;
 }
 
-bool ssmm_pair_ok(int nt, int nw, int ms, int rep, int m_tiles, int64_t tokens_per_group) {
-  if (debug_flags() & 16) return false;  // SMY_DEBUG=16: force the single-CTA kernel
-  if (ms != 2 || rep != 1 || (m_tiles & 1) || tokens_per_group < 64) return false;
-  return nw == 2 ? (nt == 64 || nt == 112) : (nt == 128 || nt == 224);
+int ssmm_pair_cluster(int nt, int nw, int ms, int rep, int m_tiles, int64_t tokens_per_group) {
+  if (debug_flags() & 16) return 0;  // SMY_DEBUG=16: force the single-CTA kernel
+  if (ms != 2 || rep != 1 || (m_tiles & 1) || tokens_per_group < 64) return 0;
+  if (!(nw == 2 ? (nt == 64 || nt == 112) : (nt == 128 || nt == 224))) return 0;
+  // two MMA pairs share each weight stage when an expert has >= 2 token tiles
+  // (4-CTA multicast clusters measured 2x slower on B200: opt-in via SMY_DEBUG=64)
+  const bool quad = (debug_flags() & 64) && tokens_per_group >= 2 * nt && (nt == 112 || nt == 224);
+  return quad ? 4 : 2;
 }
 
-smy_status ssmm_launch_pair(const SsmmArgs& a0, int nt, int nw, cudaStream_t s) {
+smy_status ssmm_launch_pair(const SsmmArgs& a0, int nt, int nw, int cl, cudaStream_t s) {
   SsmmArgs a = a0;
   a.debug = debug_flags();
-  if (nw == 2 && nt == 64) return launch_pair_t<64, 2>(a, s);
-  if (nw == 2 && nt == 112) return launch_pair_t<112, 2>(a, s);
-  if (nw == 1 && nt == 128) return launch_pair_t<128, 1>(a, s);
-  if (nw == 1 && nt == 224) return launch_pair_t<224, 1>(a, s);
+  a.prof = (a.debug & 128) ? debug_prof_buffer(148) : nullptr;
+  if (cl == 4 && nw == 2 && nt == 112) return launch_pair_t<112, 2, 4>(a, s);
+  if (cl == 4 && nw == 1 && nt == 224) return launch_pair_t<224, 1, 4>(a, s);
+  if (nw == 2 && nt == 64) return launch_pair_t<64, 2, 2>(a, s);
+  if (nw == 2 && nt == 112) return launch_pair_t<112, 2, 2>(a, s);
+  if (nw == 1 && nt == 128) return launch_pair_t<128, 1, 2>(a, s);
+  if (nw == 1 && nt == 224) return launch_pair_t<224, 1, 2>(a, s);
   set_last_error("ssmm: unsupported pair (nt, nw)");
   return SMY_E_CONFIG;
 }

@@ -9,7 +9,7 @@
 // holds its own 128 compressed rows of A and HALF of the token tile, each half
 // of B is read once for both SMs, and each CTA gathers only half the tokens.
 //
-// Roles per CTA (320 threads): warps 0-3 epilogue, 4 producer (weight-image
+// Roles per CTA (448 threads): warps 0-3 + 10-13 epilogue, 4 producer (weight-image
 // bulk copies; contiguous B tile via 2D TMA), 5 MMA issuer (leader CTA) or
 // stage relay (peer CTA), 6-9 SEL gather (cp.async).  Stage completion in the
 // peer is relayed to the leader's `pfull` barrier; the leader's MMA commits
@@ -85,6 +85,20 @@ __device__ __forceinline__ void tc_commit2_mc_elect(uint64_t* bar, uint16_t cta_
       : "memory");
 }
 
+// bulk copy global -> the same smem offset in every CTA of cta_mask; each
+// destination CTA's mbarrier (same offset) receives the complete_tx
+__device__ __forceinline__ void bulk_g2s_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint16_t cta_mask,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4, %5;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(cta_mask), "l"(policy)
+      : "memory");
+}
+
+constexpr int kPairEpiWarps = 8;                    // warps 0-3 and 10-13
+constexpr int kPairThreads = 32 * (10 + kPairEpiWarps - 4);  // + producer, MMA, 4 gather
+
 template <int NT, int NW>
 struct PairCfg {
   static constexpr int MS = 2;
@@ -107,10 +121,15 @@ struct PairCfg {
   static_assert(NT % 16 == 0 && (NT / 2) % 8 == 0 && NT >= 32 && NT <= 256, "UMMA N (cta_group::2) / 8-row halves");
 };
 
-template <int NT, int NW>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+// CL = 2: one MMA pair per cluster.  CL = 4: two MMA pairs (ranks {0,1},
+// {2,3}) on adjacent token tiles of the same weight m-tiles; each weight stage
+// is fetched once and multicast to both pairs (ranks c and c+2), halving the
+// weight requests and L2 reads per SM.
+template <int NT, int NW, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
     ssmm_pair_kernel(const __grid_constant__ SsmmArgs a) {
   using C = PairCfg<NT, NW>;
+  static_assert(CL == 2 || CL == 4, "cluster of one or two MMA pairs");
   constexpr int S = C::kStages;
   constexpr int MS = 2;
   constexpr int H = C::kHalf;
@@ -125,18 +144,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
   int32_t* rows = reinterpret_cast<int32_t*>(aux + 1024);
 
-  const uint32_t cta = cluster_rank();
+  const uint32_t rank = cluster_rank();
+  const uint32_t cta = rank & 1;           // rank inside the MMA pair
+  const uint32_t pi = rank >> 1;           // which pair of the cluster
+  const uint32_t lead_rank = rank & ~1u;   // the pair's leader
   const bool leader = cta == 0;
   const bool gather = a.sel_in != nullptr;
   const int warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], gather ? 1 + kGatherThreads : 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL / 2);  // every pair's MMA must be done with the slot
       mbar_init(&pfull[s], 1);
     }
     mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 8);
+    mbar_init(acc_empty, 2 * kPairEpiWarps);  // every epilogue warp of both CTAs
     fence_mbar_init();
   }
   if (warp == 5) tmem_alloc2(tmem_slot, C::kTmemCols);
@@ -149,8 +171,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   auto bsm = [&](int st) { return smem + st * C::kStageBytes + NW * C::kWStride; };
   auto psm = [&](int st) { return smem + st * C::kStageBytes + NW * C::kWStride + C::kBBytes; };
   const int ks = a.k_stages;
-  const int pair0 = blockIdx.x >> 1, pstep = gridDim.x >> 1;
+  const int pair0 = blockIdx.x / CL, pstep = gridDim.x / CL;
+  // cluster tile -> this pair's token tile
+  auto pair_tile = [&](TileInfo& ti) {
+    if (CL == 4) {
+      ti.t0 += (int)pi * NT;
+      ti.n_local = min(NT, ti.n_local - (int)pi * NT);  // may be <= 0: the pair idles through the tile
+    }
+  };
 
+  const bool prof = a.prof != nullptr;
+  unsigned long long pc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  auto clk = []() { unsigned long long c; asm volatile("mov.u64 %0, %%clock64;" : "=l"(c)); return c; };
   if (warp == 4) {
     // ========= producer: own weight image + (leader) peer planes + contiguous B half =========
     if (lane == 0) {
@@ -161,17 +193,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint64_t pol_x = policy_evict_last();
       uint32_t it = 0;
       TileInfo ti;
-      for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep) {
+      for (int tile = pair0; decode_tile(a, NT * (CL / 2), tile, ti) && (pair_tile(ti), true); tile += pstep) {
         const int m_own = 2 * ti.m_tile + (int)cta, m_peer = 2 * ti.m_tile + 1;
         const uint8_t* src[2] = {a.img0[ti.g], NW == 2 ? a.img1[ti.g] : nullptr};
         const int xrow = ti.row0 + ti.t0 + (int)cta * H;
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % S;
+          const unsigned long long t0 = prof ? clk() : 0;
           mbar_wait_acq_cluster(&empty[st], ((it / S) & 1) ^ 1);
+          if (prof) pc[5] += clk() - t0;
           mbar_arrive_expect_tx(&full[st], stage_bytes);
 #pragma unroll
           for (int w = 0; w < NW; ++w) {
-            bulk_g2s(wsm(st, w), src[w] + ((size_t)m_own * ks + k) * a.block, wbytes, &full[st], pol_w);
+            if (CL == 4) {  // the two pairs alternate issuing each k-stage for both of them
+              if ((k & 1) == (int)pi)
+                bulk_g2s_mc(wsm(st, w), src[w] + ((size_t)m_own * ks + k) * a.block, wbytes, &full[st],
+                            (uint16_t)((1u << cta) | (1u << (cta + 2))), pol_w);
+            } else {
+              bulk_g2s(wsm(st, w), src[w] + ((size_t)m_own * ks + k) * a.block, wbytes, &full[st], pol_w);
+            }
             if (leader)
               bulk_g2s(psm(st) + 64 * w, src[w] + ((size_t)m_peer * ks + k) * a.block + kABytes + kEBytes, 64,
                        &full[st], pol_w);
@@ -193,13 +233,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t tm = __reduce_or_sync(0xffffffffu, tmem);
       uint32_t it = 0, tcount = 0;
       TileInfo ti;
-      for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep, ++tcount) {
+      const unsigned long long tstart = prof ? clk() : 0;
+      for (int tile = pair0; decode_tile(a, NT * (CL / 2), tile, ti) && (pair_tile(ti), true); tile += pstep, ++tcount) {
+        unsigned long long t0 = prof ? clk() : 0;
         mbar_wait_acq_cluster(acc_empty, tcount & 1);  // both epilogues drained and re-zeroed
+        if (prof) pc[1] += clk() - t0;
         tc_fence_after();
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % S;
+          t0 = prof ? clk() : 0;
           mbar_wait(&full[st], (it / S) & 1);
           mbar_wait_acq_cluster(&pfull[st], (it / S) & 1);
+          if (prof) pc[0] += clk() - t0;
           tc_fence_after();
           const uint32_t sbase = smem_base + st * C::kStageBytes;
           const uint32_t ecol = C::kECol + (it & 1) * 4 * NW;
@@ -240,30 +285,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               }
             }
           }
-          tc_commit2_mc_elect(&empty[st], 0x3);
+          tc_commit2_mc_elect(&empty[st], (uint16_t)(CL == 4 ? 0xF : 0x3));
         }
-        tc_commit2_mc_elect(acc_full, 0x3);
+        tc_commit2_mc_elect(acc_full, (uint16_t)(0x3u << (2 * pi)));
+        pc[7] += 1;
       }
+      if (prof) pc[2] = clk() - tstart;
     } else if (lane == 0) {
       // ============== peer: relay "stage complete" to the leader's pfull ==============
-      const uint32_t pfull_leader = mapa_shared(smem_u32(pfull), 0);
+      const uint32_t pfull_leader = mapa_shared(smem_u32(pfull), lead_rank);
       uint32_t it = 0;
       TileInfo ti;
-      for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep)
+      for (int tile = pair0; decode_tile(a, NT * (CL / 2), tile, ti) && (pair_tile(ti), true); tile += pstep)
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % S;
           mbar_wait(&full[st], (it / S) & 1);
           mbar_arrive_cluster(pfull_leader + st * 8);
         }
     }
-  } else if (warp >= 6) {
+  } else if (warp >= 6 && warp < 10) {
     // ============ SEL gather of this CTA's half of the token rows (cp.async) ============
     if (gather) {
       const int tb = threadIdx.x - 6 * 32;
       constexpr int CHUNKS = H * 16;
       uint32_t it = 0;
       TileInfo ti;
-      for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep) {
+      for (int tile = pair0; decode_tile(a, NT * (CL / 2), tile, ti) && (pair_tile(ti), true); tile += pstep) {
         named_bar_sync(1, kGatherThreads);
         for (int i = tb; i < H; i += kGatherThreads) {
           const int t = (int)cta * H + i;
@@ -288,12 +335,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ============ epilogue (warps 0-3): this CTA's 128 lanes x all NT tokens ============
-    const int q = warp;
+    // ==== epilogue (warps 0-3 and 10-13): this CTA's 128 lanes x all NT tokens ====
+    // warp w reaches TMEM lanes 32*(w%4)..+31; warps w and w+10 split the
+    // 16-column chunks (even / odd) so two warps per SM sub-partition hide the
+    // epilogue's dependent-latency chains.
+    const int q = warp & 3;
+    const int h = warp >= 10 ? 1 : 0;
     const uint32_t lane_base = (uint32_t)(32 * q) << 16;
-    const uint32_t acc_empty_leader = mapa_shared(smem_u32(acc_empty), 0);
+    const uint32_t acc_empty_leader = mapa_shared(smem_u32(acc_empty), lead_rank);
     auto zero_acc = [&]() {
-      for (int c = 0; c < C::kAccCols; c += 16) tmem_st16_zero(tmem + lane_base + c);
+      // the same (weight, slot, chunk) split as the reads: regions start at j*NT,
+      // and NT (e.g. 112) need not be a multiple of 32
+      for (int j = 0; j < NW * MS; ++j)
+        for (int c = 16 * h; c < NT; c += 32) tmem_st16_zero(tmem + lane_base + j * NT + c);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -302,20 +356,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     zero_acc();
     uint32_t tcount = 0;
     TileInfo ti;
-    for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep, ++tcount) {
+    for (int tile = pair0; decode_tile(a, NT * (CL / 2), tile, ti) && (pair_tile(ti), true); tile += pstep, ++tcount) {
       const int m_own = 2 * ti.m_tile + (int)cta;
       const int cr = m_own * kTileM + 32 * q + lane;
       const bool valid = cr < a.R;
       const int grp = cr;  // (1,2,V): one compressed row per group
+      unsigned long long t0 = prof ? clk() : 0;
       mbar_wait_acq_cluster(acc_full, tcount & 1);
+      if (prof) { const unsigned long long t1 = clk(); pc[3] += t1 - t0; t0 = t1; }
       tc_fence_after();
-      for (int c0 = 0; c0 < ti.n_local; c0 += 16) {
+      for (int c0 = 16 * h; c0 < ti.n_local; c0 += 32) {
         float v[NW][MS][16];
+        const unsigned long long tl0 = prof ? clk() : 0;
 #pragma unroll
         for (int w = 0; w < NW; ++w)
 #pragma unroll
           for (int p = 0; p < MS; ++p) tmem_ld16(tmem + lane_base + (w * MS + p) * NT + c0, v[w][p]);
         tmem_ld_wait();
+        if (prof) pc[8] += clk() - tl0;
         if (!valid || (a.debug & 8)) continue;
         const int jmax = min(16, ti.n_local - c0);
 #pragma unroll
@@ -344,9 +402,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       }
+      const unsigned long long tz0 = prof ? clk() : 0;
       tc_fence_before();
       zero_acc();
+      if (prof) { const unsigned long long t1 = clk(); pc[9] += t1 - tz0; pc[4] += t1 - t0; }
     }
+  }
+  if (prof) {
+    unsigned long long* o = a.prof + ((size_t)(a.epi == kEpiScatter) * 148 + blockIdx.x) * 16;
+    if (warp == 5 && lane == 0) { atomicAdd(o + 0, pc[0]); atomicAdd(o + 1, pc[1]); atomicAdd(o + 2, pc[2]); atomicAdd(o + 7, pc[7]); }
+    if (warp == 0 && lane == 0) { atomicAdd(o + 3, pc[3]); atomicAdd(o + 4, pc[4]); atomicAdd(o + 8, pc[8]); atomicAdd(o + 9, pc[9]); }
+    if (warp == 4 && lane == 0) { atomicAdd(o + 5, pc[5]); }
   }
   tc_fence_before();
   __syncthreads();
@@ -355,12 +421,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 5) tmem_dealloc2(tmem, C::kTmemCols);
 }
 
-template <int NT, int NW>
+template <int NT, int NW, int CL>
 smy_status launch_pair_t(const SsmmArgs& a, cudaStream_t s) {
   using C = PairCfg<NT, NW>;
   static bool configured = false;
   static int num_sms = 0;
-  auto kern = ssmm_pair_kernel<NT, NW>;
+  auto kern = ssmm_pair_kernel<NT, NW, CL>;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return cuda_status(e);
@@ -370,8 +436,8 @@ smy_status launch_pair_t(const SsmmArgs& a, cudaStream_t s) {
     configured = true;
   }
   if (a.max_tiles <= 0) return SMY_OK;
-  const int pairs = a.max_tiles < num_sms / 2 ? a.max_tiles : num_sms / 2;
-  kern<<<2 * pairs, kThreads, C::kSmemBytes, s>>>(a);
+  const int clusters = a.max_tiles < num_sms / CL ? a.max_tiles : num_sms / CL;
+  kern<<<CL * clusters, kPairThreads, C::kSmemBytes, s>>>(a);
   count_launch();
   return cuda_status(cudaGetLastError());
 }

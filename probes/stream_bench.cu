@@ -17,7 +17,7 @@ __device__ __forceinline__ void wait(uint64_t* b, uint32_t ph) {
 }
 
 __global__ void __launch_bounds__(64, 1) stream(const uint8_t* src, size_t per_cta, int chunk, int nchunk_per_stage, int S,
-                                               int evict_first) {
+                                               int evict_first, size_t wrap) {
   extern __shared__ uint8_t raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
   const int stage_bytes = chunk * nchunk_per_stage;
@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(64, 1) stream(const uint8_t* src, size_t per_c
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   __syncthreads();
-  const uint8_t* base = src + (size_t)blockIdx.x * per_cta;
+  const uint8_t* base = src + ((size_t)blockIdx.x * per_cta) % wrap;
   const int iters = (int)(per_cta / stage_bytes);
   uint64_t pol;
   if (evict_first) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(64, 1) stream(const uint8_t* src, size_t per_c
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su(&full[st])), "r"(stage_bytes) : "memory");
       for (int c = 0; c < nchunk_per_stage; ++c)
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-                     ::"r"(su(sm + st * stage_bytes + c * chunk)), "l"(base + (size_t)it * stage_bytes + c * chunk), "r"(chunk),
+                     ::"r"(su(sm + st * stage_bytes + c * chunk)), "l"(src + (((size_t)(base - src) + (size_t)it * stage_bytes + c * chunk) % wrap)), "r"(chunk),
                      "r"(su(&full[st])), "l"(pol) : "memory");
     }
   } else if (threadIdx.x == 32) {
@@ -64,8 +64,9 @@ int main() {
   struct Cfg { int chunk, nchunk, S; } cfgs[] = {
       {18496, 2, 5}, {18496, 2, 3}, {18496, 1, 10}, {16384, 1, 12}, {32768, 1, 6}, {65536, 1, 3},
       {8192, 1, 24}, {4096, 4, 12}, {18496, 2, 2}};
+  for (size_t wrap : {per_cta * 148, (size_t)32 << 20})
   for (auto c : cfgs)
-    for (int ef = 0; ef < 2; ++ef) {
+    for (int ef = 0; ef < 1; ++ef) {
       const int smem = c.chunk * c.nchunk * c.S + 2048;
       if (smem > 232448) continue;
       CK(cudaFuncSetAttribute(stream, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -73,7 +74,7 @@ int main() {
       for (int rep = 0; rep < 3; ++rep) {
         cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
         cudaEventRecord(a);
-        stream<<<148, 64, smem>>>(src, per_cta, c.chunk, c.nchunk, c.S, ef);
+        stream<<<148, 64, smem>>>(src, per_cta, c.chunk, c.nchunk, c.S, ef, wrap);
         cudaEventRecord(b);
         CK(cudaEventSynchronize(b));
         float ms; cudaEventElapsedTime(&ms, a, b);
@@ -81,7 +82,7 @@ int main() {
       }
       const size_t iters = per_cta / ((size_t)c.chunk * c.nchunk);
       const double bytes = 148.0 * iters * c.chunk * c.nchunk;
-      printf("chunk %6d x%d  stages %2d  in-flight %4d KB  %s  %7.3f ms  %7.1f GB/s\n", c.chunk, c.nchunk, c.S,
+      printf("%s chunk %6d x%d  stages %2d  in-flight %4d KB  %s  %7.3f ms  %7.1f GB/s\n", wrap < per_cta * 148 ? "L2  " : "DRAM", c.chunk, c.nchunk, c.S,
              c.chunk * c.nchunk * c.S / 1024, ef ? "evict_first " : "evict_normal", best, bytes / best / 1e6);
     }
   return 0;

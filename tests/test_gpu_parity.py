@@ -304,6 +304,7 @@ def test_moe_layer_parity(smy, case):
     dict(E=4, d=512, f=512, T=512, k=2),                       # tokens/expert >= 64: CTA-pair kernels
     dict(E=8, d=1024, f=768, T=700, k=2, gating="softmax_all"),
     dict(E=2, d=512, f=1024, T=300, k=2, skew=2.0),            # unbalanced experts, ragged tiles
+    dict(E=2, d=512, f=512, T=1000, k=2),                      # >= 2 token tiles per expert: 4-CTA clusters
 ], ids=lambda c: f"E{c['E']}-d{c['d']}-f{c['f']}-T{c['T']}")
 def test_moe_layer_prefill_pair_kernels(smy, case):
     case = dict(case)
