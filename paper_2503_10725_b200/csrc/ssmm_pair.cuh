@@ -9,9 +9,9 @@
 // holds its own 128 compressed rows of A and HALF of the token tile, each half
 // of B is read once for both SMs, and each CTA gathers only half the tokens.
 //
-// Roles per CTA (448 threads): warps 0-3 + 10-13 epilogue, 4 producer (weight-image
-// bulk copies; contiguous B tile via 2D TMA), 5 MMA issuer (leader CTA) or
-// stage relay (peer CTA), 6-9 SEL gather (cp.async).  Stage completion in the
+// Roles per CTA (480 threads): warps 0-3 + 10-13 epilogue, 4 producer (weight-image
+// bulk copies; contiguous B tile via 2D TMA), 5 + 14 MMA issuers (leader CTA) or
+// stage relay (warp 5 of the peer CTA), 6-9 SEL gather (cp.async).  Stage completion in the
 // peer is relayed to the leader's `pfull` barrier; the leader's MMA commits
 // multicast to both CTAs' `empty` / `acc_full`; both epilogues arrive on the
 // leader's `acc_empty`.
@@ -97,7 +97,7 @@ __device__ __forceinline__ void bulk_g2s_mc(void* dst, const void* src, uint32_t
 }
 
 constexpr int kPairEpiWarps = 8;                    // warps 0-3 and 10-13
-constexpr int kPairThreads = 32 * (10 + kPairEpiWarps - 4);  // + producer, MMA, 4 gather
+constexpr int kPairThreads = 32 * (11 + kPairEpiWarps - 4);  // + producer, 2 MMA issuers, 4 gather
 
 template <int NT, int NW>
 struct PairCfg {
@@ -109,7 +109,7 @@ struct PairCfg {
   static constexpr int kStageBytes = (NW * kWStride + kBBytes + kPeerPl + 1023) / 1024 * 1024;
   static constexpr int kAccCols = NW * MS * NT;
   static constexpr int kECol = (kAccCols + 3) / 4 * 4;
-  static constexpr int kColsNeeded = kECol + 8 * NW;
+  static constexpr int kColsNeeded = kECol + 16;            // E: 2 buffers x 2 issuer warps x 4 cols
   static constexpr int kTmemCols = kColsNeeded <= 128 ? 128 : kColsNeeded <= 256 ? 256 : 512;
   static constexpr int kAux = 2048;
   static constexpr int kSmemCap = 232448 - 1024 - kAux;
@@ -154,10 +154,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], gather ? 1 + kGatherThreads : 1);
-      mbar_init(&empty[s], CL / 2);  // every pair's MMA must be done with the slot
+      mbar_init(&empty[s], CL);  // both issuer warps of every pair must be done with the slot
       mbar_init(&pfull[s], 1);
     }
-    mbar_init(acc_full, 1);
+    mbar_init(acc_full, 2);  // both issuer warps' commits
     mbar_init(acc_empty, 2 * kPairEpiWarps);  // every epilogue warp of both CTAs
     fence_mbar_init();
   }
@@ -224,9 +224,18 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 5 || warp == 14) {
     if (leader) {
-      // ========================= MMA issuer (leader CTA) =========================
+      // ==================== MMA issuers (leader CTA, warps 5 and 14) ====================
+      // The per-stage issue work (plane words -> uniform lane masks, descriptors,
+      // elect) costs about as much as the tensor work itself, so two warps split
+      // the MMAs: NW == 2 -> warp mi issues weight mi; NW == 1 -> slot p = mi.
+      // tcgen05.commit tracks the issuing thread's MMAs, so both warps commit and
+      // `empty` / `acc_full` expect two arrivals per pair.  Each warp copies the
+      // E image it uses into its own TMEM columns (ordered before its MMAs).
+      const int mi = warp == 14 ? 1 : 0;
+      const int w = NW == 2 ? mi : 0;
+      constexpr int NP = NW == 2 ? MS : 1;  // slots this warp issues
       constexpr uint32_t idesc = (1u << 2) | (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NT >> 3) << 17) |
                                  ((uint32_t)(256 >> 4) << 24);
       const uint32_t smem_base = smem_u32(smem);
@@ -247,42 +256,36 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
           if (prof) pc[0] += clk() - t0;
           tc_fence_after();
           const uint32_t sbase = smem_base + st * C::kStageBytes;
-          const uint32_t ecol = C::kECol + (it & 1) * 4 * NW;
+          const uint32_t ecol = C::kECol + (it & 1) * 8 + 4 * mi;
+          tc_cp2_elect(tm + ecol, desc_interleave(sbase + w * C::kWStride + kABytes));
+          uint32_t pl[4][8];  // lane planes: words 0-3 this CTA's 128 lanes, 4-7 the peer's
 #pragma unroll
-          for (int w = 0; w < NW; ++w)
-            tc_cp2_elect(tm + ecol + 4 * w, desc_interleave(sbase + w * C::kWStride + kABytes));
-          uint32_t pl[NW][4][8];  // lane planes: words 0-3 this CTA's 128 lanes, 4-7 the peer's
-#pragma unroll
-          for (int w = 0; w < NW; ++w)
-#pragma unroll
-            for (int kb = 0; kb < 4; ++kb) {
-              const uint4 v = *reinterpret_cast<const uint4*>(wsm(st, w) + kABytes + kEBytes + kb * 16);
-              const uint4 u = *reinterpret_cast<const uint4*>(psm(st) + 64 * w + kb * 16);
-              pl[w][kb][0] = __reduce_or_sync(0xffffffffu, v.x);
-              pl[w][kb][1] = __reduce_or_sync(0xffffffffu, v.y);
-              pl[w][kb][2] = __reduce_or_sync(0xffffffffu, v.z);
-              pl[w][kb][3] = __reduce_or_sync(0xffffffffu, v.w);
-              pl[w][kb][4] = __reduce_or_sync(0xffffffffu, u.x);
-              pl[w][kb][5] = __reduce_or_sync(0xffffffffu, u.y);
-              pl[w][kb][6] = __reduce_or_sync(0xffffffffu, u.z);
-              pl[w][kb][7] = __reduce_or_sync(0xffffffffu, u.w);
-            }
+          for (int kb = 0; kb < 4; ++kb) {
+            const uint4 v = *reinterpret_cast<const uint4*>(wsm(st, w) + kABytes + kEBytes + kb * 16);
+            const uint4 u = *reinterpret_cast<const uint4*>(psm(st) + 64 * w + kb * 16);
+            pl[kb][0] = __reduce_or_sync(0xffffffffu, v.x);
+            pl[kb][1] = __reduce_or_sync(0xffffffffu, v.y);
+            pl[kb][2] = __reduce_or_sync(0xffffffffu, v.z);
+            pl[kb][3] = __reduce_or_sync(0xffffffffu, v.w);
+            pl[kb][4] = __reduce_or_sync(0xffffffffu, u.x);
+            pl[kb][5] = __reduce_or_sync(0xffffffffu, u.y);
+            pl[kb][6] = __reduce_or_sync(0xffffffffu, u.z);
+            pl[kb][7] = __reduce_or_sync(0xffffffffu, u.w);
+          }
 #pragma unroll
           for (int kb = 0; kb < 4; ++kb) {
             const int e0 = kb * 32;
             const uint64_t bdesc = desc_sw128(sbase + NW * C::kWStride + (e0 / 64) * (H * 128) + (e0 % 64) * 2);
+            const uint64_t adesc = desc_sw128(sbase + w * C::kWStride + kb * 32);
 #pragma unroll
-            for (int w = 0; w < NW; ++w) {
-              const uint64_t adesc = desc_sw128(sbase + w * C::kWStride + kb * 32);
+            for (int pp = 0; pp < NP; ++pp) {
+              const int p = NW == 2 ? pp : mi;
+              uint32_t mask[8];
 #pragma unroll
-              for (int p = 0; p < MS; ++p) {
-                uint32_t mask[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) mask[q] = p ? ~pl[w][kb][q] : pl[w][kb][q];  // disable lanes idx != p
-                if (!(a.debug & 4))
-                  tc_mma_sp2_elect(tm + (w * MS + p) * NT, adesc, bdesc, idesc | (uint32_t)(kb & 1), mask,
-                                   tm + ecol + 4 * w + (kb & 2));
-              }
+              for (int q = 0; q < 8; ++q) mask[q] = p ? ~pl[kb][q] : pl[kb][q];  // disable lanes idx != p
+              if (!(a.debug & 4))
+                tc_mma_sp2_elect(tm + (w * MS + p) * NT, adesc, bdesc, idesc | (uint32_t)(kb & 1), mask,
+                                 tm + ecol + (kb & 2));
             }
           }
           tc_commit2_mc_elect(&empty[st], (uint16_t)(CL == 4 ? 0xF : 0x3));
@@ -291,7 +294,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
         pc[7] += 1;
       }
       if (prof) pc[2] = clk() - tstart;
-    } else if (lane == 0) {
+    } else if (warp == 5 && lane == 0) {
       // ============== peer: relay "stage complete" to the leader's pfull ==============
       const uint32_t pfull_leader = mapa_shared(smem_u32(pfull), lead_rank);
       uint32_t it = 0;
