@@ -143,6 +143,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
   uint64_t* acc_empty = acc_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
   int32_t* rows = reinterpret_cast<int32_t*>(aux + 1024);
+  unsigned long long* stamp = reinterpret_cast<unsigned long long*>(aux + 512);  // SMY_DEBUG & 128
 
   const uint32_t rank = cluster_rank();
   const uint32_t cta = rank & 1;           // rank inside the MMA pair
@@ -201,7 +202,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
           const int st = it % S;
           const unsigned long long t0 = prof ? clk() : 0;
           mbar_wait_acq_cluster(&empty[st], ((it / S) & 1) ^ 1);
-          if (prof) pc[5] += clk() - t0;
+          if (prof) { const unsigned long long t1 = clk(); pc[5] += t1 - t0; stamp[st] = t1; }
           mbar_arrive_expect_tx(&full[st], stage_bytes);
 #pragma unroll
           for (int w = 0; w < NW; ++w) {
@@ -252,8 +253,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
           const int st = it % S;
           t0 = prof ? clk() : 0;
           mbar_wait(&full[st], (it / S) & 1);
+          if (prof) { const unsigned long long t1 = clk(); pc[0] += t1 - t0; pc[12] += t1 - stamp[st]; t0 = t1; }
           mbar_wait_acq_cluster(&pfull[st], (it / S) & 1);
-          if (prof) pc[0] += clk() - t0;
+          if (prof) pc[6] += clk() - t0;
           tc_fence_after();
           const uint32_t sbase = smem_base + st * C::kStageBytes;
           const uint32_t ecol = C::kECol + (it & 1) * 8 + 4 * mi;
@@ -308,32 +310,44 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
     }
   } else if (warp >= 6 && warp < 10) {
     // ============ SEL gather of this CTA's half of the token rows (cp.async) ============
+    // Thread tb owns the 16-B chunk ch = tb % 16 of rows tb/16 + 8i (i < H/8) of
+    // the tile for every k-stage, so the row lookups, source pointers and
+    // swizzled destination offsets are computed once per tile; a stage is then
+    // H/8 (address add + cp.async) per thread.
     if (gather) {
       const int tb = threadIdx.x - 6 * 32;
-      constexpr int CHUNKS = H * 16;
+      static_assert(kGatherThreads == 128 && H % 8 == 0, "gather mapping");
+      constexpr int NI = H / 8;
+      const int r0 = tb >> 4, ch = tb & 15;
+      const uint32_t dst0 = (uint32_t)((ch >> 3) * (H * 128) + r0 * 128 + (((ch & 7) ^ r0) << 4));
       uint32_t it = 0;
       TileInfo ti;
       for (int tile = pair0; decode_tile(a, NT * (CL / 2), tile, ti) && (pair_tile(ti), true); tile += pstep) {
-        named_bar_sync(1, kGatherThreads);
-        for (int i = tb; i < H; i += kGatherThreads) {
-          const int t = (int)cta * H + i;
-          rows[i] = t < ti.n_local ? a.sel_in[ti.row0 + ti.t0 + t] : -1;
+        const uint16_t* src[NI];
+        uint32_t valid = 0;
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          const int t = (int)cta * H + r0 + 8 * i;
+          const int rid = t < ti.n_local ? a.sel_in[ti.row0 + ti.t0 + t] : -1;
+          src[i] = a.x + (rid >= 0 ? (int64_t)rid * a.ldx : 0) + ch * 8;
+          valid |= (rid >= 0 ? 1u : 0u) << i;
         }
-        named_bar_sync(1, kGatherThreads);
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % S;
+          unsigned long long tg0 = prof ? clk() : 0;
           mbar_wait_acq_cluster(&empty[st], ((it / S) & 1) ^ 1);
+          if (prof) { const unsigned long long t1 = clk(); pc[10] += t1 - tg0; tg0 = t1; }
           const int64_t kcol0 = (int64_t)k * 128;
-          uint8_t* bs = bsm(st);
-          for (int idx = tb; idx < ((a.debug & 1) ? 0 : CHUNKS); idx += kGatherThreads) {
-            const int row = idx / 16, ch = idx % 16;
-            const int atom = ch >> 3, c8 = ch & 7;
-            const int rid = rows[row];
-            const uint16_t* srcp = rid >= 0 ? a.x + (int64_t)rid * a.ldx + kcol0 + ch * 8 : a.x;
-            uint8_t* dst = bs + atom * (H * 128) + (row >> 3) * 1024 + (row & 7) * 128 + ((c8 ^ (row & 7)) << 4);
-            cp_async16(dst, srcp, rid >= 0 ? 16u : 0u);
+          const uint32_t bs = smem_u32(bsm(st)) + dst0;
+          if (!(a.debug & 1)) {
+#pragma unroll
+            for (int i = 0; i < NI; ++i)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(bs + 1024u * i),
+                           "l"(src[i] + ((valid >> i) & 1u ? kcol0 : 0)), "r"((valid >> i) & 1u ? 16u : 0u)
+                           : "memory");
           }
           cp_async_mbar_arrive_noinc(&full[st]);
+          if (prof) pc[11] += clk() - tg0;
         }
       }
     }
@@ -413,7 +427,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
   }
   if (prof) {
     unsigned long long* o = a.prof + ((size_t)(a.epi == kEpiScatter) * 148 + blockIdx.x) * 16;
-    if (warp == 5 && lane == 0) { atomicAdd(o + 0, pc[0]); atomicAdd(o + 1, pc[1]); atomicAdd(o + 2, pc[2]); atomicAdd(o + 7, pc[7]); }
+    if (warp == 5 && lane == 0) {
+      atomicAdd(o + 0, pc[0]); atomicAdd(o + 1, pc[1]); atomicAdd(o + 2, pc[2]); atomicAdd(o + 6, pc[6]);
+      atomicAdd(o + 7, pc[7]); atomicAdd(o + 12, pc[12]);
+    }
+    if (warp == 6 && lane == 0) { atomicAdd(o + 10, pc[10]); atomicAdd(o + 11, pc[11]); }
     if (warp == 0 && lane == 0) { atomicAdd(o + 3, pc[3]); atomicAdd(o + 4, pc[4]); atomicAdd(o + 8, pc[8]); atomicAdd(o + 9, pc[9]); }
     if (warp == 4 && lane == 0) { atomicAdd(o + 5, pc[5]); }
   }
