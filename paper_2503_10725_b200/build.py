@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
                  "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-                 "-DSMY_BUILD"]
+                 "-DSMY_BUILD"] + os.environ.get("SMY_EXTRA_CFLAGS", "").split()
 
 
 def sources():

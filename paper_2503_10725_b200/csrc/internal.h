@@ -31,6 +31,8 @@ enum EpiKind { kEpiCompact = 0, kEpiSiluMul = 1, kEpiScatter = 2 };
 
 struct SsmmArgs {
   CUtensorMap tmap_x;               // contiguous x rows: 2D TMA box 64 x NT, 128B swizzle
+  CUtensorMap tmap_w;       // pair kernel: all weight images as rows of 128 B from `wbase`
+  const uint8_t* wbase;
   const uint8_t* img0[kMaxGroups];  // weight image per group (gate / single)
   const uint8_t* img1[kMaxGroups];  // up weight image (SILU_MUL only)
   int num_groups;
@@ -65,6 +67,7 @@ int ssmm_pick_ksplit(int64_t tiles, int k_stages);
 
 // Tensor map over a token-major bf16 activation matrix [rows x cols] (ld elements):
 // boxes of 64 elements x box_rows rows, 128-byte swizzle (the UMMA K-major atom).
+smy_status make_w_tmap(CUtensorMap* map, const void* base, int64_t rows, int box_rows);
 smy_status make_x_tmap(CUtensorMap* map, const void* x, int64_t cols, int64_t rows, int64_t ld, int box_rows);
 
 struct SsmmPlan {

@@ -162,7 +162,7 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   const int mt_gu = cl_gu ? ggu.m_tiles / 2 : ggu.m_tiles;
   const int mt_dn = cl_dn ? gdn.m_tiles / 2 : gdn.m_tiles;
   // the routing scan counts tiles per expert in units of the launch's token span
-  const int nts[2] = {cl_gu == 4 ? 2 * nt_gu : nt_gu, cl_dn == 4 ? 2 * nt_dn : nt_dn};
+  const int nts[2] = {nt_gu, nt_dn};
   const int mts[2] = {mt_gu, mt_dn * ks_dn};
   int32_t* prefix_gu = w.prefix;
   int32_t* prefix_dn = w.prefix + (E + 1);

@@ -30,12 +30,10 @@ extern template smy_status launch_t<16,1,16,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<32,2,4,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<16,2,8,1>(const SsmmArgs&, cudaStream_t);
 
-extern template smy_status launch_pair_t<64, 2, 2>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<112, 2, 2>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<128, 1, 2>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<224, 1, 2>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<112, 2, 4>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<224, 1, 4>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<64, 2>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<112, 2>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<128, 1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<224, 1>(const SsmmArgs&, cudaStream_t);
 
 namespace {
 struct Entry { int nt, nw, ms, rep; smy_status (*fn)(const SsmmArgs&, cudaStream_t); };
@@ -84,22 +82,49 @@ int ssmm_pair_cluster(int nt, int nw, int ms, int rep, int m_tiles, int64_t toke
   if (debug_flags() & 16) return 0;  // SMY_DEBUG=16: force the single-CTA kernel
   if (ms != 2 || rep != 1 || (m_tiles & 1) || tokens_per_group < 64) return 0;
   if (!(nw == 2 ? (nt == 64 || nt == 112) : (nt == 128 || nt == 224))) return 0;
-  // two MMA pairs share each weight stage when an expert has >= 2 token tiles
-  // (4-CTA multicast clusters measured 2x slower on B200: opt-in via SMY_DEBUG=64)
-  const bool quad = (debug_flags() & 64) && tokens_per_group >= 2 * nt && (nt == 112 || nt == 224);
-  return quad ? 4 : 2;
+  // (4-CTA clusters sharing weight stages by multicast measured 2x slower on
+  // B200 -- probes/mcast_bench.cu -- and were removed)
+  return 2;
 }
 
 smy_status ssmm_launch_pair(const SsmmArgs& a0, int nt, int nw, int cl, cudaStream_t s) {
   SsmmArgs a = a0;
   a.debug = debug_flags();
   a.prof = (a.debug & 128) ? debug_prof_buffer(148) : nullptr;
-  if (cl == 4 && nw == 2 && nt == 112) return launch_pair_t<112, 2, 4>(a, s);
-  if (cl == 4 && nw == 1 && nt == 224) return launch_pair_t<224, 1, 4>(a, s);
-  if (nw == 2 && nt == 64) return launch_pair_t<64, 2, 2>(a, s);
-  if (nw == 2 && nt == 112) return launch_pair_t<112, 2, 2>(a, s);
-  if (nw == 1 && nt == 128) return launch_pair_t<128, 1, 2>(a, s);
-  if (nw == 1 && nt == 224) return launch_pair_t<224, 1, 2>(a, s);
+  if (cl != 2 || a.planes != 1 || (a.block & 127)) {
+    set_last_error("ssmm: pair kernel needs (N,M) = (1,2) tiles of 128-B rows");
+    return SMY_E_CONFIG;
+  }
+  // one tensor map over every weight image of the launch (rows of 128 B)
+  uintptr_t lo = UINTPTR_MAX, hi = 0;
+  const size_t img_bytes = (size_t)a.m_tiles * a.k_stages * a.block;
+  for (int g = 0; g < a.num_groups; ++g)
+    for (int w = 0; w < nw; ++w) {
+      const uintptr_t p = reinterpret_cast<uintptr_t>(w ? a.img1[g] : a.img0[g]);
+      if (!p) continue;
+      if (p < lo) lo = p;
+      if (p + img_bytes > hi) hi = p + img_bytes;
+    }
+  if (hi <= lo) return SMY_OK;
+  for (int g = 0; g < a.num_groups; ++g)
+    for (int w = 0; w < nw; ++w) {
+      const uintptr_t p = reinterpret_cast<uintptr_t>(w ? a.img1[g] : a.img0[g]);
+      if (p && ((p - lo) & 127)) {
+        set_last_error("ssmm: weight images must be 128-B aligned");
+        return SMY_E_CONFIG;
+      }
+    }
+  if ((hi - lo) / 128 >= ((uint64_t)1 << 31)) {
+    set_last_error("ssmm: weight images span more than 256 GB");
+    return SMY_E_CONFIG;
+  }
+  a.wbase = reinterpret_cast<const uint8_t*>(lo);
+  smy_status st = make_w_tmap(&a.tmap_w, a.wbase, (int64_t)((hi - lo) / 128), (kABytes + kEBytes + 64 + 127) / 128);
+  if (st != SMY_OK) return st;
+  if (nw == 2 && nt == 64) return launch_pair_t<64, 2>(a, s);
+  if (nw == 2 && nt == 112) return launch_pair_t<112, 2>(a, s);
+  if (nw == 1 && nt == 128) return launch_pair_t<128, 1>(a, s);
+  if (nw == 1 && nt == 224) return launch_pair_t<224, 1>(a, s);
   set_last_error("ssmm: unsupported pair (nt, nw)");
   return SMY_E_CONFIG;
 }

@@ -1,11 +1,9 @@
-// Explicit instantiations of the CTA-pair SSMM kernel (cluster of 2 or 4).
+// Explicit instantiations of the CTA-pair SSMM kernel.
 #include "ssmm_pair.cuh"
 
 namespace smy {
-template smy_status launch_pair_t<64, 2, 2>(const SsmmArgs&, cudaStream_t);
-template smy_status launch_pair_t<112, 2, 2>(const SsmmArgs&, cudaStream_t);
-template smy_status launch_pair_t<128, 1, 2>(const SsmmArgs&, cudaStream_t);
-template smy_status launch_pair_t<224, 1, 2>(const SsmmArgs&, cudaStream_t);
-template smy_status launch_pair_t<112, 2, 4>(const SsmmArgs&, cudaStream_t);
-template smy_status launch_pair_t<224, 1, 4>(const SsmmArgs&, cudaStream_t);
+template smy_status launch_pair_t<64, 2>(const SsmmArgs&, cudaStream_t);
+template smy_status launch_pair_t<112, 2>(const SsmmArgs&, cudaStream_t);
+template smy_status launch_pair_t<128, 1>(const SsmmArgs&, cudaStream_t);
+template smy_status launch_pair_t<224, 1>(const SsmmArgs&, cudaStream_t);
 }  // namespace smy

@@ -9,12 +9,14 @@
 // holds its own 128 compressed rows of A and HALF of the token tile, each half
 // of B is read once for both SMs, and each CTA gathers only half the tokens.
 //
-// Roles per CTA (480 threads): warps 0-3 + 10-13 epilogue, 4 producer (weight-image
-// bulk copies; contiguous B tile via 2D TMA), 5 + 14 MMA issuers (leader CTA) or
-// stage relay (warp 5 of the peer CTA), 6-9 SEL gather (cp.async).  Stage completion in the
-// peer is relayed to the leader's `pfull` barrier; the leader's MMA commits
-// multicast to both CTAs' `empty` / `acc_full`; both epilogues arrive on the
-// leader's `acc_empty`.
+// Roles per CTA (480 threads): warps 0-3 + 10-13 epilogue, 4 producer (TMA
+// loads of the weight image and the contiguous B half), 5 + 14 MMA issuers
+// (leader CTA) or gather relay (warp 5 of the peer), 6-9 SEL gather
+// (cp.async).  Both CTAs' TMA loads use .cta_group::2 and complete on the
+// LEADER's `full` barrier, so the peer's weights / contiguous B need no relay;
+// only the peer's cp.async gather is forwarded (peer-local `full` -> one remote
+// arrive).  The leader's MMA commits multicast to both CTAs' `empty` /
+// `acc_full`; both epilogues arrive on the leader's `acc_empty`.
 #include "ssmm_kernel.cuh"
 
 namespace smy {
@@ -35,9 +37,32 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
 __device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar), done = 0;
   do {
+#ifdef SMY_SPIN_CLUSTER_WAIT
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+#endif
+  } while (!done);
+}
+// non-suspending poll: the stage relay forwards completions with minimum latency
+__device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar), done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
         : "r"(addr), "r"(parity)
@@ -85,14 +110,14 @@ __device__ __forceinline__ void tc_commit2_mc_elect(uint64_t* bar, uint16_t cta_
       : "memory");
 }
 
-// bulk copy global -> the same smem offset in every CTA of cta_mask; each
-// destination CTA's mbarrier (same offset) receives the complete_tx
-__device__ __forceinline__ void bulk_g2s_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint16_t cta_mask,
-                                            uint64_t policy) {
+// TMA 2D tile load into this CTA's shared memory whose complete_tx lands on
+// the pair leader's mbarrier (`bar` is a shared::cluster address)
+__device__ __forceinline__ void tma2d_pair(void* dst, const CUtensorMap* map, int c0, int c1, uint32_t bar,
+                                           uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
-      " [%0], [%1], %2, [%3], %4, %5;" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(cta_mask), "l"(policy)
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar), "l"(policy)
       : "memory");
 }
 
@@ -103,7 +128,8 @@ template <int NT, int NW>
 struct PairCfg {
   static constexpr int MS = 2;
   static constexpr int kHalf = NT / 2;                      // tokens per CTA
-  static constexpr int kWStride = 19456;                    // A|E|planes
+  static constexpr int kWStride = 19456;                    // A|E|planes (kWRows rows of 128 B)
+  static constexpr int kWRows = (kABytes + kEBytes + 64 + 127) / 128;  // TMA box rows of one weight tile
   static constexpr int kBBytes = kHalf * 256;               // 2 K-atoms x kHalf rows x 128 B
   static constexpr int kPeerPl = 128;                       // the peer m-tile's index planes (leader)
   static constexpr int kStageBytes = (NW * kWStride + kBBytes + kPeerPl + 1023) / 1024 * 1024;
@@ -121,15 +147,10 @@ struct PairCfg {
   static_assert(NT % 16 == 0 && (NT / 2) % 8 == 0 && NT >= 32 && NT <= 256, "UMMA N (cta_group::2) / 8-row halves");
 };
 
-// CL = 2: one MMA pair per cluster.  CL = 4: two MMA pairs (ranks {0,1},
-// {2,3}) on adjacent token tiles of the same weight m-tiles; each weight stage
-// is fetched once and multicast to both pairs (ranks c and c+2), halving the
-// weight requests and L2 reads per SM.
-template <int NT, int NW, int CL>
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
+template <int NT, int NW>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     ssmm_pair_kernel(const __grid_constant__ SsmmArgs a) {
   using C = PairCfg<NT, NW>;
-  static_assert(CL == 2 || CL == 4, "cluster of one or two MMA pairs");
   constexpr int S = C::kStages;
   constexpr int MS = 2;
   constexpr int H = C::kHalf;
@@ -138,25 +159,20 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
   uint8_t* aux = smem + S * C::kStageBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(aux);
   uint64_t* empty = full + S;
-  uint64_t* pfull = empty + S;   // leader: the peer's stage is complete
-  uint64_t* acc_full = pfull + S;
+  uint64_t* acc_full = empty + S;
   uint64_t* acc_empty = acc_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
-  int32_t* rows = reinterpret_cast<int32_t*>(aux + 1024);
-  unsigned long long* stamp = reinterpret_cast<unsigned long long*>(aux + 512);  // SMY_DEBUG & 128
 
-  const uint32_t rank = cluster_rank();
-  const uint32_t cta = rank & 1;           // rank inside the MMA pair
-  const uint32_t pi = rank >> 1;           // which pair of the cluster
-  const uint32_t lead_rank = rank & ~1u;   // the pair's leader
+  const uint32_t cta = cluster_rank();
   const bool leader = cta == 0;
   const bool gather = a.sel_in != nullptr;
   const int warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], gather ? 1 + kGatherThreads : 1);
-      mbar_init(&empty[s], CL);  // both issuer warps of every pair must be done with the slot
-      mbar_init(&pfull[s], 1);
+      // leader: its producer's expect_tx (all TMA bytes of both CTAs) + its gather
+      // threads + the peer's gather relay; peer: its gather threads (relayed)
+      mbar_init(&full[s], leader ? 1 + (gather ? kGatherThreads + 1 : 0) : (gather ? kGatherThreads : 1));
+      mbar_init(&empty[s], 2);  // both issuer warps' commits
     }
     mbar_init(acc_full, 2);  // both issuer warps' commits
     mbar_init(acc_empty, 2 * kPairEpiWarps);  // every epilogue warp of both CTAs
@@ -172,47 +188,40 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
   auto bsm = [&](int st) { return smem + st * C::kStageBytes + NW * C::kWStride; };
   auto psm = [&](int st) { return smem + st * C::kStageBytes + NW * C::kWStride + C::kBBytes; };
   const int ks = a.k_stages;
-  const int pair0 = blockIdx.x / CL, pstep = gridDim.x / CL;
-  // cluster tile -> this pair's token tile
-  auto pair_tile = [&](TileInfo& ti) {
-    if (CL == 4) {
-      ti.t0 += (int)pi * NT;
-      ti.n_local = min(NT, ti.n_local - (int)pi * NT);  // may be <= 0: the pair idles through the tile
-    }
-  };
+  const int pair0 = blockIdx.x >> 1, pstep = gridDim.x >> 1;
+  const uint32_t full_lead = mapa_shared(smem_u32(full), 0);  // the leader's full[0], cluster window
 
   const bool prof = a.prof != nullptr;
   unsigned long long pc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   auto clk = []() { unsigned long long c; asm volatile("mov.u64 %0, %%clock64;" : "=l"(c)); return c; };
   if (warp == 4) {
-    // ========= producer: own weight image + (leader) peer planes + contiguous B half =========
+    // ========= producer: own weight tiles + contiguous B half (TMA, completing on
+    // the leader's full) + (leader) the peer m-tile's index planes =========
     if (lane == 0) {
-      const uint32_t wbytes = kABytes + kEBytes + 64;
-      const uint32_t stage_bytes =
-          NW * wbytes + (leader ? NW * 64u : 0u) + (gather ? 0u : (uint32_t)C::kBBytes);
+      const uint32_t wbytes = (a.debug & 2) ? 0u : (uint32_t)C::kWRows * 128;
+      const uint32_t pair_bytes = 2 * (NW * wbytes + (gather ? 0u : (uint32_t)C::kBBytes)) + NW * 64u;
       const uint64_t pol_w = a.weights_stream ? policy_evict_first() : policy_evict_normal();
       const uint64_t pol_x = policy_evict_last();
+      const int brows = a.block >> 7;
       uint32_t it = 0;
       TileInfo ti;
-      for (int tile = pair0; decode_tile(a, NT * (CL / 2), tile, ti) && (pair_tile(ti), true); tile += pstep) {
+      for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep) {
         const int m_own = 2 * ti.m_tile + (int)cta, m_peer = 2 * ti.m_tile + 1;
         const uint8_t* src[2] = {a.img0[ti.g], NW == 2 ? a.img1[ti.g] : nullptr};
+        int wrow[2];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) wrow[w] = (int)((src[w] - a.wbase) >> 7) + m_own * ks * brows;
         const int xrow = ti.row0 + ti.t0 + (int)cta * H;
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % S;
           const unsigned long long t0 = prof ? clk() : 0;
           mbar_wait_acq_cluster(&empty[st], ((it / S) & 1) ^ 1);
-          if (prof) { const unsigned long long t1 = clk(); pc[5] += t1 - t0; stamp[st] = t1; }
-          mbar_arrive_expect_tx(&full[st], stage_bytes);
+          if (prof) pc[5] += clk() - t0;
+          const uint32_t bar = full_lead + st * 8;
+          if (leader) mbar_arrive_expect_tx(&full[st], pair_bytes);
 #pragma unroll
           for (int w = 0; w < NW; ++w) {
-            if (CL == 4) {  // the two pairs alternate issuing each k-stage for both of them
-              if ((k & 1) == (int)pi)
-                bulk_g2s_mc(wsm(st, w), src[w] + ((size_t)m_own * ks + k) * a.block, wbytes, &full[st],
-                            (uint16_t)((1u << cta) | (1u << (cta + 2))), pol_w);
-            } else {
-              bulk_g2s(wsm(st, w), src[w] + ((size_t)m_own * ks + k) * a.block, wbytes, &full[st], pol_w);
-            }
+            if (!(a.debug & 2)) tma2d_pair(wsm(st, w), &a.tmap_w, 0, wrow[w] + k * brows, bar, pol_w);
             if (leader)
               bulk_g2s(psm(st) + 64 * w, src[w] + ((size_t)m_peer * ks + k) * a.block + kABytes + kEBytes, 64,
                        &full[st], pol_w);
@@ -220,7 +229,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
           if (!gather) {
 #pragma unroll
             for (int atom = 0; atom < 2; ++atom)
-              tma_tile2d(bsm(st) + atom * (H * 128), &a.tmap_x, k * 128 + atom * 64, xrow, &full[st], pol_x);
+              tma2d_pair(bsm(st) + atom * (H * 128), &a.tmap_x, k * 128 + atom * 64, xrow, bar, pol_x);
           }
         }
       }
@@ -244,7 +253,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
       uint32_t it = 0, tcount = 0;
       TileInfo ti;
       const unsigned long long tstart = prof ? clk() : 0;
-      for (int tile = pair0; decode_tile(a, NT * (CL / 2), tile, ti) && (pair_tile(ti), true); tile += pstep, ++tcount) {
+      for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep, ++tcount) {
         unsigned long long t0 = prof ? clk() : 0;
         mbar_wait_acq_cluster(acc_empty, tcount & 1);  // both epilogues drained and re-zeroed
         if (prof) pc[1] += clk() - t0;
@@ -252,10 +261,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % S;
           t0 = prof ? clk() : 0;
-          mbar_wait(&full[st], (it / S) & 1);
-          if (prof) { const unsigned long long t1 = clk(); pc[0] += t1 - t0; pc[12] += t1 - stamp[st]; t0 = t1; }
-          mbar_wait_acq_cluster(&pfull[st], (it / S) & 1);
-          if (prof) pc[6] += clk() - t0;
+          mbar_wait_acq_cluster(&full[st], (it / S) & 1);  // both CTAs' stage (peer bytes + relay)
+          if (prof) pc[0] += clk() - t0;
           tc_fence_after();
           const uint32_t sbase = smem_base + st * C::kStageBytes;
           const uint32_t ecol = C::kECol + (it & 1) * 8 + 4 * mi;
@@ -290,22 +297,21 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
                                  tm + ecol + (kb & 2));
             }
           }
-          tc_commit2_mc_elect(&empty[st], (uint16_t)(CL == 4 ? 0xF : 0x3));
+          tc_commit2_mc_elect(&empty[st], 0x3);
         }
-        tc_commit2_mc_elect(acc_full, (uint16_t)(0x3u << (2 * pi)));
+        tc_commit2_mc_elect(acc_full, 0x3);
         pc[7] += 1;
       }
       if (prof) pc[2] = clk() - tstart;
-    } else if (warp == 5 && lane == 0) {
-      // ============== peer: relay "stage complete" to the leader's pfull ==============
-      const uint32_t pfull_leader = mapa_shared(smem_u32(pfull), lead_rank);
+    } else if (warp == 5 && lane == 0 && gather) {
+      // ============== peer: forward "gather landed" to the leader's full ==============
       uint32_t it = 0;
       TileInfo ti;
-      for (int tile = pair0; decode_tile(a, NT * (CL / 2), tile, ti) && (pair_tile(ti), true); tile += pstep)
+      for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep)
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % S;
-          mbar_wait(&full[st], (it / S) & 1);
-          mbar_arrive_cluster(pfull_leader + st * 8);
+          mbar_spin(&full[st], (it / S) & 1);
+          mbar_arrive_cluster(full_lead + st * 8);
         }
     }
   } else if (warp >= 6 && warp < 10) {
@@ -322,7 +328,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
       const uint32_t dst0 = (uint32_t)((ch >> 3) * (H * 128) + r0 * 128 + (((ch & 7) ^ r0) << 4));
       uint32_t it = 0;
       TileInfo ti;
-      for (int tile = pair0; decode_tile(a, NT * (CL / 2), tile, ti) && (pair_tile(ti), true); tile += pstep) {
+      for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep) {
         const uint16_t* src[NI];
         uint32_t valid = 0;
 #pragma unroll
@@ -359,7 +365,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
     const int q = warp & 3;
     const int h = warp >= 10 ? 1 : 0;
     const uint32_t lane_base = (uint32_t)(32 * q) << 16;
-    const uint32_t acc_empty_leader = mapa_shared(smem_u32(acc_empty), lead_rank);
+    const uint32_t acc_empty_leader = mapa_shared(smem_u32(acc_empty), 0);
     auto zero_acc = [&]() {
       // the same (weight, slot, chunk) split as the reads: regions start at j*NT,
       // and NT (e.g. 112) need not be a multiple of 32
@@ -373,7 +379,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
     zero_acc();
     uint32_t tcount = 0;
     TileInfo ti;
-    for (int tile = pair0; decode_tile(a, NT * (CL / 2), tile, ti) && (pair_tile(ti), true); tile += pstep, ++tcount) {
+    for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep, ++tcount) {
       const int m_own = 2 * ti.m_tile + (int)cta;
       const int cr = m_own * kTileM + 32 * q + lane;
       const bool valid = cr < a.R;
@@ -428,8 +434,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
   if (prof) {
     unsigned long long* o = a.prof + ((size_t)(a.epi == kEpiScatter) * 148 + blockIdx.x) * 16;
     if (warp == 5 && lane == 0) {
-      atomicAdd(o + 0, pc[0]); atomicAdd(o + 1, pc[1]); atomicAdd(o + 2, pc[2]); atomicAdd(o + 6, pc[6]);
-      atomicAdd(o + 7, pc[7]); atomicAdd(o + 12, pc[12]);
+      atomicAdd(o + 0, pc[0]); atomicAdd(o + 1, pc[1]); atomicAdd(o + 2, pc[2]); atomicAdd(o + 7, pc[7]);
     }
     if (warp == 6 && lane == 0) { atomicAdd(o + 10, pc[10]); atomicAdd(o + 11, pc[11]); }
     if (warp == 0 && lane == 0) { atomicAdd(o + 3, pc[3]); atomicAdd(o + 4, pc[4]); atomicAdd(o + 8, pc[8]); atomicAdd(o + 9, pc[9]); }
@@ -442,12 +447,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kPairThreads, 1)
   if (warp == 5) tmem_dealloc2(tmem, C::kTmemCols);
 }
 
-template <int NT, int NW, int CL>
+template <int NT, int NW>
 smy_status launch_pair_t(const SsmmArgs& a, cudaStream_t s) {
   using C = PairCfg<NT, NW>;
   static bool configured = false;
   static int num_sms = 0;
-  auto kern = ssmm_pair_kernel<NT, NW, CL>;
+  auto kern = ssmm_pair_kernel<NT, NW>;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return cuda_status(e);
@@ -457,8 +462,8 @@ smy_status launch_pair_t(const SsmmArgs& a, cudaStream_t s) {
     configured = true;
   }
   if (a.max_tiles <= 0) return SMY_OK;
-  const int clusters = a.max_tiles < num_sms / CL ? a.max_tiles : num_sms / CL;
-  kern<<<CL * clusters, kPairThreads, C::kSmemBytes, s>>>(a);
+  const int pairs = a.max_tiles < num_sms / 2 ? a.max_tiles : num_sms / 2;
+  kern<<<2 * pairs, kPairThreads, C::kSmemBytes, s>>>(a);
   count_launch();
   return cuda_status(cudaGetLastError());
 }

@@ -44,4 +44,28 @@ smy_status make_x_tmap(CUtensorMap* map, const void* x, int64_t cols, int64_t ro
   return SMY_OK;
 }
 
+// The weight images of one launch viewed as a single 2D tensor of 128-byte rows
+// starting at `base` (the lowest image address): a weight tile (A | E | planes)
+// is a box of `box_rows` rows, no swizzle (the image already holds the smem
+// layout).  Images need only be 128-B aligned relative to `base`.
+smy_status make_w_tmap(CUtensorMap* map, const void* base, int64_t rows, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) {
+    set_last_error("cuTensorMapEncodeTiled unavailable");
+    return SMY_E_CUDA;
+  }
+  const cuuint64_t dims[2] = {64, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_last_error("cuTensorMapEncodeTiled failed for the weight images");
+    return SMY_E_CUDA;
+  }
+  return SMY_OK;
+}
+
 }  // namespace smy

@@ -36,10 +36,8 @@ for name, a in zip(("gate/up", "down"), A):
     lead = a[0::2]
     t = max(lead[:, 7].mean(), 1e-9)
     print(f"{model} T={T} {name}: kcycles per CTA per layer call; tiles/pair {lead[:, 7].mean() * 1e3:.1f}")
-    print("  MMA warp: total %.1f  wait_full(own) %.1f  wait_pfull(peer) %.1f  wait_acc_empty %.1f  issue %.1f"
-          % (lead[:, 2].mean(), lead[:, 0].mean(), lead[:, 6].mean(), lead[:, 1].mean(),
-             (lead[:, 2] - lead[:, 0] - lead[:, 6] - lead[:, 1]).mean()))
-    print("  stage fill latency (producer issue -> MMA sees full), mean per stage %.2f" % (lead[:, 12].sum() / max(1, (lead[:, 7] > 0).sum()) / 1e3 * 0 + lead[:, 12].mean()))
+    print("  MMA warp: total %.1f  wait_full %.1f  wait_acc_empty %.1f  issue %.1f"
+          % (lead[:, 2].mean(), lead[:, 0].mean(), lead[:, 1].mean(), (lead[:, 2] - lead[:, 0] - lead[:, 1]).mean()))
     print("  gather warp: wait_empty %.1f  issue %.1f (leader) / %.1f %.1f (peer)"
           % (lead[:, 10].mean(), lead[:, 11].mean(), a[1::2, 10].mean(), a[1::2, 11].mean()))
     print("  epilogue: wait_acc_full %.1f  work %.1f (tmem_ld %.1f, zero %.1f)   producer wait_empty %.1f"
