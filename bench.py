@@ -393,8 +393,8 @@ def run_ours(args):
              "peak_source": f"2 x {src} bf16 dense burst ({bf16_burst} TF/s)"} if tensor_bound else
             {"bound": "hbm", "achieved": ach_gbs, "peak": hbm, "unit": "GB/s", "frac": ach_gbs / hbm,
              "traffic": None, "peak_source": f"{src} hbm_gbs"})
-    roof["traffic"] = ncu_traffic(model, T, "ssmm_kernel<%d, 2, 2, 1>" % nt_gate_up(T * k // E))
-    roof.update({"kernel": "ssmm_kernel gate/up (NW=2, fused SiLU*up)", "per_launch_ms": ph_ms[2],
+    roof["traffic"] = ncu_traffic(model, T, gate_up_kernel(T * k // E, f))
+    roof.update({"kernel": gate_up_kernel(T * k // E, f) + " gate/up (fused SiLU*up)", "per_launch_ms": ph_ms[2],
                  "algorithmic_flops": flops_gu, "algorithmic_bytes": bytes_gu,
                  "other_view": ({"achieved_gbs": ach_gbs, "hbm_frac": ach_gbs / hbm} if tensor_bound else
                                 {"achieved_tflops": ach_tf, "sparse_frac": ach_tf / sparse_peak})})
@@ -436,6 +436,16 @@ def nt_gate_up(tokens_per_expert):
         if nt >= tokens_per_expert:
             return nt
     return 112
+
+
+def gate_up_kernel(tokens_per_expert, f):
+    """Name of the fused gate/up SSMM kernel the library launches (ssmm.cu:
+    ssmm_pick_nt / ssmm_pair_cluster) -- the key into the ncu summary."""
+    nt = nt_gate_up(tokens_per_expert)
+    m_tiles = (f // 2 + 127) // 128        # (1,2,V): f/2 compressed rows per weight
+    if tokens_per_expert >= 64 and nt in (64, 112) and m_tiles % 2 == 0:
+        return "ssmm_pair_kernel<%d, 2>" % nt
+    return "ssmm_kernel<%d, 2, 2, 1>" % nt
 
 
 def ncu_traffic(model, T, kernel):
