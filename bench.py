@@ -340,24 +340,51 @@ def run_ours(args):
                "down_hbm_frac": dn_bytes / (dpm[3] * 1e-3) / 1e9 / hbm_,
                "layer_hbm_frac": (gu_bytes + dn_bytes) / (dms * 1e-3) / 1e9 / hbm_}
 
-    # ---------------- end to end: host buffers, copies inside the timed region
+    # ---------------- end to end through the public call, from pinned host memory:
+    # every step uploads its x + logits and downloads its fp32 output inside the
+    # timed region; as in a serving loop, step s+1's upload and step s-1's
+    # download run on copy streams beside step s's compute (double-buffered
+    # device tensors, event-ordered), so e2e = max(PCIe, compute) when they overlap.
+    nb = 2
     x_h = x.cpu().pin_memory()
     lg_h = lg.cpu().pin_memory()
-    out_h = torch.empty(T, d, dtype=torch.float32).pin_memory()
-    for _ in range(max(2, args.warmup // 2)):
-        x.copy_(x_h, non_blocking=True)
-        lg.copy_(lg_h, non_blocking=True)
-        layer(x, lg, out)
-        out_h.copy_(out, non_blocking=True)
+    out_h = [torch.empty(T, d, dtype=torch.float32).pin_memory() for _ in range(nb)]
+    xs = [x] + [torch.empty_like(x) for _ in range(nb - 1)]
+    lgs = [lg] + [torch.empty_like(lg) for _ in range(nb - 1)]
+    outs = [out] + [torch.empty_like(out) for _ in range(nb - 1)]
+    h2d, d2h = torch.cuda.Stream(device), torch.cuda.Stream(device)
+    ev_in = [torch.cuda.Event() for _ in range(nb)]
+    ev_done = [torch.cuda.Event() for _ in range(nb)]
+    ev_free = [torch.cuda.Event() for _ in range(nb)]
+
+    def e2e_step(s_):
+        i = s_ % nb
+        with torch.cuda.stream(h2d):
+            if s_ >= nb:
+                h2d.wait_event(ev_done[i])        # step s-nb no longer reads xs[i] / lgs[i]
+            xs[i].copy_(x_h, non_blocking=True)
+            lgs[i].copy_(lg_h, non_blocking=True)
+            ev_in[i].record(h2d)
+        stream.wait_event(ev_in[i])
+        if s_ >= nb:
+            stream.wait_event(ev_free[i])         # step s-nb's output has been downloaded
+        layer(xs[i], lgs[i], outs[i])
+        ev_done[i].record(stream)
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(ev_done[i])
+            out_h[i].copy_(outs[i], non_blocking=True)
+            ev_free[i].record(d2h)
+
+    for s_ in range(max(2, args.warmup // 2) * nb):
+        e2e_step(s_)
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(K):
-        x.copy_(x_h, non_blocking=True)
-        lg.copy_(lg_h, non_blocking=True)
-        layer(x, lg, out)
-        out_h.copy_(out, non_blocking=True)
+    h2d.wait_stream(stream)
+    for s_ in range(K):
+        e2e_step(s_)
+    stream.wait_stream(d2h)                       # the last download is inside the region
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -416,7 +443,8 @@ def run_ours(args):
         "down_ssmm_tflops": (flops_gu / 2) / (ph_ms[3] * 1e-3) / 1e12,
         "roofline": roof,
         "e2e": {"value": T * world / (ms_e2e * 1e-3), "unit": "tokens/s",
-                "h2d_bytes_per_step": T * d * 2 + T * E * 4, "d2h_bytes_per_step": T * d * 4},
+                "h2d_bytes_per_step": T * d * 2 + T * E * 4, "d2h_bytes_per_step": T * d * 4,
+                "overlap": "copies of steps s+1 / s-1 on separate streams beside step s (double-buffered)"},
         "decode": dec,
         "gpu_launches": int(launches),
         "clocks": clk,
