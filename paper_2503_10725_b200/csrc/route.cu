@@ -14,32 +14,65 @@ constexpr int kRouteWarps = kRouteThreads / 32;
 constexpr int kMaxK = 8;
 constexpr int kMaxE = 256;
 
-__device__ __forceinline__ void topk_token(const float* __restrict__ lg, int E, int k, int gating, int* ids,
-                                           float* w) {
-  float bv[kMaxK];
-  int bi[kMaxK];
-  for (int i = 0; i < kMaxK; ++i) { bv[i] = -INFINITY; bi[i] = -1; }
-  for (int e = 0; e < E; ++e) {
-    const float v = lg[e];
-    if (bi[k - 1] >= 0 && !(v > bv[k - 1])) continue;  // ties keep the lower id (R10)
-    int p = k - 1;
-    while (p > 0 && (bi[p - 1] < 0 || v > bv[p - 1])) {
-      bv[p] = bv[p - 1]; bi[p] = bi[p - 1];
-      --p;
+// One warp per token: lane l holds logits l, l+32, ... (coalesced).  Each
+// element's rank = #{elements with a larger logit, or an equal logit and a
+// lower expert id} (ties keep the lower id, R10) is counted against all E
+// values broadcast by shuffles -- independent, pipelined steps instead of k
+// dependent argmax rounds.  Elements of rank < k are the top-k, in order.
+// Writes ids / gate weights of token row `t` directly.
+template <int V>
+__device__ __forceinline__ void topk_warp(const float* __restrict__ lg, int E, int k, int gating, int lane,
+                                          int32_t* __restrict__ ids, float* __restrict__ w) {
+  float v[V];
+  int rank[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const int e = lane + 32 * j;
+    v[j] = e < E ? lg[e] : -INFINITY;
+    rank[j] = 0;
+  }
+#pragma unroll
+  for (int jj = 0; jj < V; ++jj) {
+    const int cols = min(32, E - 32 * jj);
+    for (int src = 0; src < cols; ++src) {
+      const float o = __shfl_sync(0xffffffffu, v[jj], src);
+      const int oe = src + 32 * jj;
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const int e = lane + 32 * j;
+        rank[j] += (o > v[j] || (o == v[j] && oe < e)) ? 1 : 0;
+      }
     }
-    bv[p] = v; bi[p] = e;
   }
-  const float m = bv[0];
+  // the maximum logit (rank 0) and the normaliser
+  float m = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < V; ++j)
+    if (lane + 32 * j < E) m = fmaxf(m, v[j]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
   float s = 0.f;
-  if (gating == SMY_GATE_SOFTMAX_ALL) {
-    for (int e = 0; e < E; ++e) s += expf(lg[e] - m);
-  } else {
-    for (int i = 0; i < k; ++i) s += expf(bv[i] - m);
+#pragma unroll
+  for (int j = 0; j < V; ++j)
+    if (lane + 32 * j < E && (gating == SMY_GATE_SOFTMAX_ALL || rank[j] < k)) s += expf(v[j] - m);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const int e = lane + 32 * j;
+    if (e < E && rank[j] < k) {
+      ids[rank[j]] = e;
+      w[rank[j]] = expf(v[j] - m) / s;
+    }
   }
-  for (int i = 0; i < k; ++i) {
-    ids[i] = bi[i];
-    w[i] = expf(bv[i] - m) / s;
-  }
+}
+
+__device__ __forceinline__ void topk_token(const float* __restrict__ lg, int E, int k, int gating, int lane,
+                                           int32_t* __restrict__ ids, float* __restrict__ w) {
+  if (E <= 32) topk_warp<1>(lg, E, k, gating, lane, ids, w);
+  else if (E <= 64) topk_warp<2>(lg, E, k, gating, lane, ids, w);
+  else if (E <= 128) topk_warp<4>(lg, E, k, gating, lane, ids, w);
+  else topk_warp<8>(lg, E, k, gating, lane, ids, w);
 }
 
 // Build per-warp expert masks for this block's tokens (from ids).
@@ -57,22 +90,83 @@ __device__ __forceinline__ void build_masks(const int32_t* __restrict__ ids, int
   __syncthreads();
 }
 
-__global__ void route_count_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int gating,
-                                   int32_t* __restrict__ ids, float* __restrict__ w, int32_t* __restrict__ blk_counts) {
+// One warp per token over the whole grid (8 tokens per 256-thread block).
+__global__ void route_topk_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int gating,
+                                  int32_t* __restrict__ ids, float* __restrict__ w) {
+  const int lane = threadIdx.x % 32;
+  const int64_t t = (int64_t)blockIdx.x * kRouteWarps + threadIdx.x / 32;
+  if (t >= T) return;
+  topk_token(logits + t * E, E, k, gating, lane, ids + t * k, w + t * k);
+}
+
+__global__ void route_count_kernel(const int32_t* __restrict__ ids, int64_t T, int E, int k,
+                                   int32_t* __restrict__ blk_counts) {
   __shared__ uint32_t mask[kRouteWarps][kMaxE];
-  const int64_t t = (int64_t)blockIdx.x * kRouteThreads + threadIdx.x;
-  if (t < T && logits != nullptr) {  // logits == nullptr: keys are given (generic compaction)
-    int li[kMaxK];
-    float lw[kMaxK];
-    topk_token(logits + t * E, E, k, gating, li, lw);
-    for (int i = 0; i < k; ++i) { ids[t * k + i] = li[i]; w[t * k + i] = lw[i]; }
+  build_masks(ids, T, E, k, mask);
+  for (int e = threadIdx.x; e < E; e += kRouteThreads) {
+    int c = 0;
+    for (int ww = 0; ww < kRouteWarps; ++ww) c += __popc(mask[ww][e]);
+    blk_counts[(int64_t)blockIdx.x * E + e] = c;
+  }
+}
+
+// T <= kRouteThreads: the whole routing + compaction in one block / one launch
+// (top-k, masks, counts, offsets, tile prefixes, scatter).
+__global__ void route_small_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int gating,
+                                   int32_t* __restrict__ ids, float* __restrict__ w, int32_t* __restrict__ counts,
+                                   int32_t* __restrict__ offsets, int nt0, int mt0, int32_t* __restrict__ prefix0,
+                                   int nt1, int mt1, int32_t* __restrict__ prefix1, int32_t* __restrict__ sel,
+                                   float* __restrict__ gw) {
+  __shared__ uint32_t mask[kRouteWarps][kMaxE];
+  __shared__ int32_t wbase[kRouteWarps][kMaxE];
+  const int wp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (logits != nullptr) {
+    for (int t = wp; t < T; t += kRouteWarps)
+      topk_token(logits + (int64_t)t * E, E, k, gating, lane, ids + (int64_t)t * k, w + (int64_t)t * k);
   }
   __syncthreads();
   build_masks(ids, T, E, k, mask);
   for (int e = threadIdx.x; e < E; e += kRouteThreads) {
     int c = 0;
     for (int ww = 0; ww < kRouteWarps; ++ww) c += __popc(mask[ww][e]);
-    blk_counts[(int64_t)blockIdx.x * E + e] = c;
+    wbase[0][e] = c;  // temporarily: the count
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0, p0 = 0, p1 = 0;
+    for (int e = 0; e < E; ++e) {
+      const int c = wbase[0][e];
+      counts[e] = c;
+      offsets[e] = acc;
+      if (prefix0) prefix0[e] = p0;
+      if (prefix1) prefix1[e] = p1;
+      if (prefix0) p0 += mt0 * ((c + nt0 - 1) / nt0);
+      if (prefix1) p1 += mt1 * ((c + nt1 - 1) / nt1);
+      wbase[0][e] = acc;  // now: the expert's first row
+      acc += c;
+    }
+    offsets[E] = acc;
+    if (prefix0) prefix0[E] = p0;
+    if (prefix1) prefix1[E] = p1;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += kRouteThreads) {
+    int run = wbase[0][e];
+    for (int ww = 0; ww < kRouteWarps; ++ww) {
+      wbase[ww][e] = run;
+      run += __popc(mask[ww][e]);
+    }
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t >= T) return;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int i = 0; i < k; ++i) {
+    const int e = ids[(int64_t)t * k + i];
+    if (e < 0) continue;
+    const int pos = wbase[wp][e] + __popc(mask[wp][e] & lt);
+    sel[pos] = t;
+    gw[pos] = w[(int64_t)t * k + i];
   }
 }
 
@@ -166,26 +260,40 @@ smy_status route_launch(const float* logits, int64_t T, int E, int k, int gating
   const int nblk = (int)((T + kRouteThreads - 1) / kRouteThreads);
   int32_t* blk_counts = static_cast<int32_t*>(ws);
   int32_t* blk_base = blk_counts + (int64_t)nblk * E;
-  if (T > 0) {
-    route_count_kernel<<<nblk, kRouteThreads, 0, s>>>(logits, T, E, k, gating, ids, w, blk_counts);
+  const int nt0 = n_tile_cfgs > 0 ? tile_nt[0] : 1, mt0 = n_tile_cfgs > 0 ? tile_mt[0] : 0;
+  const int nt1 = n_tile_cfgs > 1 ? tile_nt[1] : 1, mt1 = n_tile_cfgs > 1 ? tile_mt[1] : 0;
+  int32_t* pre0 = n_tile_cfgs > 0 ? tile_prefix : nullptr;
+  int32_t* pre1 = n_tile_cfgs > 1 ? tile_prefix + (E + 1) : nullptr;
+  if (T <= kRouteThreads) {  // one block for the compaction (decode sizes)
+    // up to 4 tokens per warp: top-k inside the same launch; more: a grid-wide
+    // top-k launch first (one warp per token) so the block only compacts
+    const bool fused_topk = T <= 4 * kRouteWarps;
+    if (logits != nullptr && !fused_topk) {
+      route_topk_kernel<<<(unsigned)((T + kRouteWarps - 1) / kRouteWarps), kRouteThreads, 0, s>>>(logits, T, E, k,
+                                                                                                 gating, ids, w);
+      count_launch();
+    }
+    route_small_kernel<<<1, kRouteThreads, 0, s>>>(fused_topk ? logits : nullptr, T, E, k, gating, ids, w, counts,
+                                                   offsets, nt0, mt0, pre0, nt1, mt1, pre1, sel, gw);
     count_launch();
+    return cuda_status(cudaGetLastError());
+  }
+  if (logits != nullptr) {
+    route_topk_kernel<<<(unsigned)((T + kRouteWarps - 1) / kRouteWarps), kRouteThreads, 0, s>>>(logits, T, E, k,
+                                                                                               gating, ids, w);
+    count_launch();
+  }
+  route_count_kernel<<<nblk, kRouteThreads, 0, s>>>(ids, T, E, k, blk_counts);
+  count_launch();
+  {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_status(e);
   }
-  route_scan_kernel<<<1, 256, 0, s>>>(blk_counts, nblk, E, counts, offsets, blk_base,
-                                      n_tile_cfgs > 0 ? tile_nt[0] : 1, n_tile_cfgs > 0 ? tile_mt[0] : 0,
-                                      n_tile_cfgs > 0 ? tile_prefix : nullptr,
-                                      n_tile_cfgs > 1 ? tile_nt[1] : 1, n_tile_cfgs > 1 ? tile_mt[1] : 0,
-                                      n_tile_cfgs > 1 ? tile_prefix + (E + 1) : nullptr);
+  route_scan_kernel<<<1, 256, 0, s>>>(blk_counts, nblk, E, counts, offsets, blk_base, nt0, mt0, pre0, nt1, mt1, pre1);
   count_launch();
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_status(e);
-  if (T > 0) {
-    route_scatter_kernel<<<nblk, kRouteThreads, 0, s>>>(ids, w, T, E, k, blk_base, sel, gw);
-    count_launch();
-    e = cudaGetLastError();
-  }
-  return cuda_status(e);
+  route_scatter_kernel<<<nblk, kRouteThreads, 0, s>>>(ids, w, T, E, k, blk_base, sel, gw);
+  count_launch();
+  return cuda_status(cudaGetLastError());
 }
 
 }  // namespace smy

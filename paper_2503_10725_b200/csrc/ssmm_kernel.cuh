@@ -44,7 +44,7 @@ struct Cfg {
   static constexpr int kStageBytes = NW * kWStride + kBBytes;
   static constexpr int kAccCols = NW * MS * NT;
   static constexpr int kECol = (kAccCols + 3) / 4 * 4;
-  static constexpr int kColsNeeded = kECol + 8 * NW;       // E double-buffered across stages
+  static constexpr int kColsNeeded = kECol + 16;           // E: 2 stage buffers x 2 issuer warps x 4 cols
   static constexpr int kTmemCols = kColsNeeded <= 32    ? 32
                                    : kColsNeeded <= 64  ? 64
                                    : kColsNeeded <= 128 ? 128
@@ -61,7 +61,7 @@ struct Cfg {
   static_assert(NT % 16 == 0 && NT >= 16 && NT <= 256, "UMMA N");
 };
 
-constexpr int kThreads = 320;  // warps 0-3 epilogue, 4 producer, 5 MMA, 6-9 gather
+constexpr int kThreads = 352;  // warps 0-3 epilogue, 4 producer, 5 + 10 MMA, 6-9 gather
 constexpr int kGatherThreads = 128;
 
 struct TileInfo {
@@ -113,6 +113,7 @@ __device__ __forceinline__ void tma_tile2d(void* dst, const CUtensorMap* map, in
 
 template <int NT, int NW, int MS, int REP>
 __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant__ SsmmArgs a) {
+  constexpr int kIssuers = (NW == 2 || MS >= 2) ? 2 : 1;  // MMA-issuing warps
   using C = Cfg<NT, NW, MS, REP>;
   constexpr int S = C::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -130,9 +131,9 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], gather ? 1 + kGatherThreads : 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kIssuers);
     }
-    mbar_init(acc_full, 1);
+    mbar_init(acc_full, kIssuers);
     mbar_init(acc_empty, 4);
     fence_mbar_init();
   }
@@ -176,10 +177,19 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
         }
       }
     }
-  } else if (warp == 5) {
-    // ======================= MMA issuer (whole warp, one elected lane) =======================
+  } else if (warp == 5 || warp == 10) {
+    // ============ MMA issuers (warps 5 and 10; whole warp, one elected lane) ============
+    // Per-stage issue work (plane words -> uniform lane masks, descriptors,
+    // elect) is as long as the MMAs at decode sizes, so two warps split it:
+    // NW == 2 -> warp mi issues weight mi; NW == 1 -> slots p = mi (mod 2).
+    // tcgen05.commit tracks the issuing thread's MMAs, so each issuer commits and
+    // `empty` / `acc_full` expect kIssuers arrivals.  Each warp copies the E tile
+    // it uses into its own TMEM columns (ordered before its own MMAs).
+    const int mi = warp == 10 ? 1 : 0;
+    if (mi < kIssuers) {
     constexpr uint32_t idesc = (1u << 2) | (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NT >> 3) << 17) |
                                ((uint32_t)(128 >> 4) << 24);
+    const int we = NW == 2 ? mi : 0;  // the weight whose E this warp needs
     const uint32_t smem_base = smem_u32(smem);
     // redux.sync results live in uniform registers: keeps every MMA operand uniform
     // so the compiler issues UTCHMMA without a per-instruction R2UR waterfall
@@ -194,56 +204,51 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
         mbar_wait(&full[st], (it / S) & 1);
         tc_fence_after();
         const uint32_t sbase = smem_base + st * C::kStageBytes;
-#pragma unroll
         // E double-buffered in TMEM: this stage's copy does not overwrite columns
         // the previous stage's MMAs may still be reading
-        const uint32_t ecol = C::kECol + (it & 1) * 4 * NW;
+        const uint32_t ecol = C::kECol + (it & 1) * 8 + 4 * mi;
+        tc_cp_128x128b_elect(tm + ecol, desc_interleave(sbase + we * C::kWStride + kABytes));
+        // index bit-planes of this stage (this warp's weight), made explicitly warp-uniform
+        uint32_t pl[4][C::kPlanes > 0 ? C::kPlanes : 1][4];
 #pragma unroll
-        for (int w = 0; w < NW; ++w) tc_cp_128x128b_elect(tm + ecol + 4 * w, desc_interleave(sbase + w * C::kWStride + kABytes));
-        // index bit-planes of this stage, made explicitly warp-uniform
-        uint32_t pl[NW][4][C::kPlanes > 0 ? C::kPlanes : 1][4];
+        for (int kb = 0; kb < 4; ++kb)
 #pragma unroll
-        for (int w = 0; w < NW; ++w)
-#pragma unroll
-          for (int kb = 0; kb < 4; ++kb)
-#pragma unroll
-            for (int b = 0; b < C::kPlanes; ++b) {
-              const uint4 v = *reinterpret_cast<const uint4*>(wsm(st, w) + kABytes + kEBytes + (kb * C::kPlanes + b) * 16);
-              pl[w][kb][b][0] = __reduce_or_sync(0xffffffffu, v.x);
-              pl[w][kb][b][1] = __reduce_or_sync(0xffffffffu, v.y);
-              pl[w][kb][b][2] = __reduce_or_sync(0xffffffffu, v.z);
-              pl[w][kb][b][3] = __reduce_or_sync(0xffffffffu, v.w);
-            }
+          for (int b = 0; b < C::kPlanes; ++b) {
+            const uint4 v = *reinterpret_cast<const uint4*>(wsm(st, we) + kABytes + kEBytes + (kb * C::kPlanes + b) * 16);
+            pl[kb][b][0] = __reduce_or_sync(0xffffffffu, v.x);
+            pl[kb][b][1] = __reduce_or_sync(0xffffffffu, v.y);
+            pl[kb][b][2] = __reduce_or_sync(0xffffffffu, v.z);
+            pl[kb][b][3] = __reduce_or_sync(0xffffffffu, v.w);
+          }
 #pragma unroll
         for (int kb = 0; kb < 4; ++kb) {
           const int e0 = (kb / REP) * 32;  // first B element of this K=32 window
           const uint64_t bdesc = desc_sw128(sbase + NW * C::kWStride + (e0 / 64) * (NT * 128) + (e0 % 64) * 2);
+          const uint64_t adesc = desc_sw128(sbase + we * C::kWStride + kb * 32);
 #pragma unroll
-          for (int w = 0; w < NW; ++w) {
-            const uint64_t adesc = desc_sw128(sbase + w * C::kWStride + kb * 32);
+          for (int p = 0; p < MS; ++p) {
+            if (NW == 1 && kIssuers == 2 && (p & 1) != mi) continue;
+            uint32_t mask[4];
 #pragma unroll
-            for (int p = 0; p < MS; ++p) {
-              uint32_t mask[4];
+            for (int q = 0; q < 4; ++q) {
+              uint32_t en = 0xffffffffu;
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                uint32_t en = 0xffffffffu;
-#pragma unroll
-                for (int b = 0; b < C::kPlanes; ++b) en &= ((p >> b) & 1) ? pl[w][kb][b][q] : ~pl[w][kb][b][q];
-                mask[q] = MS == 1 ? 0u : ~en;
-              }
-              // metadata column of this K=32 window: even part in the address,
-              // the odd bit in idesc.sparse_id2 (bits [0,2))
-              if (!(a.debug & 4))
-              tc_mma_sp_elect(tm + (w * MS + p) * NT, adesc, bdesc, idesc | (uint32_t)(kb & 1), mask[0], mask[1],
-                              mask[2], mask[3], tm + ecol + 4 * w + (kb & 2));
+              for (int b = 0; b < C::kPlanes; ++b) en &= ((p >> b) & 1) ? pl[kb][b][q] : ~pl[kb][b][q];
+              mask[q] = MS == 1 ? 0u : ~en;
             }
+            // metadata column of this K=32 window: even part in the address,
+            // the odd bit in idesc.sparse_id2 (bits [0,2))
+            if (!(a.debug & 4))
+              tc_mma_sp_elect(tm + (we * MS + p) * NT, adesc, bdesc, idesc | (uint32_t)(kb & 1), mask[0], mask[1],
+                              mask[2], mask[3], tm + ecol + (kb & 2));
           }
         }
         tc_commit_elect(&empty[st]);
       }
       tc_commit_elect(acc_full);
     }
-  } else if (warp >= 6) {
+    }
+  } else if (warp >= 6 && warp < 10) {
     // ================== SEL gather of token rows (warps 6-9, cp.async) ==================
     if (gather) {
       const int tb = threadIdx.x - 6 * 32;

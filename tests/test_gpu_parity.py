@@ -241,7 +241,10 @@ def test_ssmm_full_size_sampled(smy):
 
 @pytest.mark.parametrize("T,E,k,gating", [(1, 8, 2, "renorm_topk"), (1000, 64, 6, "renorm_topk"),
                                           (777, 64, 8, "softmax_all"), (4096, 8, 2, "renorm_topk"),
-                                          (300, 60, 4, "renorm_topk")])
+                                          (300, 60, 4, "renorm_topk"),
+                                          # T <= 256: the single-launch path; E up to 256
+                                          (16, 64, 6, "softmax_all"), (256, 160, 8, "renorm_topk"),
+                                          (257, 256, 8, "softmax_all")])
 def test_route_bit_exact(smy, T, E, k, gating):
     lg = synth.router_logits(synth.SEED_LOGITS, T, E, skew=1.0 if E == 64 else 0.0)
     ids, w, counts, offsets, sel, gw = smy.route(torch.from_numpy(lg).cuda(), k, gating)
