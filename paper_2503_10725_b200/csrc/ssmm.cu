@@ -144,6 +144,7 @@ smy_status ssmm_launch(const SsmmArgs& a0, int nt, int nw, int ms, int rep, cuda
   if (debug_flags()) {
     dbg = a0;
     dbg.debug = debug_flags();
+    dbg.prof = (dbg.debug & 128) ? debug_prof_buffer(148) : nullptr;
     ap = &dbg;
   }
   const SsmmArgs& a = *ap;

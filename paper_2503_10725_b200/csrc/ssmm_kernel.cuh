@@ -43,7 +43,10 @@ struct Cfg {
   static constexpr int kBBytes = NT * 128 * (2 / REP);     // token tile per stage
   static constexpr int kStageBytes = NW * kWStride + kBBytes;
   static constexpr int kAccCols = NW * MS * NT;
-  static constexpr int kECol = (kAccCols + 3) / 4 * 4;
+  // two accumulator sets when they fit: the epilogue drains tile i while the
+  // MMAs of tile i+1 run (decode-sized tiles)
+  static constexpr int kAccBufs = 2 * kAccCols + 16 <= 512 ? 2 : 1;
+  static constexpr int kECol = (kAccBufs * kAccCols + 3) / 4 * 4;
   static constexpr int kColsNeeded = kECol + 16;           // E: 2 stage buffers x 2 issuer warps x 4 cols
   static constexpr int kTmemCols = kColsNeeded <= 32    ? 32
                                    : kColsNeeded <= 64  ? 64
@@ -121,9 +124,10 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
   uint8_t* aux = smem + S * C::kStageBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(aux);
   uint64_t* empty = full + S;
-  uint64_t* acc_full = empty + S;
-  uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t* acc_full = empty + S;      // [kAccBufs]
+  uint64_t* acc_empty = acc_full + 2;  // [kAccBufs]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  constexpr int AB = C::kAccBufs;
   int32_t* rows = reinterpret_cast<int32_t*>(aux + 1024);  // gather row ids of the current tile
   const bool gather = a.sel_in != nullptr;
 
@@ -133,8 +137,10 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
       mbar_init(&full[s], gather ? 1 + kGatherThreads : 1);
       mbar_init(&empty[s], kIssuers);
     }
-    mbar_init(acc_full, kIssuers);
-    mbar_init(acc_empty, 4);
+    for (int b = 0; b < AB; ++b) {
+      mbar_init(&acc_full[b], kIssuers);
+      mbar_init(&acc_empty[b], 4);
+    }
     fence_mbar_init();
   }
   if (warp == 5) tmem_alloc(tmem_slot, C::kTmemCols);
@@ -146,6 +152,10 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
   auto bsm = [&](int st) { return smem + st * C::kStageBytes + NW * C::kWStride; };
   const int ks = a.k_stages;
   const int tile0 = blockIdx.x, tstep = gridDim.x;
+  // SMY_DEBUG & 128: per-role cycle counters (same slots as the pair kernel)
+  const bool prof = a.prof != nullptr;
+  unsigned long long pc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  auto clk = []() { unsigned long long c; asm volatile("mov.u64 %0, %%clock64;" : "=l"(c)); return c; };
 
   if (warp == 4) {
     // ========== producer: weight image (bulk) + contiguous token tile (2D TMA) ==========
@@ -162,7 +172,9 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
         const int xrow = ti.row0 + ti.t0;
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % S;
+          const unsigned long long t0 = prof ? clk() : 0;
           mbar_wait(&empty[st], ((it / S) & 1) ^ 1);
+          if (prof) pc[5] += clk() - t0;
           const bool skip_w = a.debug & 2;
           mbar_arrive_expect_tx(&full[st], stage_bytes - (skip_w ? NW * wbytes : 0u));
           if (!skip_w) {
@@ -196,12 +208,19 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
     const uint32_t tm = __reduce_or_sync(0xffffffffu, tmem);
     uint32_t it = 0, tcount = 0;
     TileInfo ti;
+    const unsigned long long tstart = prof ? clk() : 0;
     for (int tile = tile0; decode_tile(a, NT, tile, ti); tile += tstep, ++tcount) {
-      mbar_wait(acc_empty, tcount & 1);  // accumulators drained and re-zeroed
+      unsigned long long t0 = prof ? clk() : 0;
+      const int ab = tcount % AB;
+      const uint32_t tacc = tm + ab * C::kAccCols;
+      mbar_wait(&acc_empty[ab], (tcount / AB) & 1);  // this accumulator set drained and re-zeroed
+      if (prof) pc[1] += clk() - t0;
       tc_fence_after();
       for (int k = ti.k0; k < ti.k1; ++k, ++it) {
         const int st = it % S;
+        t0 = prof ? clk() : 0;
         mbar_wait(&full[st], (it / S) & 1);
+        if (prof) pc[0] += clk() - t0;
         tc_fence_after();
         const uint32_t sbase = smem_base + st * C::kStageBytes;
         // E double-buffered in TMEM: this stage's copy does not overwrite columns
@@ -239,14 +258,16 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
             // metadata column of this K=32 window: even part in the address,
             // the odd bit in idesc.sparse_id2 (bits [0,2))
             if (!(a.debug & 4))
-              tc_mma_sp_elect(tm + (we * MS + p) * NT, adesc, bdesc, idesc | (uint32_t)(kb & 1), mask[0], mask[1],
+              tc_mma_sp_elect(tacc + (we * MS + p) * NT, adesc, bdesc, idesc | (uint32_t)(kb & 1), mask[0], mask[1],
                               mask[2], mask[3], tm + ecol + (kb & 2));
           }
         }
         tc_commit_elect(&empty[st]);
       }
-      tc_commit_elect(acc_full);
+      tc_commit_elect(&acc_full[ab]);
+      pc[7] += 1;
     }
+    if (prof) pc[2] = clk() - tstart;
     }
   } else if (warp >= 6 && warp < 10) {
     // ================== SEL gather of token rows (warps 6-9, cp.async) ==================
@@ -263,7 +284,9 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
         named_bar_sync(1, kGatherThreads);
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % S;
+          unsigned long long tg0 = prof ? clk() : 0;
           mbar_wait(&empty[st], ((it / S) & 1) ^ 1);
+          if (prof) { const unsigned long long t1 = clk(); pc[10] += t1 - tg0; tg0 = t1; }
           const int64_t kcol0 = (int64_t)k * (128 / REP);
           uint8_t* bs = bsm(st);
           for (int idx = tb; idx < ((a.debug & 1) ? 0 : CHUNKS); idx += kGatherThreads) {
@@ -277,6 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
           // the barrier completes when every gather thread's copies have landed;
           // the thread moves on to the next stage immediately
           cp_async_mbar_arrive_noinc(&full[st]);
+          if (prof) pc[11] += clk() - tg0;
         }
       }
     }
@@ -285,28 +309,32 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
     const int q = warp;  // TMEM lane quarter
     const uint32_t lane_base = (uint32_t)(32 * q) << 16;
     const int nf = a.n_fmt;
-    auto zero_acc = [&]() {
-      for (int c = 0; c < C::kAccCols; c += 16) tmem_st16_zero(tmem + lane_base + c);
+    auto zero_acc = [&](int b) {
+      for (int c = 0; c < C::kAccCols; c += 16) tmem_st16_zero(tmem + lane_base + b * C::kAccCols + c);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(acc_empty);
+      if (lane == 0) mbar_arrive(&acc_empty[b]);
     };
-    zero_acc();
+    for (int b = 0; b < AB; ++b) zero_acc(b);
     uint32_t tcount = 0;
     TileInfo ti;
     for (int tile = tile0; decode_tile(a, NT, tile, ti); tile += tstep, ++tcount) {
       const int cr = ti.m_tile * kTileM + 32 * q + lane;  // compressed row of this lane
       const bool valid = cr < a.R;
       const int grp = cr / nf;
-      mbar_wait(acc_full, tcount & 1);
+      unsigned long long t0 = prof ? clk() : 0;
+      const int ab = tcount % AB;
+      mbar_wait(&acc_full[ab], (tcount / AB) & 1);
+      if (prof) { const unsigned long long t1 = clk(); pc[3] += t1 - t0; t0 = t1; }
       tc_fence_after();
       for (int c0 = 0; c0 < ti.n_local; c0 += 16) {
         float v[NW][MS][16];
 #pragma unroll
         for (int w = 0; w < NW; ++w)
 #pragma unroll
-          for (int p = 0; p < MS; ++p) tmem_ld16(tmem + lane_base + (w * MS + p) * NT + c0, v[w][p]);
+          for (int p = 0; p < MS; ++p)
+            tmem_ld16(tmem + lane_base + ab * C::kAccCols + (w * MS + p) * NT + c0, v[w][p]);
         tmem_ld_wait();
         if (MS > 1 && nf > 1) {  // N>1: sum the N lanes of a block (compressed rows of one group)
 #pragma unroll
@@ -317,15 +345,18 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
               for (int j = 0; j < 16; ++j)
                 for (int off = nf >> 1; off > 0; off >>= 1) v[w][p][j] += __shfl_xor_sync(0xffffffffu, v[w][p][j], off);
         }
-        if (!valid || (a.debug & 8)) continue;
         const int jmax = min(16, ti.n_local - c0);
+        if (a.epi == kEpiScatter) {
+          // destination rows / gate weights of these 16 tokens: one load per lane,
+          // broadcast by shuffle (all lanes take part, so no early exit above)
+          const int rl = ti.row0 + ti.t0 + c0 + (lane & 15);
+          const int my_dst = (lane & 15) < jmax ? (a.sel_out ? a.sel_out[rl] : rl) : 0;
+          const float my_s = (lane & 15) < jmax ? (a.scale ? a.scale[rl] : 1.f) : 0.f;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          if (j >= jmax) break;
-          const int r = ti.row0 + ti.t0 + c0 + j;  // compact row of this token
-          if (a.epi == kEpiScatter) {
-            const int dst = a.sel_out ? a.sel_out[r] : r;
-            const float s = a.scale ? a.scale[r] : 1.f;
+          for (int j = 0; j < 16; ++j) {
+            const int dst = __shfl_sync(0xffffffffu, my_dst, j);
+            const float s = __shfl_sync(0xffffffffu, my_s, j);
+            if (j >= jmax || !valid || (a.debug & 8)) continue;
             float* o = static_cast<float*>(a.out) + (int64_t)dst * a.ldo;
             if (MS == 1) {
               atomicAdd(o + cr, s * v[0][0][j]);
@@ -336,7 +367,15 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
               for (int p = 0; p < MS; ++p)
                 if ((p % nf) == (cr % nf)) atomicAdd(o + grp * MS + p, s * v[0][p][j]);
             }
-          } else if (NW == 2) {  // SiLU(gate) * up -> bf16
+          }
+          continue;
+        }
+        if (!valid || (a.debug & 8)) continue;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (j >= jmax) break;
+          const int r = ti.row0 + ti.t0 + c0 + j;  // compact row of this token
+          if (NW == 2) {  // SiLU(gate) * up -> bf16
             uint16_t* o = static_cast<uint16_t*>(a.out) + (int64_t)r * a.ldo;
             if (MS == 2 && nf == 1) {
               float act[2];
@@ -378,10 +417,18 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
         }
       }
       tc_fence_before();
-      zero_acc();  // hand the accumulators back for the next tile
+      zero_acc(ab);  // hand this accumulator set back
+      if (prof) pc[4] += clk() - t0;
     }
   }
   tc_fence_before();
+  if (prof) {
+    unsigned long long* o = a.prof + ((size_t)(a.epi == kEpiScatter) * 148 + blockIdx.x) * 16;
+    if (warp == 5 && lane == 0) { atomicAdd(o + 0, pc[0]); atomicAdd(o + 1, pc[1]); atomicAdd(o + 2, pc[2]); atomicAdd(o + 7, pc[7]); }
+    if (warp == 6 && lane == 0) { atomicAdd(o + 10, pc[10]); atomicAdd(o + 11, pc[11]); }
+    if (warp == 0 && lane == 0) { atomicAdd(o + 3, pc[3]); atomicAdd(o + 4, pc[4]); }
+    if (warp == 4 && lane == 0) { atomicAdd(o + 5, pc[5]); }
+  }
   __syncthreads();
   tc_fence_after();
   if (warp == 5) tmem_dealloc(tmem, C::kTmemCols);
