@@ -277,3 +277,52 @@ def canonical_bytes(rows: int, cols: int, fmt: SparseFormat, elem_bytes: int = 2
         "codes": R * (cols // 2) * 2 // 8,
         "indices": R * (cols // fmt.v),
     }
+
+
+# ------------------------------------------- interleaved gate/up (reading R20)
+
+GU_BLOCK = 128   # output rows per interleave block
+
+
+def interleave_rows(w_gate: np.ndarray, w_up: np.ndarray, block: int = GU_BLOCK) -> np.ndarray:
+    """Dense [2f x d] gate/up weight with the two projections interleaved in
+    blocks of `block` output rows: rows [2b*block, (2b+1)*block) are gate rows
+    [b*block, (b+1)*block) and the next `block` rows are the same up rows.
+
+    The paper fuses the activation with "its precedent operator" but
+    does not fix how gate and up share a kernel; this row relabeling (R20)
+    puts the gate and up rows of the same outputs into one 128-lane tile."""
+    w_gate, w_up = np.asarray(w_gate), np.asarray(w_up)
+    if w_gate.shape != w_up.shape or w_gate.shape[0] % block:
+        raise ShapeError("gate/up must have equal shapes with rows % block == 0")
+    f, d = w_gate.shape
+    out = np.empty((2 * f, d), dtype=w_gate.dtype)
+    for b in range(f // block):
+        out[2 * b * block:(2 * b + 1) * block] = w_gate[b * block:(b + 1) * block]
+        out[(2 * b + 1) * block:(2 * b + 2) * block] = w_up[b * block:(b + 1) * block]
+    return out
+
+
+def deinterleave_rows(w_gu: np.ndarray, block: int = GU_BLOCK):
+    """Inverse of interleave_rows on the row axis: returns (gate, up).  Works
+    on any array whose axis 0 is the interleaved row index."""
+    w_gu = np.asarray(w_gu)
+    nb = w_gu.shape[0] // (2 * block)
+    gate = np.concatenate([w_gu[2 * b * block:(2 * b + 1) * block] for b in range(nb)])
+    up = np.concatenate([w_gu[(2 * b + 1) * block:(2 * b + 2) * block] for b in range(nb)])
+    return gate, up
+
+
+def interleave_gate_up(eg: Encoded, eu: Encoded, block: int = GU_BLOCK) -> Encoded:
+    """Canonical encoding of interleave_rows(gate, up) built from the two
+    encodings: a block of `block` output rows is block*N/M compressed rows
+    (R1), so the relabeling moves whole compressed rows of values, codes and
+    indices (no re-encoding)."""
+    if eg.fmt != eu.fmt or (eg.rows, eg.cols) != (eu.rows, eu.cols) or eg.rows % block:
+        raise ShapeError("gate/up encodings must match and rows % block == 0")
+    cb = eg.fmt.comp_rows(block)
+    out = {}
+    for name in ("values", "codes", "idx"):
+        a, b = getattr(eg, name), getattr(eu, name)
+        out[name] = interleave_rows(a, b, cb)
+    return Encoded(2 * eg.rows, eg.cols, eg.fmt, out["values"], out["codes"], out["idx"])

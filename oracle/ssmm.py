@@ -12,6 +12,8 @@ matmul as one step).  Fused epilogues (§4.3 "Operator fusion"):
   * SILU_MUL_COMPACT bf16( silu(C_gate) * C_up ) -- gate/up with the
                      activation fused (R11: SiLU gated MLP; R12: the
                      intermediate is stored as bf16, emulated with RNE)
+  * SILU_MUL_INTERLEAVED  the same on one weight holding gate and up rows
+                     interleaved in blocks of 128 (fmt.interleave_rows, R20)
   * SCATTER_ADD      out[sel[t]] += scale[t] * C[t] -- "the weighted
                      accumulation ... is fused with matrix multiplication"
 
@@ -26,6 +28,7 @@ import numpy as np
 
 from . import bf16
 from .fmt import Encoded, dense_f64
+from .fmt import deinterleave_rows as fmt_deinterleave
 
 
 def _silu(h: np.ndarray) -> np.ndarray:
@@ -53,6 +56,15 @@ def ssmm_abs(enc: Encoded, x_bits: np.ndarray, sel: np.ndarray) -> np.ndarray:
 def silu_mul_bf16(c_gate: np.ndarray, c_up: np.ndarray) -> np.ndarray:
     """bf16 bits of silu(C_gate) * C_up, RNE from fp64 (R12)."""
     return bf16.from_f64(_silu(c_gate) * c_up)
+
+
+def silu_mul_interleaved_bf16(c_gu: np.ndarray) -> np.ndarray:
+    """SILU_MUL_INTERLEAVED epilogue: C_gu = C of the interleaved gate/up
+    weight (fmt.interleave_rows, reading R20) [n x 2f]; the output column o < f
+    is bf16(silu(C_gate[:, o]) * C_up[:, o]) with the gate/up columns recovered
+    by the inverse relabeling."""
+    g, u = fmt_deinterleave(np.asarray(c_gu).T)
+    return silu_mul_bf16(g.T, u.T)
 
 
 def scatter_add(out: np.ndarray, c: np.ndarray, sel_out: np.ndarray, scale=None) -> np.ndarray:

@@ -227,3 +227,35 @@ def test_bytes_per_element_bf16():
     b = F.canonical_bytes(4096, 14336, F.SparseFormat(*g["fmt"]), 2)
     per = (b["values"] + b["codes"] + b["indices"]) / (4096 * 14336)
     assert per == g["bytes_per_logical_element"]
+
+
+# ------------------------------------------------ interleaved gate/up (R20)
+
+@pytest.mark.parametrize("fmt", list(F.TABLE4) + [F.SparseFormat(2, 2, 32)])
+def test_interleave_commutes_with_prune_and_encode(fmt):
+    """Pruning and encoding act on M-row groups and 128 is a multiple of every
+    M, so encoding the interleaved dense weight must give exactly the
+    interleaved encodings (a wrong block size, offset or row order breaks it)."""
+    f, d = 256, 128
+    wg = synth.weight_bf16(71, f, d)
+    wu = synth.weight_bf16(72, f, d)
+    direct = F.encode(F.prune(F.interleave_rows(wg, wu), fmt), fmt)
+    built = F.interleave_gate_up(F.encode(F.prune(wg, fmt), fmt), F.encode(F.prune(wu, fmt), fmt))
+    assert (direct.rows, direct.cols) == (built.rows, built.cols) == (2 * f, d)
+    for name in ("values", "codes", "idx"):
+        assert np.array_equal(getattr(direct, name), getattr(built, name)), name
+
+
+def test_interleave_rows_layout_and_inverse():
+    f, d = 384, 8
+    wg = np.arange(f * d, dtype=np.uint16).reshape(f, d)
+    wu = wg + np.uint16(10000)
+    gu = F.interleave_rows(wg, wu)
+    # row 128 of the interleaved weight is up row 0; row 256 is gate row 128
+    assert np.array_equal(gu[0], wg[0]) and np.array_equal(gu[127], wg[127])
+    assert np.array_equal(gu[128], wu[0]) and np.array_equal(gu[255], wu[127])
+    assert np.array_equal(gu[256], wg[128]) and np.array_equal(gu[767], wu[383])
+    g2, u2 = F.deinterleave_rows(gu)
+    assert np.array_equal(g2, wg) and np.array_equal(u2, wu)
+    with pytest.raises(F.ShapeError):
+        F.interleave_rows(wg[:100], wu[:100])

@@ -232,3 +232,17 @@ def test_ep_plan_covers_routing_once():
             for le, _ in tags:
                 seen.add((s, t, d * (E // P) + le))
     assert seen == {(s, t, int(e)) for s in range(P) for t in range(T) for e in ids_r[s][t]}
+
+
+def test_silu_mul_interleaved_equals_two_weight_epilogue():
+    """One SSMM on the interleaved gate/up weight + the interleaved epilogue
+    equals the two-weight SILU_MUL path bit for bit (same fp64 arithmetic)."""
+    fmt = F.SparseFormat(1, 2, 32)
+    eg, eu = make_enc(fmt, 256, 128, seed=81), make_enc(fmt, 256, 128, seed=82)
+    x = synth.activations_bf16(83, 40, 128)
+    sel = np.array([0, 3, 4, 9, 17, 21, 39], dtype=np.int32)
+    gu = F.interleave_gate_up(eg, eu)
+    got = ssmm.silu_mul_interleaved_bf16(ssmm.ssmm(gu, x, sel))
+    ref = ssmm.silu_mul_bf16(ssmm.ssmm(eg, x, sel), ssmm.ssmm(eu, x, sel))
+    assert got.shape == (len(sel), 256)
+    assert np.array_equal(got, ref)
