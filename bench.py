@@ -213,9 +213,15 @@ def build_layer(P, model, device, experts=None):
                          float(synth.uniform_scale(np.sqrt(3.0 / cols))))
             sw, status = P.compress(dense, fmt, prune=True)
             del dense
-            sw.drop_canonical()
             trip.append(sw)
         experts_out.append(tuple(trip))
+    # the layout the layer runs on (interleaved gate/up, one image block), then
+    # drop everything the kernels do not read
+    experts_out = P.prepare_experts(P.MoEConfig(E, k, d, f, 0, gating, fmt), experts_out)
+    for trip in experts_out:
+        for sw in trip:
+            if sw is not None:
+                sw.drop_canonical()
     torch.cuda.synchronize()
     return experts_out
 

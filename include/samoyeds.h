@@ -112,17 +112,40 @@ typedef struct {
 SMY_API smy_status samoyeds_compress(const smy_wdesc* desc, const void* w_bf16, int64_t ldw, int flags,
                              smy_weight* out, int32_t* d_status, void* stream);
 
+/* samoyeds_interleave_gate_up: the interleaved gate/up weight of one expert
+ * (reading R20; the paper fuses the activation with "its precedent
+ * operator", without fixing how gate and up share a kernel).  The
+ * logical weight is [2f x d]: rows [64b, 64b+32) are gate rows [32b, 32b+32)
+ * and rows [64b+32, 64b+64) the same up rows, so each warp's 32 TMEM lanes of
+ * an SSMM tile hold the gate AND up rows of the same 32 outputs (16 groups).
+ * Pruning/encoding act on M-row groups, so this equals samoyeds_compress of
+ * the interleaved dense weight bit for bit; it is built by moving whole
+ * compressed rows of gate/up's canonical arrays (which must be present) and
+ * re-packing the device image.  gate, up: same desc, rows % 32 == 0; gu:
+ * caller-owned buffers sized by smy_weight_layout({2*rows, cols, fmt}).    */
+SMY_API smy_status samoyeds_interleave_gate_up(const smy_weight* gate, const smy_weight* up, smy_weight* gu,
+                                               void* stream);
+
 /* ------------------------------------------------------------- SSMM -----
  * C[t, o] = sum_k W[o, k] * x[sel[t], k] for t < n_sel  (Alg. 1)
  * with a fused epilogue:
  *   SMY_EPI_COMPACT          out[t * ldo + o] = C[t, o]      (out_dtype)
  *   SMY_EPI_SILU_MUL_COMPACT out[t * ldo + o] = bf16(silu(C_w[t,o]) * C_w2[t,o])
  *                            (w = gate, w2 = up; out_dtype must be BF16)
+ *   SMY_EPI_SILU_MUL_INTERLEAVED  w = the interleaved gate/up weight [2f x d]
+ *                            (samoyeds_interleave_gate_up), w2 = NULL:
+ *                            out[t * ldo + o] = bf16(silu(C_gate[t,o]) * C_up[t,o])
+ *                            for o < f (BF16; format (1,2,V), V % 32 == 0)
  *   SMY_EPI_SCATTER_ADD      out[sel[t] * ldo + o] += scale[t] * C[t, o]  (f32;
  *                            scale NULL = 1; atomic, order not deterministic)
  * x: dev bf16 [x_rows x ldx], token-major; sel: dev int32 [n_sel], each in
  * [0, x_rows) (not validated on device); n_sel may be 0.  fp32 accumulation. */
-typedef enum { SMY_EPI_COMPACT = 0, SMY_EPI_SILU_MUL_COMPACT = 1, SMY_EPI_SCATTER_ADD = 2 } smy_epi;
+typedef enum {
+  SMY_EPI_COMPACT = 0,
+  SMY_EPI_SILU_MUL_COMPACT = 1,
+  SMY_EPI_SCATTER_ADD = 2,
+  SMY_EPI_SILU_MUL_INTERLEAVED = 3
+} smy_epi;
 #define SMY_F32 0
 #define SMY_BF16 1
 SMY_API smy_status samoyeds_ssmm(const smy_weight* w, const smy_weight* w2, const void* x_bf16, int64_t ldx,
@@ -145,13 +168,19 @@ SMY_API smy_status samoyeds_route(const float* logits, int64_t T, int32_t E, int
 /* ---------------------------------------------------------- MoE layer ---
  * out[t] = sum_{(e,g) in topk(t)} g * Wd_e( silu(Wg_e x_t) * (Wu_e x_t) )
  *          + sum_s Wd_s( silu(Wg_s x_t) * (Wu_s x_t) )
- * experts: host array [E][3] of smy_weight (gate, up, down); shared: host
- * array [num_shared][3] or NULL.  x dev bf16 [T x hidden]; logits dev fp32
+ * experts: host array [E][3] of smy_weight: (gate, up, down) when
+ * cfg->gate_up == SMY_GU_SEPARATE, or (gu, unused, down) when SMY_GU_INTERLEAVED
+ * (gu from samoyeds_interleave_gate_up; format (1,2,V), V % 32 == 0 -- the
+ * prefill kernels read one 128-lane tile of gate+up rows per MMA); shared: host
+ * array [num_shared][3] in the same layout, or NULL.  x dev bf16 [T x hidden]; logits dev fp32
  * [T x E]; out dev fp32 [T x hidden] (overwritten).  The gate/up -> down
  * intermediate is bf16 (reading R12).                                     */
+#define SMY_GU_SEPARATE 0
+#define SMY_GU_INTERLEAVED 1
 typedef struct {
   int32_t num_experts, top_k, hidden, ffn, num_shared, gating;
   smy_format fmt;
+  int32_t gate_up; /* SMY_GU_SEPARATE | SMY_GU_INTERLEAVED */
 } smy_moe_config;
 typedef struct smy_ep_comm smy_ep_comm; /* opaque, library-owned (EP) */
 SMY_API smy_status smy_moe_workspace_bytes(const smy_moe_config* cfg, int64_t max_tokens, size_t* bytes);

@@ -281,7 +281,7 @@ def canonical_bytes(rows: int, cols: int, fmt: SparseFormat, elem_bytes: int = 2
 
 # ------------------------------------------- interleaved gate/up (reading R20)
 
-GU_BLOCK = 128   # output rows per interleave block
+GU_BLOCK = 32    # output rows per interleave block
 
 
 def interleave_rows(w_gate: np.ndarray, w_up: np.ndarray, block: int = GU_BLOCK) -> np.ndarray:
@@ -291,7 +291,8 @@ def interleave_rows(w_gate: np.ndarray, w_up: np.ndarray, block: int = GU_BLOCK)
 
     The paper fuses the activation with "its precedent operator" but
     does not fix how gate and up share a kernel; this row relabeling (R20)
-    puts the gate and up rows of the same outputs into one 128-lane tile."""
+    puts the gate and up rows of the same 32 outputs into one 32-lane slice of
+    a 128-lane tile (gate in lanes 0-15, up in 16-31 for N/M = 1/2)."""
     w_gate, w_up = np.asarray(w_gate), np.asarray(w_up)
     if w_gate.shape != w_up.shape or w_gate.shape[0] % block:
         raise ShapeError("gate/up must have equal shapes with rows % block == 0")

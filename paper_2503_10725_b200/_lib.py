@@ -8,7 +8,8 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libsamoyeds.so")
+# SMY_LIB_PATH: load another build of the same library (A/B experiments in probes/)
+LIB_PATH = os.environ.get("SMY_LIB_PATH") or os.path.join(_PKG, "libsamoyeds.so")
 
 
 class smy_format(C.Structure):
@@ -32,7 +33,7 @@ class smy_weight(C.Structure):
 
 class smy_moe_config(C.Structure):
     _fields_ = [("num_experts", C.c_int32), ("top_k", C.c_int32), ("hidden", C.c_int32), ("ffn", C.c_int32),
-                ("num_shared", C.c_int32), ("gating", C.c_int32), ("fmt", smy_format)]
+                ("num_shared", C.c_int32), ("gating", C.c_int32), ("fmt", smy_format), ("gate_up", C.c_int32)]
 
 
 # name -> (restype, argtypes)
@@ -43,6 +44,8 @@ SIGNATURES = {
     "smy_weight_layout": (C.c_int, [C.POINTER(smy_wdesc), C.POINTER(smy_wlayout)]),
     "samoyeds_compress": (C.c_int, [C.POINTER(smy_wdesc), C.c_void_p, C.c_int64, C.c_int, C.POINTER(smy_weight),
                                     C.c_void_p, C.c_void_p]),
+    "samoyeds_interleave_gate_up": (C.c_int, [C.POINTER(smy_weight), C.POINTER(smy_weight), C.POINTER(smy_weight),
+                                              C.c_void_p]),
     "samoyeds_ssmm": (C.c_int, [C.POINTER(smy_weight), C.POINTER(smy_weight), C.c_void_p, C.c_int64, C.c_int64,
                                 C.c_void_p, C.c_int32, C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_int,
                                 C.c_void_p]),

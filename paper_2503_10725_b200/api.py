@@ -14,7 +14,8 @@ import torch
 from . import _lib
 from ._lib import check, smy_format, smy_moe_config, smy_wdesc, smy_weight, smy_wlayout
 
-EPI = {"compact": 0, "silu_mul": 1, "scatter_add": 2}
+EPI = {"compact": 0, "silu_mul": 1, "scatter_add": 2, "silu_mul_interleaved": 3}
+GATE_UP = {"separate": 0, "interleaved": 1}
 GATING = {"renorm_topk": 0, "softmax_all": 1}
 PRUNE_MAGNITUDE = 1
 ASSUME_PRUNED = 2
@@ -55,7 +56,9 @@ def weight_layout(rows: int, cols: int, fmt: Format) -> dict:
 class SparseWeight:
     """An encoded weight: canonical (values, codes, indices) + device image."""
 
-    def __init__(self, rows: int, cols: int, fmt: Format, device=None):
+    def __init__(self, rows: int, cols: int, fmt: Format, device=None, image: Optional[torch.Tensor] = None):
+        """`image`: optional caller-provided uint8 view of layout["image"] bytes
+        (e.g. a slice of one block holding every expert's image)."""
         self.rows, self.cols, self.fmt = rows, cols, fmt
         self.layout = weight_layout(rows, cols, fmt)
         dev = device or torch.device("cuda")
@@ -63,7 +66,10 @@ class SparseWeight:
         self.values = torch.empty(L["values"] // 2, dtype=torch.int16, device=dev)
         self.codes = torch.empty(L["codes"], dtype=torch.uint8, device=dev)
         self.indices = torch.empty(L["indices"], dtype=torch.uint8, device=dev)
-        self.image = torch.empty(L["image"], dtype=torch.uint8, device=dev)
+        if image is not None and (image.dtype != torch.uint8 or image.numel() != L["image"] or
+                                  not image.is_contiguous()):
+            raise ValueError("image must be a contiguous uint8 tensor of layout['image'] bytes")
+        self.image = torch.empty(L["image"], dtype=torch.uint8, device=dev) if image is None else image
 
     def c(self) -> smy_weight:
         return smy_weight(smy_wdesc(self.rows, self.cols, self.fmt.c()), _ptr(self.values), _ptr(self.codes),
@@ -95,6 +101,21 @@ def compress(w: torch.Tensor, fmt: Format, prune: bool = True, stream=None):
     return sw, status
 
 
+def interleave_gate_up(gate: SparseWeight, up: SparseWeight, stream=None,
+                       image: Optional[torch.Tensor] = None) -> SparseWeight:
+    """samoyeds_interleave_gate_up: the [2f x d] gate/up weight whose 128-row
+    blocks alternate gate and up rows (reading R20).  Needs the
+    canonical arrays of both inputs.  `image`: optional preallocated image view."""
+    lib = _lib.load()
+    if gate.values is None or up.values is None:
+        raise ValueError("interleave_gate_up needs the canonical arrays (drop_canonical() was called)")
+    gu = SparseWeight(2 * gate.rows, gate.cols, gate.fmt, gate.image.device, image=image)
+    cg, cu, cgu = gate.c(), up.c(), gu.c()
+    check(lib.samoyeds_interleave_gate_up(C.byref(cg), C.byref(cu), C.byref(cgu), _stream(stream)),
+          "samoyeds_interleave_gate_up")
+    return gu
+
+
 def ssmm(w: SparseWeight, x: torch.Tensor, sel: torch.Tensor, epi: str = "compact",
          w2: Optional[SparseWeight] = None, scale: Optional[torch.Tensor] = None,
          out: Optional[torch.Tensor] = None, out_dtype=torch.float32, stream=None) -> torch.Tensor:
@@ -106,8 +127,9 @@ def ssmm(w: SparseWeight, x: torch.Tensor, sel: torch.Tensor, epi: str = "compac
     if out is None:
         if epi == "scatter_add":
             raise ValueError("scatter_add needs an output tensor")
-        dt = torch.bfloat16 if epi == "silu_mul" else out_dtype
-        out = torch.empty(n_sel, w.rows, dtype=dt, device=x.device)
+        dt = torch.bfloat16 if epi.startswith("silu_mul") else out_dtype
+        cols = w.rows // 2 if epi == "silu_mul_interleaved" else w.rows
+        out = torch.empty(n_sel, cols, dtype=dt, device=x.device)
     odt = 1 if out.dtype == torch.bfloat16 else 0
     xb = x.view(torch.int16) if x.dtype == torch.bfloat16 else x
     cw = w.c()
@@ -147,16 +169,42 @@ class MoEConfig:
     num_shared: int = 0
     gating: str = "renorm_topk"
     fmt: Format = Format()
+    # "auto": the interleaved gate/up weight (one SSMM, reading R20) whenever the
+    # format allows it -- (1,2,V), V % 32 == 0 -- else separate gate and up
+    gate_up: str = "auto"
+
+    def resolved_gate_up(self) -> str:
+        if self.gate_up != "auto":
+            return self.gate_up
+        ok = self.fmt.n == 1 and self.fmt.m == 2 and self.fmt.v % 32 == 0 and self.ffn % 128 == 0
+        return "interleaved" if ok else "separate"
 
     def c(self) -> smy_moe_config:
         return smy_moe_config(self.num_experts, self.top_k, self.hidden, self.ffn, self.num_shared,
-                              GATING[self.gating], self.fmt.c())
+                              GATING[self.gating], self.fmt.c(), GATE_UP[self.resolved_gate_up()])
 
 
-def _weight_array(triples: Sequence[Sequence[SparseWeight]]):
+def _weight_array(triples: Sequence[Sequence[Optional[SparseWeight]]]):
     flat = [w for t in triples for w in t]
-    arr = (smy_weight * len(flat))(*[w.c() for w in flat])
+    arr = (smy_weight * len(flat))(*[w.c() if w is not None else smy_weight() for w in flat])
     return arr
+
+
+def prepare_experts(cfg: MoEConfig, triples, stream=None):
+    """(gate, up, down) triples -> the layout cfg.c() announces: unchanged for
+    "separate", (gu, None, down) with gu = interleave_gate_up(gate, up) for
+    "interleaved"."""
+    if cfg.resolved_gate_up() == "separate":
+        return [tuple(t) for t in triples]
+    if not triples or all(t[1] is None for t in triples):   # already (gu, None, down)
+        return [tuple(t) for t in triples]
+    # one block for all experts' images: a grouped CTA-pair launch addresses them
+    # through a single tensor map (include/samoyeds.h, samoyeds_moe_layer)
+    g0 = triples[0][0]
+    nb = weight_layout(2 * g0.rows, g0.cols, g0.fmt)["image"]
+    block = torch.empty(len(triples) * nb, dtype=torch.uint8, device=g0.image.device)
+    return [(interleave_gate_up(g, u, stream, image=block[i * nb:(i + 1) * nb]), None, d)
+            for i, (g, u, d) in enumerate(triples)]
 
 
 class MoELayer:
@@ -164,8 +212,8 @@ class MoELayer:
 
     def __init__(self, cfg: MoEConfig, experts, shared=(), max_tokens: int = 4096, device=None):
         self.cfg = cfg
-        self.experts = experts
-        self.shared = shared
+        self.experts = experts = prepare_experts(cfg, experts)
+        self.shared = shared = prepare_experts(cfg, shared) if shared else shared
         self._arr = _weight_array(experts)
         self._sarr = _weight_array(shared) if shared else None
         self._cfg = cfg.c()
@@ -243,7 +291,7 @@ class MoEExperts:
 
     def __init__(self, cfg: MoEConfig, experts, max_rows: int, device=None):
         self.cfg = cfg
-        self.experts = experts
+        self.experts = experts = prepare_experts(cfg, experts)
         self._arr = _weight_array(experts)
         self._cfg = cfg.c()
         lib = _lib.load()

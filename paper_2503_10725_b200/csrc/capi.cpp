@@ -107,6 +107,26 @@ smy_status moe_layer(const smy_moe_config* c, const smy_weight* experts, const s
 
 using namespace smy;
 
+static smy_status check_experts(const smy_moe_config* cfg, const smy_weight* experts, int n) {
+  if (cfg->gate_up != SMY_GU_SEPARATE && cfg->gate_up != SMY_GU_INTERLEAVED) return SMY_E_CONFIG;
+  const bool ilv = cfg->gate_up == SMY_GU_INTERLEAVED;
+  if (ilv && !ilv_format(cfg->fmt)) {
+    set_last_error("SMY_GU_INTERLEAVED needs format (1,2,V) with V % 32 == 0");
+    return SMY_E_CONFIG;
+  }
+  for (int e = 0; e < n; ++e)
+    for (int i = 0; i < 3; ++i) {
+      if (ilv && i == 1) continue;  // unused slot
+      const smy_weight& w = experts[3 * e + i];
+      const int64_t rows = i < 2 ? (ilv ? 2 * (int64_t)cfg->ffn : cfg->ffn) : cfg->hidden;
+      const int64_t cols = i < 2 ? cfg->hidden : cfg->ffn;
+      if (!w.image) return SMY_E_NULL;
+      if (w.d.rows != rows || w.d.cols != cols || memcmp(&w.d.fmt, &cfg->fmt, sizeof(smy_format)) != 0)
+        return SMY_E_SHAPE;
+    }
+  return SMY_OK;
+}
+
 extern "C" {
 
 const char* smy_status_str(int s) {
@@ -163,6 +183,22 @@ smy_status samoyeds_compress(const smy_wdesc* desc, const void* w_bf16, int64_t 
                          static_cast<cudaStream_t>(stream));
 }
 
+smy_status samoyeds_interleave_gate_up(const smy_weight* gate, const smy_weight* up, smy_weight* gu, void* stream) {
+  if (!gate || !up || !gu) return SMY_E_NULL;
+  if (!gate->values || !gate->codes || !gate->indices || !up->values || !up->codes || !up->indices || !gu->values ||
+      !gu->codes || !gu->indices || !gu->image)
+    return SMY_E_NULL;
+  if (memcmp(&gate->d, &up->d, sizeof(smy_wdesc)) != 0 || gate->d.rows % 32) return SMY_E_SHAPE;
+  smy_wdesc d = gate->d;
+  d.rows *= 2;
+  Geometry g;
+  smy_status st = geometry(&d, &g);
+  if (st != SMY_OK) return st;
+  if ((st = check_arch()) != SMY_OK) return st;
+  gu->d = d;
+  return interleave_launch(gate, up, d, g, gu, static_cast<cudaStream_t>(stream));
+}
+
 smy_status samoyeds_ssmm(const smy_weight* w, const smy_weight* w2, const void* x_bf16, int64_t ldx, int64_t x_rows,
                          const int32_t* sel, int32_t n_sel, const float* scale, int epi, void* out, int64_t ldo,
                          int out_dtype, void* stream) {
@@ -180,13 +216,21 @@ smy_status samoyeds_ssmm(const smy_weight* w, const smy_weight* w2, const void* 
       set_last_error("SILU_MUL fusion unsupported for M=16 (use two COMPACT calls)");
       return SMY_E_CONFIG;
     }
+  } else if (epi == SMY_EPI_SILU_MUL_INTERLEAVED) {
+    if (out_dtype != SMY_BF16) return SMY_E_CONFIG;
+    if (!ilv_format(w->d.fmt)) {
+      set_last_error("SILU_MUL_INTERLEAVED needs format (1,2,V) with V % 32 == 0");
+      return SMY_E_CONFIG;
+    }
+    if (w->d.rows % 64) return SMY_E_SHAPE;
   } else if (epi == SMY_EPI_SCATTER_ADD) {
     if (out_dtype != SMY_F32) return SMY_E_CONFIG;
   } else if (epi != SMY_EPI_COMPACT) {
     return SMY_E_CONFIG;
   }
   if (out_dtype != SMY_F32 && out_dtype != SMY_BF16) return SMY_E_CONFIG;
-  if (ldo < w->d.rows || (ldo % 2)) return SMY_E_SHAPE;
+  const int64_t out_cols = epi == SMY_EPI_SILU_MUL_INTERLEAVED ? w->d.rows / 2 : w->d.rows;
+  if (ldo < out_cols || (ldo % 2)) return SMY_E_SHAPE;
   if ((st = check_arch()) != SMY_OK) return st;
   if (n_sel == 0) return SMY_OK;
   const int nw = epi == SMY_EPI_SILU_MUL_COMPACT ? 2 : 1;
@@ -211,7 +255,10 @@ smy_status samoyeds_ssmm(const smy_weight* w, const smy_weight* w2, const void* 
   a.offsets = nullptr;
   a.tile_prefix = nullptr;
   a.n_sel = n_sel;
-  a.epi = epi == SMY_EPI_COMPACT ? kEpiCompact : epi == SMY_EPI_SILU_MUL_COMPACT ? kEpiSiluMul : kEpiScatter;
+  a.epi = epi == SMY_EPI_COMPACT               ? kEpiCompact
+          : epi == SMY_EPI_SILU_MUL_COMPACT    ? kEpiSiluMul
+          : epi == SMY_EPI_SILU_MUL_INTERLEAVED ? kEpiSiluMulIlv
+                                               : kEpiScatter;
   a.out_bf16 = out_dtype == SMY_BF16;
   a.out = out;
   a.ldo = ldo;
@@ -264,31 +311,14 @@ smy_status samoyeds_moe_layer(const smy_moe_config* cfg, const smy_weight* exper
     set_last_error("expert-parallel communicator: use the Python EP driver (parallel.ep)");
     return SMY_E_CONFIG;
   }
-  for (int e = 0; e < cfg->num_experts; ++e)
-    for (int i = 0; i < 3; ++i) {
-      const smy_weight& w = experts[3 * e + i];
-      const int64_t rows = i < 2 ? cfg->ffn : cfg->hidden, cols = i < 2 ? cfg->hidden : cfg->ffn;
-      if (!w.image) return SMY_E_NULL;
-      if (w.d.rows != rows || w.d.cols != cols || memcmp(&w.d.fmt, &cfg->fmt, sizeof(smy_format)) != 0)
-        return SMY_E_SHAPE;
-    }
   smy_status st;
+  if ((st = check_experts(cfg, experts, cfg->num_experts)) != SMY_OK) return st;
+  if (cfg->num_shared > 0 && (st = check_experts(cfg, shared, cfg->num_shared)) != SMY_OK) return st;
   if ((st = check_arch()) != SMY_OK) return st;
   return moe_layer(cfg, experts, shared, x_bf16, logits, T, out, workspace, ws_bytes,
                    static_cast<cudaStream_t>(stream));
 }
 
-static smy_status check_experts(const smy_moe_config* cfg, const smy_weight* experts) {
-  for (int e = 0; e < cfg->num_experts; ++e)
-    for (int i = 0; i < 3; ++i) {
-      const smy_weight& w = experts[3 * e + i];
-      const int64_t rows = i < 2 ? cfg->ffn : cfg->hidden, cols = i < 2 ? cfg->hidden : cfg->ffn;
-      if (!w.image) return SMY_E_NULL;
-      if (w.d.rows != rows || w.d.cols != cols || memcmp(&w.d.fmt, &cfg->fmt, sizeof(smy_format)) != 0)
-        return SMY_E_SHAPE;
-    }
-  return SMY_OK;
-}
 
 smy_status smy_ep_plan_workspace_bytes(int64_t T, int32_t k, int32_t world, size_t* bytes) {
   if (!bytes) return SMY_E_NULL;
@@ -327,7 +357,7 @@ smy_status samoyeds_moe_experts(const smy_moe_config* cfg, const smy_weight* exp
   if (cfg->num_experts < 1 || cfg->top_k < 1 || cfg->top_k > 8 || cfg->num_experts > kMaxGroups) return SMY_E_CONFIG;
   if (cfg->hidden % 128 || cfg->ffn % 128 || rows < 0) return SMY_E_SHAPE;
   smy_status st;
-  if ((st = check_experts(cfg, experts)) != SMY_OK) return st;
+  if ((st = check_experts(cfg, experts, cfg->num_experts)) != SMY_OK) return st;
   if ((st = check_arch()) != SMY_OK) return st;
   return moe_core(cfg, experts, nullptr, x_bf16, nullptr, keys, vals, rows, out, workspace, ws_bytes,
                   static_cast<cudaStream_t>(stream));

@@ -159,6 +159,50 @@ __global__ void pack_kernel(const uint16_t* __restrict__ values, const uint8_t* 
     *reinterpret_cast<uint32_t*>(blk + o) = 0u;
 }
 
+// Interleaved gate/up (reading R20): gu compressed row r' of block b = r' / (2 cb)
+// (cb = compressed rows per 32 output rows) comes from gate (first half of the
+// block) or up (second half), row b * cb + r' % cb.  One CTA per gu row.
+__global__ void interleave_rows_kernel(const uint8_t* __restrict__ gv, const uint8_t* __restrict__ gc,
+                                       const uint8_t* __restrict__ gi, const uint8_t* __restrict__ uv,
+                                       const uint8_t* __restrict__ uc, const uint8_t* __restrict__ ui, int64_t cb,
+                                       int64_t vbytes, int64_t cbytes, int64_t ibytes, uint8_t* __restrict__ ov,
+                                       uint8_t* __restrict__ oc, uint8_t* __restrict__ oi) {
+  const int64_t r = blockIdx.x;
+  const int64_t b = r / (2 * cb), within = r % (2 * cb);
+  const bool from_up = within >= cb;
+  const int64_t src = b * cb + (from_up ? within - cb : within);
+  const uint4* sv = reinterpret_cast<const uint4*>((from_up ? uv : gv) + src * vbytes);
+  const uint4* sc = reinterpret_cast<const uint4*>((from_up ? uc : gc) + src * cbytes);
+  const uint8_t* si = (from_up ? ui : gi) + src * ibytes;
+  uint4* dv = reinterpret_cast<uint4*>(ov + r * vbytes);
+  uint4* dc = reinterpret_cast<uint4*>(oc + r * cbytes);
+  for (int64_t i = threadIdx.x; i < vbytes / 16; i += blockDim.x) dv[i] = sv[i];
+  for (int64_t i = threadIdx.x; i < cbytes / 16; i += blockDim.x) dc[i] = sc[i];
+  for (int64_t i = threadIdx.x; i < ibytes; i += blockDim.x) oi[r * ibytes + i] = si[i];
+}
+
+smy_status interleave_launch(const smy_weight* gate, const smy_weight* up, const smy_wdesc& d, const Geometry& g,
+                             smy_weight* gu, cudaStream_t s) {
+  const int64_t cols = d.cols;
+  if (cols % 128) return SMY_E_SHAPE;
+  const int64_t cb = (int64_t)32 * d.fmt.n / d.fmt.m;  // compressed rows per 32 output rows
+  interleave_rows_kernel<<<(unsigned)g.R, 128, 0, s>>>(
+      static_cast<const uint8_t*>(gate->values), static_cast<const uint8_t*>(gate->codes),
+      static_cast<const uint8_t*>(gate->indices), static_cast<const uint8_t*>(up->values),
+      static_cast<const uint8_t*>(up->codes), static_cast<const uint8_t*>(up->indices), cb, cols, cols / 8,
+      cols / d.fmt.v, static_cast<uint8_t*>(gu->values), static_cast<uint8_t*>(gu->codes),
+      static_cast<uint8_t*>(gu->indices));
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_status(e);
+  pack_kernel<<<(unsigned)(g.m_tiles * g.k_stages), kTileM, 0, s>>>(
+      static_cast<const uint16_t*>(gu->values), static_cast<const uint8_t*>(gu->codes),
+      static_cast<const uint8_t*>(gu->indices), g.R, cols, d.fmt.v, g.rep, g.planes, g.k_stages, g.block,
+      static_cast<uint8_t*>(gu->image));
+  count_launch();
+  return cuda_status(cudaGetLastError());
+}
+
 smy_status compress_launch(const smy_wdesc* d, const Geometry& g, const uint16_t* w, int64_t ldw, int flags,
                            smy_weight* out, int32_t* d_status, cudaStream_t s) {
   const int64_t G = d->rows / d->fmt.m, J = d->cols / d->fmt.v;

@@ -27,7 +27,10 @@ void set_last_error(const char* msg);
 smy_status cuda_status(cudaError_t e);
 
 // ---------------------------------------------------------------- SSMM
-enum EpiKind { kEpiCompact = 0, kEpiSiluMul = 1, kEpiScatter = 2 };
+enum EpiKind { kEpiCompact = 0, kEpiSiluMul = 1, kEpiScatter = 2, kEpiSiluMulIlv = 3 };
+// kEpiSiluMulIlv: one weight whose compressed rows alternate 16 gate / 16 up rows
+// (the interleaved gate/up weight, reading R20); the epilogue pairs TMEM
+// lane l (gate) with lane l + 16 (up) of the same warp by shuffles.
 
 struct SsmmArgs {
   CUtensorMap tmap_x;               // contiguous x rows: 2D TMA box 64 x NT, 128B swizzle
@@ -80,6 +83,8 @@ smy_status ssmm_launch(const SsmmArgs& a, int nt, int nw, int ms, int rep, cudaS
 // returns the cluster size to use (2: one MMA pair, 4: two pairs sharing weights) or 0 (single CTA)
 int ssmm_pair_cluster(int nt, int nw, int ms, int rep, int m_tiles, int64_t tokens_per_group);
 smy_status ssmm_launch_pair(const SsmmArgs& a, int nt, int nw, int cl, cudaStream_t s);
+// can one tensor map address all these images (else: single-CTA kernel)
+bool ssmm_pair_images_ok(const smy_weight* const* w0, const smy_weight* const* w1, int groups, size_t img_bytes);
 
 // --------------------------------------------------------------- routing
 smy_status route_launch(const float* logits, int64_t T, int E, int k, int gating, int32_t* ids, float* w,
@@ -92,6 +97,10 @@ smy_status compact_launch(const int32_t* keys, const float* vals, int64_t T, int
                           const int* tile_mt, int n_tile_cfgs, int32_t* tile_prefix, cudaStream_t s);
 
 // --------------------------------------------------------------- compress
+// interleaved gate/up weight (reading R20): canonical rows moved, image re-packed
+smy_status interleave_launch(const smy_weight* gate, const smy_weight* up, const smy_wdesc& d, const Geometry& g,
+                             smy_weight* gu, cudaStream_t s);
+inline bool ilv_format(const smy_format& f) { return f.n == 1 && f.m == 2 && f.v % 32 == 0; }
 smy_status compress_launch(const smy_wdesc* d, const Geometry& g, const uint16_t* w, int64_t ldw, int flags,
                            smy_weight* out, int32_t* d_status, cudaStream_t s);
 

@@ -81,12 +81,14 @@ smy_status silu_mul_launch(const float* g, const float* u, int64_t rows, int64_t
 
 static bool gate_up_fused(const Geometry& g) { return !(g.ms >= 16); }
 
+static bool interleaved(const smy_moe_config* c) { return c->gate_up == SMY_GU_INTERLEAVED; }
+
 smy_status moe_workspace_bytes(const smy_moe_config* c, int64_t T, size_t* bytes) {
   smy_wdesc d{c->ffn, c->hidden, c->fmt};
   Geometry g;
   smy_status st = geometry(&d, &g);
   if (st != SMY_OK) return st;
-  *bytes = carve(c, T, !gate_up_fused(g), nullptr).total;
+  *bytes = carve(c, T, !interleaved(c) && !gate_up_fused(g), nullptr).total;
   return SMY_OK;
 }
 
@@ -140,27 +142,42 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
                     const float* logits, const int32_t* keys, const float* vals, int64_t T, float* out,
                     void* workspace, size_t ws_bytes, cudaStream_t s) {
   const int E = c->num_experts, k = c->top_k, d = c->hidden, f = c->ffn;
-  smy_wdesc dgu{f, d, c->fmt}, ddn{d, f, c->fmt};
+  // interleaved: experts[3e] is the [2f x d] gate/up weight (reading R20), experts[3e+1] unused
+  const bool ilv = interleaved(c);
+  smy_wdesc dgu{ilv ? 2 * f : f, d, c->fmt}, ddn{d, f, c->fmt};
   Geometry ggu, gdn;
   smy_status st;
   if ((st = geometry(&dgu, &ggu)) != SMY_OK) return st;
   if ((st = geometry(&ddn, &gdn)) != SMY_OK) return st;
   if (E > kMaxGroups) return SMY_E_CONFIG;
-  const bool fused = gate_up_fused(ggu);
+  const bool fused = ilv || gate_up_fused(ggu);
+  const int nw_gu = ilv ? 1 : fused ? 2 : 1;
   LayerWs w = carve(c, T, !fused, static_cast<uint8_t*>(workspace));
   if (w.total > ws_bytes) return SMY_E_WORKSPACE;
 
   const int64_t tpg = E ? (T * k + E - 1) / E : 0;
-  const int nt_gu = ssmm_pick_nt(fused ? 2 : 1, ggu.ms, ggu.rep, tpg);
+  const int nt_gu = ssmm_pick_nt(nw_gu, ggu.ms, ggu.rep, tpg);
   const int nt_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, tpg);
   // expected down tiles -> K split (the scatter-add epilogue makes partial sums free)
   const int64_t act = E < T * k ? E : T * k;
   const int ks_dn = ssmm_pick_ksplit((int64_t)gdn.m_tiles * act * ((tpg + nt_dn - 1) / (nt_dn > 0 ? nt_dn : 1)),
                                      gdn.k_stages);
-  const int cl_gu = fused ? ssmm_pair_cluster(nt_gu, 2, ggu.ms, ggu.rep, ggu.m_tiles, tpg) : 0;
-  const int cl_dn = ssmm_pair_cluster(nt_dn, 1, gdn.ms, gdn.rep, gdn.m_tiles, tpg);
-  const int mt_gu = cl_gu ? ggu.m_tiles / 2 : ggu.m_tiles;
-  const int mt_dn = cl_dn ? gdn.m_tiles / 2 : gdn.m_tiles;
+  const smy_weight* wg[kMaxGroups];
+  const smy_weight* wu[kMaxGroups];
+  const smy_weight* wd[kMaxGroups];
+  for (int e = 0; e < E; ++e) {
+    wg[e] = &experts[3 * e + 0];
+    wu[e] = &experts[3 * e + 1];
+    wd[e] = &experts[3 * e + 2];
+  }
+  const size_t img_gu = (size_t)ggu.m_tiles * ggu.k_stages * ggu.block;
+  const size_t img_dn = (size_t)gdn.m_tiles * gdn.k_stages * gdn.block;
+  const bool pair_gu_ok = ssmm_pair_images_ok(wg, nw_gu == 2 ? wu : nullptr, E, img_gu);
+  const bool pair_dn_ok = ssmm_pair_images_ok(wd, nullptr, E, img_dn);
+  const int cl_gu = fused && pair_gu_ok ? ssmm_pair_cluster(nt_gu, nw_gu, ggu.ms, ggu.rep, ggu.m_tiles, tpg) : 0;
+  const int cl_dn = pair_dn_ok ? ssmm_pair_cluster(nt_dn, 1, gdn.ms, gdn.rep, gdn.m_tiles, tpg) : 0;
+  const int mt_gu = cl_gu ? (ggu.m_tiles + 1) / 2 : ggu.m_tiles;
+  const int mt_dn = cl_dn ? (gdn.m_tiles + 1) / 2 : gdn.m_tiles;
   // the routing scan counts tiles per expert in units of the launch's token span
   const int nts[2] = {nt_gu, nt_dn};
   const int mts[2] = {mt_gu, mt_dn * ks_dn};
@@ -184,21 +201,16 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
     return SMY_OK;
   }
 
-  const smy_weight* wg[kMaxGroups];
-  const smy_weight* wu[kMaxGroups];
-  const smy_weight* wd[kMaxGroups];
-  for (int e = 0; e < E; ++e) {
-    wg[e] = &experts[3 * e + 0];
-    wu[e] = &experts[3 * e + 1];
-    wd[e] = &experts[3 * e + 2];
-  }
   const int64_t Tk = T * k;
   const int max_gu = mt_gu * (E + (int)((Tk + nts[0] - 1) / nts[0]));
   const int max_dn = mt_dn * (E + (int)((Tk + nts[1] - 1) / nts[1]));
   const uint16_t* xb = static_cast<const uint16_t*>(x);
 
   // gate/up: H = Wg x[SEL], U = Wu x[SEL], inter = bf16(silu(H) * U)
-  if (fused) {
+  if (ilv) {
+    st = grouped(wg, nullptr, E, ggu, f, nt_gu, 1, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiSiluMulIlv,
+                 w.inter, f, 1, nullptr, nullptr, d, tpg <= nt_gu, 1, cl_gu, s);
+  } else if (fused) {
     st = grouped(wg, wu, E, ggu, f, nt_gu, 2, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiSiluMul, w.inter, f,
                  1, nullptr, nullptr, d, tpg <= nt_gu, 1, cl_gu, s);
   } else {
@@ -222,7 +234,7 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
     const smy_weight* sg[1] = {&shared[3 * i + 0]};
     const smy_weight* su[1] = {&shared[3 * i + 1]};
     const smy_weight* sd[1] = {&shared[3 * i + 2]};
-    const int nts_gu = ssmm_pick_nt(fused ? 2 : 1, ggu.ms, ggu.rep, T);
+    const int nts_gu = ssmm_pick_nt(nw_gu, ggu.ms, ggu.rep, T);
     const int nts_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, T);
     auto single = [&](const smy_weight* const* a0, const smy_weight* const* a1, const Geometry& g, int m_out, int nt,
                       int nw, const uint16_t* xx, int64_t ldx, int epi, void* o, int64_t ldo, int ob) {
@@ -255,7 +267,9 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
       if (st2 != SMY_OK) return st2;
       return ssmm_launch(a, nt, nw, g.ms, g.rep, s);
     };
-    if (fused) {
+    if (ilv) {
+      st = single(sg, nullptr, ggu, f, nts_gu, 1, xb, d, kEpiSiluMulIlv, w.inter, f, 1);
+    } else if (fused) {
       st = single(sg, su, ggu, f, nts_gu, 2, xb, d, kEpiSiluMul, w.inter, f, 1);
     } else {
       st = single(sg, nullptr, ggu, f, nts_gu, 1, xb, d, kEpiCompact, w.fallback_g, f, 0);

@@ -80,11 +80,34 @@ int ssmm_pick_nt(int nw, int ms, int rep, int64_t tpg) {
 
 int ssmm_pair_cluster(int nt, int nw, int ms, int rep, int m_tiles, int64_t tokens_per_group) {
   if (debug_flags() & 16) return 0;  // SMY_DEBUG=16: force the single-CTA kernel
-  if (ms != 2 || rep != 1 || (m_tiles & 1) || tokens_per_group < 64) return 0;
+  // an odd m-tile count gives the last pair a phantom peer tile (loads repeated, stores masked)
+  if (ms != 2 || rep != 1 || m_tiles < 2 || tokens_per_group < 64) return 0;
   if (!(nw == 2 ? (nt == 64 || nt == 112) : (nt == 128 || nt == 224))) return 0;
   // (4-CTA clusters sharing weight stages by multicast measured 2x slower on
   // B200 -- probes/mcast_bench.cu -- and were removed)
   return 2;
+}
+
+bool ssmm_pair_images_ok(const smy_weight* const* w0, const smy_weight* const* w1, int groups, size_t img_bytes) {
+  // the pair kernel addresses every weight image of a launch through ONE tensor map
+  // (rows of 128 B, int32 row coordinates): the images must be 128-B aligned
+  // relative to each other and span < 256 GB
+  uintptr_t lo = UINTPTR_MAX, hi = 0;
+  for (int g = 0; g < groups; ++g)
+    for (int w = 0; w < 2; ++w) {
+      const smy_weight* const* arr = w ? w1 : w0;
+      if (!arr) continue;
+      const uintptr_t p = reinterpret_cast<uintptr_t>(arr[g]->image);
+      if (p < lo) lo = p;
+      if (p + img_bytes > hi) hi = p + img_bytes;
+    }
+  if (hi <= lo) return true;
+  for (int g = 0; g < groups; ++g)
+    for (int w = 0; w < 2; ++w) {
+      const smy_weight* const* arr = w ? w1 : w0;
+      if (arr && ((reinterpret_cast<uintptr_t>(arr[g]->image) - lo) & 127)) return false;
+    }
+  return (hi - lo) / 128 < ((uint64_t)1 << 31);
 }
 
 smy_status ssmm_launch_pair(const SsmmArgs& a0, int nt, int nw, int cl, cudaStream_t s) {

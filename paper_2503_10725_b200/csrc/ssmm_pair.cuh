@@ -122,6 +122,10 @@ __device__ __forceinline__ void tma2d_pair(void* dst, const CUtensorMap* map, in
 }
 
 constexpr int kPairEpiWarps = 8;                    // warps 0-3 and 10-13
+
+// tokens held by each CTA of a pair for a tile of n tokens: MMA N = 2 * half must
+// be a multiple of 16, so a half is a whole number of 8-row swizzle atoms
+__device__ __forceinline__ int pair_half(int n) { return ((n + 15) >> 4) << 3; }
 constexpr int kPairThreads = 32 * (11 + kPairEpiWarps - 4);  // + producer, 2 MMA issuers, 4 gather
 
 template <int NT, int NW>
@@ -200,18 +204,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     if (lane == 0) {
       const uint32_t wbytes = (a.debug & 2) ? 0u : (uint32_t)C::kWRows * 128;
       const uint32_t pair_bytes = 2 * (NW * wbytes + (gather ? 0u : (uint32_t)C::kBBytes)) + NW * 64u;
+      // prefill: the pairs on the same m-tile read its weights at about the same
+      // time; evict_normal measured better than evict_first (fewer re-reads)
       const uint64_t pol_w = a.weights_stream ? policy_evict_first() : policy_evict_normal();
       const uint64_t pol_x = policy_evict_last();
       const int brows = a.block >> 7;
       uint32_t it = 0;
       TileInfo ti;
       for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep) {
-        const int m_own = 2 * ti.m_tile + (int)cta, m_peer = 2 * ti.m_tile + 1;
+        // an odd m-tile count leaves the last pair's peer without a tile: it loads the
+        // last real tile again (valid memory) and its epilogue stores nothing
+        const int m_own = min(2 * ti.m_tile + (int)cta, a.m_tiles - 1), m_peer = min(2 * ti.m_tile + 1, a.m_tiles - 1);
+        const int hh = pair_half(ti.n_local);
         const uint8_t* src[2] = {a.img0[ti.g], NW == 2 ? a.img1[ti.g] : nullptr};
         int wrow[2];
 #pragma unroll
         for (int w = 0; w < NW; ++w) wrow[w] = (int)((src[w] - a.wbase) >> 7) + m_own * ks * brows;
-        const int xrow = ti.row0 + ti.t0 + (int)cta * H;
+        const int xrow = ti.row0 + ti.t0 + (int)cta * hh;
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % S;
           const unsigned long long t0 = prof ? clk() : 0;
@@ -246,8 +255,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       const int mi = warp == 14 ? 1 : 0;
       const int w = NW == 2 ? mi : 0;
       constexpr int NP = NW == 2 ? MS : 1;  // slots this warp issues
-      constexpr uint32_t idesc = (1u << 2) | (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NT >> 3) << 17) |
-                                 ((uint32_t)(256 >> 4) << 24);
+      // N of a tile = 2 * its per-CTA half (runtime: ragged tiles issue narrower MMAs)
+      constexpr uint32_t idesc0 = (1u << 2) | (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 4) << 24);
       const uint32_t smem_base = smem_u32(smem);
       const uint32_t tm = __reduce_or_sync(0xffffffffu, tmem);
       uint32_t it = 0, tcount = 0;
@@ -258,6 +267,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         mbar_wait_acq_cluster(acc_empty, tcount & 1);  // both epilogues drained and re-zeroed
         if (prof) pc[1] += clk() - t0;
         tc_fence_after();
+        const uint32_t idesc = __reduce_or_sync(0xffffffffu, idesc0 | ((uint32_t)(2 * pair_half(ti.n_local)) >> 3) << 17);
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % S;
           t0 = prof ? clk() : 0;
@@ -328,13 +338,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       const uint32_t dst0 = (uint32_t)((ch >> 3) * (H * 128) + r0 * 128 + (((ch & 7) ^ r0) << 4));
       uint32_t it = 0;
       TileInfo ti;
+      const uint64_t pol_x = policy_evict_last();
       for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep) {
         const uint16_t* src[NI];
         uint32_t valid = 0;
+        const int hh = pair_half(ti.n_local);
 #pragma unroll
         for (int i = 0; i < NI; ++i) {
-          const int t = (int)cta * H + r0 + 8 * i;
-          const int rid = t < ti.n_local ? a.sel_in[ti.row0 + ti.t0 + t] : -1;
+          const int tl = r0 + 8 * i;  // row within this CTA's half
+          const int t = (int)cta * hh + tl;
+          const int rid = (tl < hh && t < ti.n_local) ? a.sel_in[ti.row0 + ti.t0 + t] : -1;
           src[i] = a.x + (rid >= 0 ? (int64_t)rid * a.ldx : 0) + ch * 8;
           valid |= (rid >= 0 ? 1u : 0u) << i;
         }
@@ -346,11 +359,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           const int64_t kcol0 = (int64_t)k * 128;
           const uint32_t bs = smem_u32(bsm(st)) + dst0;
           if (!(a.debug & 1)) {
+            // rows past the tile's tokens are not loaded: their D columns are never read
 #pragma unroll
             for (int i = 0; i < NI; ++i)
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(bs + 1024u * i),
-                           "l"(src[i] + ((valid >> i) & 1u ? kcol0 : 0)), "r"((valid >> i) & 1u ? 16u : 0u)
-                           : "memory");
+              if ((valid >> i) & 1u)
+#ifdef SMY_X_NOHINT
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(bs + 1024u * i), "l"(src[i] + kcol0)
+                             : "memory");
+#else
+                asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(bs + 1024u * i),
+                             "l"(src[i] + kcol0), "l"(pol_x)
+                             : "memory");
+#endif
           }
           cp_async_mbar_arrive_noinc(&full[st]);
           if (prof) pc[11] += clk() - tg0;
@@ -379,16 +399,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     zero_acc();
     uint32_t tcount = 0;
     TileInfo ti;
+    const bool ilv = NW == 1 && a.epi == kEpiSiluMulIlv;
     for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep, ++tcount) {
       const int m_own = 2 * ti.m_tile + (int)cta;
       const int cr = m_own * kTileM + 32 * q + lane;
-      const bool valid = cr < a.R;
+      const bool valid = m_own < a.m_tiles && cr < a.R;
       const int grp = cr;  // (1,2,V): one compressed row per group
       unsigned long long t0 = prof ? clk() : 0;
       mbar_wait_acq_cluster(acc_full, tcount & 1);
       if (prof) { const unsigned long long t1 = clk(); pc[3] += t1 - t0; t0 = t1; }
       tc_fence_after();
-      for (int c0 = 16 * h; c0 < ti.n_local; c0 += 32) {
+      if (ilv) {
+        // lanes 0-15 gate / 16-31 up of the same 16 output pairs (reading R20)
+        const int cg = 16 * (4 * m_own + q) + (lane & 15);
+        const bool gvalid = m_own < a.m_tiles && cg < a.R / 2 && !(a.debug & 8);
+        for (int c0 = 16 * h; c0 < ti.n_local; c0 += 32) {
+          float v[2][16];
+          const unsigned long long tl0 = prof ? clk() : 0;
+          tmem_ld16(tmem + lane_base + c0, v[0]);
+          tmem_ld16(tmem + lane_base + NT + c0, v[1]);
+          tmem_ld_wait();
+          if (prof) pc[8] += clk() - tl0;
+          if (!(a.debug & 32))
+            ilv_chunk(v, gvalid, min(16, ti.n_local - c0), static_cast<uint16_t*>(a.out), a.ldo, ti.row0 + ti.t0 + c0,
+                      cg, lane);
+        }
+      }
+      for (int c0 = 16 * h; !ilv && c0 < ti.n_local; c0 += 32) {
         float v[NW][MS][16];
         const unsigned long long tl0 = prof ? clk() : 0;
 #pragma unroll
@@ -410,10 +447,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           } else if (NW == 2) {
             float act[2];
 #pragma unroll
-            for (int p = 0; p < 2; ++p) {
-              const float gv = v[0][p][j], uv = v[NW - 1][p][j];
-              act[p] = __fdividef(gv, 1.f + __expf(-gv)) * uv;
-            }
+            for (int p = 0; p < 2; ++p) act[p] = silu_mul(v[0][p][j], v[NW - 1][p][j]);
             *reinterpret_cast<__nv_bfloat162*>(static_cast<uint16_t*>(a.out) + (int64_t)r * a.ldo + 2 * grp) =
                 __floats2bfloat162_rn(act[0], act[1]);
           } else if (a.out_bf16) {

@@ -211,6 +211,56 @@ def test_ssmm_silu_mul(smy, fmt):
     assert mismatch.mean() < 0.01, mismatch.mean()
 
 
+@pytest.mark.parametrize("fmt", [F.SparseFormat(1, 2, 32), F.SparseFormat(1, 2, 16), F.SparseFormat(4, 8, 32)],
+                         ids=str)
+def test_interleave_gate_up_bit_exact(smy, fmt):
+    """samoyeds_interleave_gate_up (reading R20) == the oracle's interleaved
+    encoding + device image, and == compressing the interleaved dense weight."""
+    f, d = 384, 256
+    wg, wu = synth.weight_bf16(61, f, d), synth.weight_bf16(62, f, d)
+    eg, eu = F.encode(F.prune(wg, fmt), fmt), F.encode(F.prune(wu, fmt), fmt)
+    ref = F.interleave_gate_up(eg, eu)
+    sg, _ = smy.compress(dev16(wg), gpu_format(fmt))
+    su, _ = smy.compress(dev16(wu), gpu_format(fmt))
+    gu = smy.interleave_gate_up(sg, su)
+    torch.cuda.synchronize()
+    assert (gu.rows, gu.cols) == (2 * f, d)
+    assert np.array_equal(host16(gu.values).reshape(ref.values.shape), ref.values)
+    assert np.array_equal(gu.codes.cpu().numpy().reshape(-1, d // 8), F.pack_codes(ref.codes))
+    assert np.array_equal(gu.indices.cpu().numpy().reshape(ref.idx.shape), ref.idx)
+    assert np.array_equal(gu.image.cpu().numpy(), D.weight_image(ref))
+    direct, _ = smy.compress(dev16(F.interleave_rows(wg, wu)), gpu_format(fmt))
+    assert torch.equal(direct.image, gu.image)
+
+
+@pytest.mark.parametrize("shape", [(256, 256, 64, 16), (384, 512, 300, 130), (640, 512, 1000, 900)])
+def test_ssmm_silu_mul_interleaved(smy, shape):
+    """One SSMM over the interleaved gate/up weight with the fused SiLU*up
+    epilogue (TMEM lanes l / l+64 paired through shared memory) vs the oracle;
+    it must also equal the two-weight fused path bit for bit (same K order)."""
+    f, d, x_rows, n_sel = shape
+    fmt = F.SparseFormat(1, 2, 32)
+    sel = synth.selection(8, x_rows, n_sel)
+    x = synth.activations_bf16(12, x_rows, d)
+    wg, wu = synth.weight_bf16(50, f, d), synth.weight_bf16(51, f, d)
+    eg, eu = F.encode(F.prune(wg, fmt), fmt), F.encode(F.prune(wu, fmt), fmt)
+    sg, _ = smy.compress(dev16(wg), gpu_format(fmt))
+    su, _ = smy.compress(dev16(wu), gpu_format(fmt))
+    gu = smy.interleave_gate_up(sg, su)
+    st = torch.from_numpy(sel).cuda()
+    got_t = smy.ssmm(gu, dev16(x), st, epi="silu_mul_interleaved")
+    assert tuple(got_t.shape) == (n_sel, f)
+    two = smy.ssmm(sg, dev16(x), st, epi="silu_mul", w2=su)
+    assert torch.equal(got_t.view(torch.int16), two.view(torch.int16))
+    got = bf16.to_f64(host16(got_t.view(torch.int16)))
+    ref_bits = OS.silu_mul_interleaved_bf16(OS.ssmm(F.interleave_gate_up(eg, eu), x, sel))
+    cg, cu = OS.ssmm(eg, x, sel), OS.ssmm(eu, x, sel)
+    exact = cg / (1 + np.exp(-cg)) * cu
+    assert OS.rel_fro(got - exact, exact) <= 5e-3
+    ulp = np.abs(bf16.to_f64(ref_bits)) * 2.0 ** -7 + 1e-30
+    assert (np.abs(got - bf16.to_f64(ref_bits)) > ulp).mean() < 0.01
+
+
 def test_ssmm_full_size_sampled(smy):
     """Mixtral gate_proj at full size (14336 x 4096), 1024 of 4096 tokens, in the
     launch configuration the layer uses; the oracle recomputes sampled output
@@ -267,8 +317,8 @@ def test_route_ties(smy):
 
 # ------------------------------------------------------------------ MoE layer
 
-def _layer_case(smy, fmt, E, d, f, T, k, gating="renorm_topk", shared=0, skew=0.0, seed_off=0):
-    cfg = smy.MoEConfig(E, k, d, f, shared, gating, gpu_format(fmt))
+def _layer_case(smy, fmt, E, d, f, T, k, gating="renorm_topk", shared=0, skew=0.0, seed_off=0, gate_up="auto"):
+    cfg = smy.MoEConfig(E, k, d, f, shared, gating, gpu_format(fmt), gate_up)
     encs, sws = [], []
     for e in range(E + shared):
         te, ts = [], []
@@ -295,7 +345,10 @@ def _layer_case(smy, fmt, E, d, f, T, k, gating="renorm_topk", shared=0, skew=0.
     dict(fmt=F.SparseFormat(1, 2, 16), E=4, d=256, f=256, T=64, k=2),
     dict(fmt=F.SparseFormat(4, 8, 32), E=4, d=256, f=256, T=64, k=2),
     dict(fmt=F.SparseFormat(8, 16, 32), E=4, d=256, f=256, T=50, k=2),
-], ids=lambda c: f"{c['fmt']}-E{c['E']}-T{c['T']}")
+    dict(fmt=F.SparseFormat(1, 2, 32), E=8, d=256, f=512, T=100, k=2, gate_up="separate"),
+    dict(fmt=F.SparseFormat(1, 2, 32), E=16, d=256, f=384, T=57, k=6, gating="softmax_all", shared=2,
+         gate_up="separate"),
+], ids=lambda c: f"{c['fmt']}-E{c['E']}-T{c['T']}-{c.get('gate_up', 'auto')}")
 def test_moe_layer_parity(smy, case):
     case = dict(case)
     fmt = case.pop("fmt")
@@ -307,8 +360,11 @@ def test_moe_layer_parity(smy, case):
     dict(E=4, d=512, f=512, T=512, k=2),                       # tokens/expert >= 64: CTA-pair kernels
     dict(E=8, d=1024, f=768, T=700, k=2, gating="softmax_all"),
     dict(E=2, d=512, f=1024, T=300, k=2, skew=2.0),            # unbalanced experts, ragged tiles
-    dict(E=2, d=512, f=512, T=1000, k=2),                      # >= 2 token tiles per expert: 4-CTA clusters
-], ids=lambda c: f"E{c['E']}-d{c['d']}-f{c['f']}-T{c['T']}")
+    dict(E=2, d=512, f=512, T=1000, k=2),                      # >= 2 token tiles per expert
+    dict(E=4, d=256, f=640, T=400, k=2),                       # interleaved gate/up: 5 m-tiles (odd pair count)
+    dict(E=4, d=512, f=512, T=512, k=2, gate_up="separate"),   # two-weight gate/up pair kernel
+    dict(E=2, d=512, f=1024, T=300, k=2, skew=2.0, gate_up="separate"),
+], ids=lambda c: f"E{c['E']}-d{c['d']}-f{c['f']}-T{c['T']}-{c.get('gate_up', 'auto')}")
 def test_moe_layer_prefill_pair_kernels(smy, case):
     case = dict(case)
     got, ref, S = _layer_case(smy, F.SparseFormat(1, 2, 32), **case)

@@ -247,15 +247,16 @@ def test_interleave_commutes_with_prune_and_encode(fmt):
 
 
 def test_interleave_rows_layout_and_inverse():
-    f, d = 384, 8
+    f, d = 96, 8
     wg = np.arange(f * d, dtype=np.uint16).reshape(f, d)
     wu = wg + np.uint16(10000)
+    assert F.GU_BLOCK == 32
     gu = F.interleave_rows(wg, wu)
-    # row 128 of the interleaved weight is up row 0; row 256 is gate row 128
-    assert np.array_equal(gu[0], wg[0]) and np.array_equal(gu[127], wg[127])
-    assert np.array_equal(gu[128], wu[0]) and np.array_equal(gu[255], wu[127])
-    assert np.array_equal(gu[256], wg[128]) and np.array_equal(gu[767], wu[383])
+    # row 32 of the interleaved weight is up row 0; row 64 is gate row 32
+    assert np.array_equal(gu[0], wg[0]) and np.array_equal(gu[31], wg[31])
+    assert np.array_equal(gu[32], wu[0]) and np.array_equal(gu[63], wu[31])
+    assert np.array_equal(gu[64], wg[32]) and np.array_equal(gu[191], wu[95])
     g2, u2 = F.deinterleave_rows(gu)
     assert np.array_equal(g2, wg) and np.array_equal(u2, wu)
     with pytest.raises(F.ShapeError):
-        F.interleave_rows(wg[:100], wu[:100])
+        F.interleave_rows(wg[:40], wu[:40])
