@@ -12,6 +12,7 @@
 // graph capturable.
 #include <cuda_bf16.h>
 
+#include <cmath>
 #include <cstring>
 
 #include "internal.h"
@@ -156,8 +157,12 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   if (w.total > ws_bytes) return SMY_E_WORKSPACE;
 
   const int64_t tpg = E ? (T * k + E - 1) / E : 0;
-  const int nt_gu = ssmm_pick_nt(nw_gu, ggu.ms, ggu.rep, tpg);
-  const int nt_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, tpg);
+  // tile width: the mean tokens per expert + 3 sigma of the (binomial) spread, so a
+  // decode-sized expert rarely needs a second n-tile (which would re-stream its weights
+  // through the SMs); ragged tiles issue MMAs of their own width
+  const int64_t tpg_hi = tpg + (int64_t)(3.0 * sqrt((double)tpg) + 0.999);
+  const int nt_gu = ssmm_pick_nt(nw_gu, ggu.ms, ggu.rep, tpg_hi);
+  const int nt_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, tpg_hi);
   // expected down tiles -> K split (the scatter-add epilogue makes partial sums free)
   const int64_t act = E < T * k ? E : T * k;
   const int ks_dn = ssmm_pick_ksplit((int64_t)gdn.m_tiles * act * ((tpg + nt_dn - 1) / (nt_dn > 0 ? nt_dn : 1)),

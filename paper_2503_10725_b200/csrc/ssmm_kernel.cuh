@@ -228,8 +228,8 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
     // it uses into its own TMEM columns (ordered before its own MMAs).
     const int mi = warp == 10 ? 1 : 0;
     if (mi < kIssuers) {
-    constexpr uint32_t idesc = (1u << 2) | (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NT >> 3) << 17) |
-                               ((uint32_t)(128 >> 4) << 24);
+    // N of a tile = its token count rounded up to 16 (ragged tiles issue narrower MMAs)
+    constexpr uint32_t idesc0 = (1u << 2) | (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 4) << 24);
     const int we = NW == 2 ? mi : 0;  // the weight whose E this warp needs
     const uint32_t smem_base = smem_u32(smem);
     // redux.sync results live in uniform registers: keeps every MMA operand uniform
@@ -245,6 +245,8 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
       mbar_wait(&acc_empty[ab], (tcount / AB) & 1);  // this accumulator set drained and re-zeroed
       if (prof) pc[1] += clk() - t0;
       tc_fence_after();
+      const uint32_t idesc =
+          __reduce_or_sync(0xffffffffu, idesc0 | ((uint32_t)(((ti.n_local + 15) >> 4) << 4) >> 3) << 17);
       for (int k = ti.k0; k < ti.k1; ++k, ++it) {
         const int st = it % S;
         t0 = prof ? clk() : 0;
@@ -300,7 +302,47 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
     }
   } else if (warp >= 6 && warp < 10) {
     // ================== SEL gather of token rows (warps 6-9, cp.async) ==================
-    if (gather) {
+    if (gather && REP == 1 && NT <= 64) {
+      // Thread tb owns 16-B chunk ch = tb % 16 of rows tb/16 + 8i of the tile for
+      // every k-stage: sources and swizzled destinations are computed once per tile
+      // (as in the pair kernel); rows past the tile's tokens are not loaded.
+      const int tb = threadIdx.x - 6 * 32;
+      constexpr int NI = NT / 8;
+      const int r0 = tb >> 4, ch = tb & 15;
+      const uint32_t dst0 = (uint32_t)((ch >> 3) * (NT * 128) + r0 * 128 + (((ch & 7) ^ r0) << 4));
+      // (no L2::cache_hint on these cp.async: measured neutral, and ptxas 12.9 emitted an
+      // illegal LDGSTS descriptor operand for it in this kernel)
+      uint32_t it = 0;
+      TileInfo ti;
+      for (int tile = tile0; decode_tile(a, NT, tile, ti); tile += tstep) {
+        const uint16_t* src[NI];
+        uint32_t valid = 0;
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          const int t = r0 + 8 * i;
+          const int rid = t < ti.n_local ? a.sel_in[ti.row0 + ti.t0 + t] : -1;
+          src[i] = a.x + (rid >= 0 ? (int64_t)rid * a.ldx : 0) + ch * 8;
+          valid |= (rid >= 0 ? 1u : 0u) << i;
+        }
+        for (int k = ti.k0; k < ti.k1; ++k, ++it) {
+          const int st = it % S;
+          unsigned long long tg0 = prof ? clk() : 0;
+          mbar_wait(&empty[st], ((it / S) & 1) ^ 1);
+          if (prof) { const unsigned long long t1 = clk(); pc[10] += t1 - tg0; tg0 = t1; }
+          const int64_t kcol0 = (int64_t)k * 128;
+          const uint32_t bs = smem_u32(bsm(st)) + dst0;
+          if (!(a.debug & 1)) {
+#pragma unroll
+            for (int i = 0; i < NI; ++i)
+              if ((valid >> i) & 1u)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(bs + 1024u * i), "l"(src[i] + kcol0)
+                             : "memory");
+          }
+          cp_async_mbar_arrive_noinc(&full[st]);
+          if (prof) pc[11] += clk() - tg0;
+        }
+      }
+    } else if (gather) {
       const int tb = threadIdx.x - 6 * 32;
       constexpr int CPR = 16 / REP;  // 16-byte chunks per token row per stage
       constexpr int CHUNKS = NT * CPR;

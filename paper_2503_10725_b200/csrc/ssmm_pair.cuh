@@ -338,7 +338,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       const uint32_t dst0 = (uint32_t)((ch >> 3) * (H * 128) + r0 * 128 + (((ch & 7) ^ r0) << 4));
       uint32_t it = 0;
       TileInfo ti;
-      const uint64_t pol_x = policy_evict_last();
       for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep) {
         const uint16_t* src[NI];
         uint32_t valid = 0;
@@ -363,14 +362,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 #pragma unroll
             for (int i = 0; i < NI; ++i)
               if ((valid >> i) & 1u)
-#ifdef SMY_X_NOHINT
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(bs + 1024u * i), "l"(src[i] + kcol0)
                              : "memory");
-#else
-                asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(bs + 1024u * i),
-                             "l"(src[i] + kcol0), "l"(pol_x)
-                             : "memory");
-#endif
           }
           cp_async_mbar_arrive_noinc(&full[st]);
           if (prof) pc[11] += clk() - tg0;
