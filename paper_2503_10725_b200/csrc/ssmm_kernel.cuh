@@ -73,7 +73,26 @@ struct TileInfo {
 
 // Static schedule: tile index -> (expert, m_tile, n_tile).  n is the fastest
 // index so CTAs running concurrently share the weight tile in L2.
+//
+// Stream-K tail (a.streamk, scatter-add epilogues only -- partial sums add): with
+// `total` tiles over P workers, the first total - total % P tiles run whole; each
+// of the last rem = total % P tiles is cut into s = P / rem K-ranges, so the last
+// wave costs 1/s of a tile instead of a whole one.
 __device__ __forceinline__ bool decode_tile(const SsmmArgs& a, int nt, int tile, TileInfo& ti) {
+  int kpiece = 0, kpieces = 1;
+  if (a.streamk) {
+    const int total = a.tile_prefix != nullptr ? a.tile_prefix[a.num_groups] : a.max_tiles;
+    const int P = a.workers, rem = total % P, full = total - rem;
+    int s = rem ? P / rem : 1;
+    if (s > a.k_stages) s = a.k_stages;
+    if (s < 1) s = 1;
+    if (tile >= full + rem * s) return false;
+    if (tile >= full) {
+      kpiece = (tile - full) % s;
+      kpieces = s;
+      tile = full + (tile - full) / s;
+    }
+  }
   int g = 0, local = tile;
   if (a.tile_prefix != nullptr) {
     if (tile >= a.tile_prefix[a.num_groups]) return false;
@@ -99,6 +118,10 @@ __device__ __forceinline__ bool decode_tile(const SsmmArgs& a, int nt, int tile,
   const int per = (a.k_stages + ksplits - 1) / ksplits;
   ti.k0 = kspl * per;
   ti.k1 = min(a.k_stages, ti.k0 + per);
+  if (kpieces > 1) {
+    ti.k0 = kpiece * a.k_stages / kpieces;
+    ti.k1 = (kpiece + 1) * a.k_stages / kpieces;
+  }
   ti.t0 = n_tile * nt;
   ti.n_local = min(nt, n_g - ti.t0);
   ti.row0 = row0;
@@ -535,7 +558,10 @@ smy_status launch_t(const SsmmArgs& a, cudaStream_t s) {
   }
   if (a.max_tiles <= 0) return SMY_OK;
   const int grid = a.max_tiles < num_sms ? a.max_tiles : num_sms;
-  kern<<<grid, kThreads, C::kSmemBytes, s>>>(a);
+  SsmmArgs b = a;
+  b.workers = grid;
+  b.streamk = a.epi == kEpiScatter && a.k_splits <= 1 && !(a.debug & 512);
+  kern<<<grid, kThreads, C::kSmemBytes, s>>>(b);
   count_launch();
   return cuda_status(cudaGetLastError());
 }

@@ -490,7 +490,10 @@ smy_status launch_pair_t(const SsmmArgs& a, cudaStream_t s) {
   }
   if (a.max_tiles <= 0) return SMY_OK;
   const int pairs = a.max_tiles < num_sms / 2 ? a.max_tiles : num_sms / 2;
-  kern<<<2 * pairs, kPairThreads, C::kSmemBytes, s>>>(a);
+  SsmmArgs b = a;
+  b.workers = pairs;
+  b.streamk = a.epi == kEpiScatter && a.k_splits <= 1 && !(a.debug & 512);
+  kern<<<2 * pairs, kPairThreads, C::kSmemBytes, s>>>(b);
   count_launch();
   return cuda_status(cudaGetLastError());
 }
