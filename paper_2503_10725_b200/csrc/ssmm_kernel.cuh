@@ -462,11 +462,22 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
           const int rl = ti.row0 + ti.t0 + c0 + (lane & 15);
           const int my_dst = (lane & 15) < jmax ? (a.sel_out ? a.sel_out[rl] : rl) : 0;
           const float my_s = (lane & 15) < jmax ? (a.scale ? a.scale[rl] : 1.f) : 0.f;
+          const int nv = (valid && !(a.debug & 8)) ? jmax : 0;
+          if (MS == 2 && nf == 1) {  // the default (1,2,V): 16 independent predicated reductions
+            float* ob = static_cast<float*>(a.out) + 2 * grp;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int dst = __shfl_sync(0xffffffffu, my_dst, j);
+              const float s = __shfl_sync(0xffffffffu, my_s, j);
+              if (j < nv) red_add_v2(ob + (int64_t)dst * a.ldo, s * v[0][0][j], s * v[0][1 % MS][j]);
+            }
+            continue;
+          }
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int dst = __shfl_sync(0xffffffffu, my_dst, j);
             const float s = __shfl_sync(0xffffffffu, my_s, j);
-            if (j >= jmax || !valid || (a.debug & 8)) continue;
+            if (j >= nv) continue;
             float* o = static_cast<float*>(a.out) + (int64_t)dst * a.ldo;
             if (MS == 1) {
               atomicAdd(o + cr, s * v[0][0][j]);

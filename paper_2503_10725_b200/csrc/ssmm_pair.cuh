@@ -427,28 +427,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           for (int p = 0; p < MS; ++p) tmem_ld16(tmem + lane_base + (w * MS + p) * NT + c0, v[w][p]);
         tmem_ld_wait();
         if (prof) pc[8] += clk() - tl0;
-        if (!valid || (a.debug & 8)) continue;
         const int jmax = min(16, ti.n_local - c0);
+        const int n = (valid && !(a.debug & 8)) ? jmax : 0;
+        if (a.epi == kEpiScatter) {
+          // destination rows / gate weights of these 16 tokens: one load per lane,
+          // broadcast by shuffle; then 16 independent predicated reductions
+          const int rl = ti.row0 + ti.t0 + c0 + (lane & 15);
+          const int my_dst = (lane & 15) < jmax ? (a.sel_out ? a.sel_out[rl] : rl) : 0;
+          const float my_s = (lane & 15) < jmax ? (a.scale ? a.scale[rl] : 1.f) : 0.f;
+          float* ob = static_cast<float*>(a.out) + 2 * grp;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int dst = __shfl_sync(0xffffffffu, my_dst, j);
+            const float sc = __shfl_sync(0xffffffffu, my_s, j);
+            if (j < n) red_add_v2(ob + (int64_t)dst * a.ldo, sc * v[0][0][j], sc * v[0][1][j]);
+          }
+          continue;
+        }
+        // compact epilogues: values first, then predicated stores walking one row pointer
+        uint32_t packed[16];
+        float2 f2[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          if (j >= jmax) break;
-          const int r = ti.row0 + ti.t0 + c0 + j;
-          if (a.epi == kEpiScatter) {
-            const int dst = a.sel_out ? a.sel_out[r] : r;
-            const float s = a.scale ? a.scale[r] : 1.f;
-            red_add_v2(static_cast<float*>(a.out) + (int64_t)dst * a.ldo + 2 * grp, s * v[0][0][j], s * v[0][1][j]);
-          } else if (NW == 2) {
-            float act[2];
-#pragma unroll
-            for (int p = 0; p < 2; ++p) act[p] = silu_mul(v[0][p][j], v[NW - 1][p][j]);
-            *reinterpret_cast<__nv_bfloat162*>(static_cast<uint16_t*>(a.out) + (int64_t)r * a.ldo + 2 * grp) =
-                __floats2bfloat162_rn(act[0], act[1]);
-          } else if (a.out_bf16) {
-            *reinterpret_cast<__nv_bfloat162*>(static_cast<uint16_t*>(a.out) + (int64_t)r * a.ldo + 2 * grp) =
-                __floats2bfloat162_rn(v[0][0][j], v[0][1][j]);
+          if (NW == 2) {
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(silu_mul(v[0][0][j], v[NW - 1][0][j]),
+                                                            silu_mul(v[0][1][j], v[NW - 1][1][j]));
+            packed[j] = *reinterpret_cast<const uint32_t*>(&h2);
           } else {
-            *reinterpret_cast<float2*>(static_cast<float*>(a.out) + (int64_t)r * a.ldo + 2 * grp) =
-                make_float2(v[0][0][j], v[0][1][j]);
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(v[0][0][j], v[0][1][j]);
+            packed[j] = *reinterpret_cast<const uint32_t*>(&h2);
+            f2[j] = make_float2(v[0][0][j], v[0][1][j]);
+          }
+        }
+        const int64_t r0 = ti.row0 + ti.t0 + c0;
+        if (NW == 2 || a.out_bf16) {
+          uint32_t* o = reinterpret_cast<uint32_t*>(static_cast<uint16_t*>(a.out) + r0 * a.ldo + 2 * grp);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (j < n) *o = packed[j];
+            o += a.ldo / 2;
+          }
+        } else {
+          float2* o = reinterpret_cast<float2*>(static_cast<float*>(a.out) + r0 * a.ldo + 2 * grp);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (j < n) *o = f2[j];
+            o += a.ldo / 2;
           }
         }
       }
