@@ -427,7 +427,8 @@ def run_ours(args):
             {"bound": "hbm", "achieved": ach_gbs, "peak": hbm, "unit": "GB/s", "frac": ach_gbs / hbm,
              "traffic": None, "peak_source": f"{src} hbm_gbs"})
     roof["traffic"] = ncu_traffic(model, T, gate_up_kernel(T * k // E, f))
-    roof.update({"kernel": gate_up_kernel(T * k // E, f) + " gate/up (fused SiLU*up)", "per_launch_ms": ph_ms[2],
+    roof.update({"kernel": gate_up_kernel(T * k // E, f) + " interleaved gate/up (fused SiLU*up)",
+                 "per_launch_ms": ph_ms[2],
                  "algorithmic_flops": flops_gu, "algorithmic_bytes": bytes_gu,
                  "other_view": ({"achieved_gbs": ach_gbs, "hbm_frac": ach_gbs / hbm} if tensor_bound else
                                 {"achieved_tflops": ach_tf, "sparse_frac": ach_tf / sparse_peak})})
@@ -464,22 +465,23 @@ def run_ours(args):
     return 0
 
 
-def nt_gate_up(tokens_per_expert):
-    """Token tile the library picks for the fused gate/up launch (ssmm.cu table)."""
-    for nt in (16, 32, 64, 112):
-        if nt >= tokens_per_expert:
+def nt_pick(tokens_per_expert):
+    """Token tile the library picks (moe.cu: mean + 3 sigma tokens per expert, then
+    the smallest NW=1, M=2 tile of ssmm.cu's table that holds it)."""
+    hi = tokens_per_expert + int(3.0 * tokens_per_expert ** 0.5 + 0.999)
+    for nt in (16, 32, 64, 128, 224):
+        if nt >= hi:
             return nt
-    return 112
+    return 224
 
 
 def gate_up_kernel(tokens_per_expert, f):
-    """Name of the fused gate/up SSMM kernel the library launches (ssmm.cu:
-    ssmm_pick_nt / ssmm_pair_cluster) -- the key into the ncu summary."""
-    nt = nt_gate_up(tokens_per_expert)
-    m_tiles = (f // 2 + 127) // 128        # (1,2,V): f/2 compressed rows per weight
-    if tokens_per_expert >= 64 and nt in (64, 112) and m_tiles % 2 == 0:
-        return "ssmm_pair_kernel<%d, 2>" % nt
-    return "ssmm_kernel<%d, 2, 2, 1>" % nt
+    """Name of the interleaved gate/up SSMM kernel the library launches (moe.cu /
+    ssmm.cu: ssmm_pick_nt, ssmm_pair_cluster) -- the key into the ncu summary."""
+    nt = nt_pick(tokens_per_expert)
+    if tokens_per_expert >= 64 and nt in (128, 224):
+        return "ssmm_pair_kernel<%d, 1>" % nt
+    return "ssmm_kernel<%d, 1, 2, 1>" % nt
 
 
 def ncu_traffic(model, T, kernel):
