@@ -15,13 +15,19 @@ ki, mi, ui, vi = (hdr.index(c) for c in ("Kernel Name", "Metric Name", "Metric U
 scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
 tot = defaultdict(float)
 cnt = defaultdict(int)
+seen = defaultdict(int)   # SSMM launches of the same instantiation within one layer call
 for r in rows[1:]:
     if r[mi] != "gpu__time_duration.sum":
         continue
     name = re.sub(r"\(.*", "", r[ki])
+    if "route_topk" in name:
+        seen.clear()
+    if "ssmm" in name:       # gate/up and down may share an instantiation: label by call order
+        seen[name] += 1
+        name += " [%s]" % ("gate/up" if seen[name] == 1 else "down")
     tot[name] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
     cnt[name] += 1
-setup = re.compile(sys.argv[2] if len(sys.argv) > 2 else r"synth_kernel|encode_kernel|pack_kernel|native::|cuda::")
+setup = re.compile(sys.argv[2] if len(sys.argv) > 2 else r"synth_kernel|encode_kernel|pack_kernel|interleave_rows_kernel|native::|cuda::")
 all_us = sum(tot.values())
 layer_us = sum(t for n, t in tot.items() if not setup.search(n))
 print(f"# {sys.argv[1]}: {sum(cnt.values())} launches, {all_us:.1f} us total (ncu-serialised, cold cache);")
