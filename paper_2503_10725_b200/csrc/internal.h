@@ -59,6 +59,7 @@ struct SsmmArgs {
   int k_splits;            // >1: split K across tiles (SCATTER epilogue only; partial sums add)
   int streamk;             // 1: last partial wave of tiles split along K over all workers (SCATTER only)
   int workers;             // CTAs (single) / CTA pairs (pair kernel) of the launch; set by the launcher
+  int m_fastest;           // tile order: m-tile fastest (B shared in L2) instead of n-tile fastest
   int debug;               // profiling switches (env SMY_DEBUG): 1 no gather copies, 2 no weight
                            // copies, 4 no MMAs, 8 no epilogue math/stores -- results are garbage;
                            // 128: per-role cycle counters into `prof` (results valid)

@@ -110,8 +110,18 @@ __device__ __forceinline__ bool decode_tile(const SsmmArgs& a, int nt, int tile,
   const int n_g = a.offsets ? a.offsets[g + 1] - row0 : a.n_sel;
   const int n_tiles = (n_g + nt - 1) / nt;
   ti.g = g;
-  const int mk = local / n_tiles;              // (m_tile, k_split), k_split fastest
-  const int n_tile = local % n_tiles;
+  int mk, n_tile;                              // mk = (m_tile, k_split), k_split fastest
+  if (a.m_fastest && n_tiles > 1) {
+    // m fastest: concurrently running tiles share the token tile (B) in L2 -- the
+    // down launch, whose B (the compact intermediate) is larger than its weights
+    const int mk_count = a.tile_prefix != nullptr ? (a.tile_prefix[g + 1] - a.tile_prefix[g]) / n_tiles
+                                                   : a.max_tiles / n_tiles;
+    n_tile = local / mk_count;
+    mk = local % mk_count;
+  } else {
+    mk = local / n_tiles;
+    n_tile = local % n_tiles;
+  }
   const int ksplits = a.k_splits > 1 ? a.k_splits : 1;
   ti.m_tile = mk / ksplits;
   const int kspl = mk % ksplits;
@@ -130,6 +140,32 @@ __device__ __forceinline__ bool decode_tile(const SsmmArgs& a, int nt, int tile,
 
 // silu(g) * u (MUFU ex2 + rcp; measured faster here than hand-written .ftz PTX)
 __device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g, 1.f + __expf(-g)) * u; }
+
+// Scatter-add of one 16-token chunk for the default (1,2,V) weights: lane l holds
+// output columns (2 grp, 2 grp + 1) of 16 tokens (v0 / v1 = slot 0 / 1).  Lane pairs
+// (l even, l + 1) cover 4 adjacent columns, so each token pair (j, j + 1) costs one
+// shuffle of two values and ONE 16-byte red.add.v4 per lane -- even lanes write token
+// j, odd lanes token j + 1 -- instead of one 8-byte reduction per lane and token.
+// my_dst / my_s: destination row and routing weight of token (lane & 15); n: tokens
+// of the chunk this lane may write (0 if its rows are invalid).
+__device__ __forceinline__ void scatter_chunk_v4(const float (&v0)[16], const float (&v1)[16], int my_dst, float my_s,
+                                                 int n, float* out, int64_t ldo, int grp, int lane) {
+  const int odd = lane & 1;
+  float* base = out + 2 * (grp - odd);
+#pragma unroll
+  for (int j = 0; j < 16; j += 2) {
+    const int mine = j + odd;                                  // the token this lane writes
+    const int dst = __shfl_sync(0xffffffffu, my_dst, mine);
+    const float s = __shfl_sync(0xffffffffu, my_s, mine);
+    const float r0 = __shfl_xor_sync(0xffffffffu, odd ? v0[j] : v0[j + 1], 1);
+    const float r1 = __shfl_xor_sync(0xffffffffu, odd ? v1[j] : v1[j + 1], 1);
+    if (mine < n) {
+      float* o = base + (int64_t)dst * ldo;
+      if (odd) red_add_v4(o, s * r0, s * r1, s * v0[j + 1], s * v1[j + 1]);
+      else red_add_v4(o, s * v0[j], s * v1[j], s * r0, s * r1);
+    }
+  }
+}
 
 // Interleaved gate/up epilogue (kEpiSiluMulIlv, reading R20) for one 16-column
 // chunk of one warp: its 32 TMEM lanes are 16 gate rows (lanes 0-15) and the up
@@ -464,13 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
           const float my_s = (lane & 15) < jmax ? (a.scale ? a.scale[rl] : 1.f) : 0.f;
           const int nv = (valid && !(a.debug & 8)) ? jmax : 0;
           if (MS == 2 && nf == 1) {  // the default (1,2,V): 16 independent predicated reductions
-            float* ob = static_cast<float*>(a.out) + 2 * grp;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int dst = __shfl_sync(0xffffffffu, my_dst, j);
-              const float s = __shfl_sync(0xffffffffu, my_s, j);
-              if (j < nv) red_add_v2(ob + (int64_t)dst * a.ldo, s * v[0][0][j], s * v[0][1 % MS][j]);
-            }
+            scatter_chunk_v4(v[0][0], v[0][1 % MS], my_dst, my_s, nv, static_cast<float*>(a.out), a.ldo, grp, lane);
             continue;
           }
 #pragma unroll
@@ -572,6 +602,7 @@ smy_status launch_t(const SsmmArgs& a, cudaStream_t s) {
   SsmmArgs b = a;
   b.workers = grid;
   b.streamk = a.epi == kEpiScatter && a.k_splits <= 1 && !(a.debug & 512);
+  b.m_fastest = a.epi == kEpiScatter && !(a.debug & 2048);
   kern<<<grid, kThreads, C::kSmemBytes, s>>>(b);
   count_launch();
   return cuda_status(cudaGetLastError());

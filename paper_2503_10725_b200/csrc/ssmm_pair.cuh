@@ -138,7 +138,11 @@ struct PairCfg {
   static constexpr int kPeerPl = 128;                       // the peer m-tile's index planes (leader)
   static constexpr int kStageBytes = (NW * kWStride + kBBytes + kPeerPl + 1023) / 1024 * 1024;
   static constexpr int kAccCols = NW * MS * NT;
-  static constexpr int kECol = (kAccCols + 3) / 4 * 4;
+  // two accumulator sets when they fit (NT <= 112 at NW = 1): the epilogue drains
+  // tile i while the MMAs of tile i+1 run -- for short-K launches whose epilogue is
+  // as long as their main loop
+  static constexpr int kAccBufs = 2 * kAccCols + 16 <= 512 ? 2 : 1;
+  static constexpr int kECol = (kAccBufs * kAccCols + 3) / 4 * 4;
   static constexpr int kColsNeeded = kECol + 16;            // E: 2 buffers x 2 issuer warps x 4 cols
   static constexpr int kTmemCols = kColsNeeded <= 128 ? 128 : kColsNeeded <= 256 ? 256 : 512;
   static constexpr int kAux = 2048;
@@ -163,9 +167,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   uint8_t* aux = smem + S * C::kStageBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(aux);
   uint64_t* empty = full + S;
-  uint64_t* acc_full = empty + S;
-  uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  constexpr int AB = C::kAccBufs;
+  uint64_t* acc_full = empty + S;      // [AB]
+  uint64_t* acc_empty = acc_full + 2;  // [AB]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const uint32_t cta = cluster_rank();
   const bool leader = cta == 0;
@@ -178,8 +183,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       mbar_init(&full[s], leader ? 1 + (gather ? kGatherThreads + 1 : 0) : (gather ? kGatherThreads : 1));
       mbar_init(&empty[s], 2);  // both issuer warps' commits
     }
-    mbar_init(acc_full, 2);  // both issuer warps' commits
-    mbar_init(acc_empty, 2 * kPairEpiWarps);  // every epilogue warp of both CTAs
+    for (int b = 0; b < AB; ++b) {
+      mbar_init(&acc_full[b], 2);                  // both issuer warps' commits
+      mbar_init(&acc_empty[b], 2 * kPairEpiWarps);  // every epilogue warp of both CTAs
+    }
     fence_mbar_init();
   }
   if (warp == 5) tmem_alloc2(tmem_slot, C::kTmemCols);
@@ -264,7 +271,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       const unsigned long long tstart = prof ? clk() : 0;
       for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep, ++tcount) {
         unsigned long long t0 = prof ? clk() : 0;
-        mbar_wait_acq_cluster(acc_empty, tcount & 1);  // both epilogues drained and re-zeroed
+        const int ab = tcount % AB;
+        const uint32_t tacc = tm + ab * C::kAccCols;
+        mbar_wait_acq_cluster(&acc_empty[ab], (tcount / AB) & 1);  // both epilogues drained and re-zeroed
         if (prof) pc[1] += clk() - t0;
         tc_fence_after();
         const uint32_t idesc = __reduce_or_sync(0xffffffffu, idesc0 | ((uint32_t)(2 * pair_half(ti.n_local)) >> 3) << 17);
@@ -303,13 +312,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 #pragma unroll
               for (int q = 0; q < 8; ++q) mask[q] = p ? ~pl[kb][q] : pl[kb][q];  // disable lanes idx != p
               if (!(a.debug & 4))
-                tc_mma_sp2_elect(tm + (w * MS + p) * NT, adesc, bdesc, idesc | (uint32_t)(kb & 1), mask,
+                tc_mma_sp2_elect(tacc + (w * MS + p) * NT, adesc, bdesc, idesc | (uint32_t)(kb & 1), mask,
                                  tm + ecol + (kb & 2));
             }
           }
           tc_commit2_mc_elect(&empty[st], 0x3);
         }
-        tc_commit2_mc_elect(acc_full, 0x3);
+        tc_commit2_mc_elect(&acc_full[ab], 0x3);
         pc[7] += 1;
       }
       if (prof) pc[2] = clk() - tstart;
@@ -379,17 +388,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     const int h = warp >= 10 ? 1 : 0;
     const uint32_t lane_base = (uint32_t)(32 * q) << 16;
     const uint32_t acc_empty_leader = mapa_shared(smem_u32(acc_empty), 0);
-    auto zero_acc = [&]() {
+    auto zero_acc = [&](int b) {
       // the same (weight, slot, chunk) split as the reads: regions start at j*NT,
       // and NT (e.g. 112) need not be a multiple of 32
       for (int j = 0; j < NW * MS; ++j)
-        for (int c = 16 * h; c < NT; c += 32) tmem_st16_zero(tmem + lane_base + j * NT + c);
+        for (int c = 16 * h; c < NT; c += 32) tmem_st16_zero(tmem + lane_base + b * C::kAccCols + j * NT + c);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(acc_empty_leader);
+      if (lane == 0) mbar_arrive_cluster(acc_empty_leader + 8 * b);
     };
-    zero_acc();
+    for (int b = 0; b < AB; ++b) zero_acc(b);
     uint32_t tcount = 0;
     TileInfo ti;
     const bool ilv = NW == 1 && a.epi == kEpiSiluMulIlv;
@@ -399,7 +408,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       const bool valid = m_own < a.m_tiles && cr < a.R;
       const int grp = cr;  // (1,2,V): one compressed row per group
       unsigned long long t0 = prof ? clk() : 0;
-      mbar_wait_acq_cluster(acc_full, tcount & 1);
+      const int ab = tcount % AB;
+      const uint32_t tacc = tmem + ab * C::kAccCols;
+      mbar_wait_acq_cluster(&acc_full[ab], (tcount / AB) & 1);
       if (prof) { const unsigned long long t1 = clk(); pc[3] += t1 - t0; t0 = t1; }
       tc_fence_after();
       if (ilv) {
@@ -409,8 +420,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         for (int c0 = 16 * h; c0 < ti.n_local; c0 += 32) {
           float v[2][16];
           const unsigned long long tl0 = prof ? clk() : 0;
-          tmem_ld16(tmem + lane_base + c0, v[0]);
-          tmem_ld16(tmem + lane_base + NT + c0, v[1]);
+          tmem_ld16(tacc + lane_base + c0, v[0]);
+          tmem_ld16(tacc + lane_base + NT + c0, v[1]);
           tmem_ld_wait();
           if (prof) pc[8] += clk() - tl0;
           if (!(a.debug & 32))
@@ -424,7 +435,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 #pragma unroll
         for (int w = 0; w < NW; ++w)
 #pragma unroll
-          for (int p = 0; p < MS; ++p) tmem_ld16(tmem + lane_base + (w * MS + p) * NT + c0, v[w][p]);
+          for (int p = 0; p < MS; ++p) tmem_ld16(tacc + lane_base + (w * MS + p) * NT + c0, v[w][p]);
         tmem_ld_wait();
         if (prof) pc[8] += clk() - tl0;
         const int jmax = min(16, ti.n_local - c0);
@@ -435,13 +446,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           const int rl = ti.row0 + ti.t0 + c0 + (lane & 15);
           const int my_dst = (lane & 15) < jmax ? (a.sel_out ? a.sel_out[rl] : rl) : 0;
           const float my_s = (lane & 15) < jmax ? (a.scale ? a.scale[rl] : 1.f) : 0.f;
-          float* ob = static_cast<float*>(a.out) + 2 * grp;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int dst = __shfl_sync(0xffffffffu, my_dst, j);
-            const float sc = __shfl_sync(0xffffffffu, my_s, j);
-            if (j < n) red_add_v2(ob + (int64_t)dst * a.ldo, sc * v[0][0][j], sc * v[0][1][j]);
-          }
+          scatter_chunk_v4(v[0][0], v[0][1], my_dst, my_s, n, static_cast<float*>(a.out), a.ldo, grp, lane);
           continue;
         }
         // compact epilogues: values first, then predicated stores walking one row pointer
@@ -478,7 +483,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       }
       const unsigned long long tz0 = prof ? clk() : 0;
       tc_fence_before();
-      zero_acc();
+      zero_acc(ab);
       if (prof) { const unsigned long long t1 = clk(); pc[9] += t1 - tz0; pc[4] += t1 - t0; }
     }
   }
@@ -517,6 +522,7 @@ smy_status launch_pair_t(const SsmmArgs& a, cudaStream_t s) {
   SsmmArgs b = a;
   b.workers = pairs;
   b.streamk = a.epi == kEpiScatter && a.k_splits <= 1 && !(a.debug & 512);
+  b.m_fastest = a.epi == kEpiScatter && !(a.debug & 2048);
   kern<<<2 * pairs, kPairThreads, C::kSmemBytes, s>>>(b);
   count_launch();
   return cuda_status(cudaGetLastError());
