@@ -132,8 +132,12 @@ __device__ __forceinline__ bool decode_tile(const SsmmArgs& a, int nt, int tile,
     ti.k0 = kpiece * a.k_stages / kpieces;
     ti.k1 = (kpiece + 1) * a.k_stages / kpieces;
   }
-  ti.t0 = n_tile * nt;
-  ti.n_local = min(nt, n_g - ti.t0);
+  // the group's tokens are cut into n_tiles near-equal tiles (widths rounded up to
+  // 16, the MMA N granule) rather than full tiles plus a ragged one: equal-cost
+  // tiles balance the static schedule
+  const int tper = (a.debug & 8192) ? nt : min(nt, (((n_g + n_tiles - 1) / n_tiles) + 15) & ~15);
+  ti.t0 = n_tile * tper;
+  ti.n_local = min(tper, n_g - ti.t0);
   ti.row0 = row0;
   return true;
 }

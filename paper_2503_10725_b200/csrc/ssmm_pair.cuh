@@ -204,6 +204,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 
   const bool prof = a.prof != nullptr;
   unsigned long long pc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  auto gtime = []() { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
+  const unsigned long long g_start = prof ? gtime() : 0;
   auto clk = []() { unsigned long long c; asm volatile("mov.u64 %0, %%clock64;" : "=l"(c)); return c; };
   if (warp == 4) {
     // ========= producer: own weight tiles + contiguous B half (TMA, completing on
@@ -495,6 +497,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     if (warp == 6 && lane == 0) { atomicAdd(o + 10, pc[10]); atomicAdd(o + 11, pc[11]); }
     if (warp == 0 && lane == 0) { atomicAdd(o + 3, pc[3]); atomicAdd(o + 4, pc[4]); atomicAdd(o + 8, pc[8]); atomicAdd(o + 9, pc[9]); }
     if (warp == 4 && lane == 0) { atomicAdd(o + 5, pc[5]); }
+  }
+  if (prof) {  // CTA lifetime (ns) up to here, and the time its MMA work ended
+    unsigned long long* o = a.prof + ((size_t)(a.epi == kEpiScatter) * 148 + blockIdx.x) * 16;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned long long g_end = gtime();
+      atomicAdd(o + 13, g_end - g_start);
+      o[14] = g_start;  // the last call's start / end (absolute ns)
+      o[15] = g_end;
+    }
   }
   tc_fence_before();
   __syncthreads();

@@ -31,7 +31,8 @@ R = 5
 for _ in range(R):
     layer(x, lg, out)
 lib.smy_debug_prof(buf, 148)
-A = np.array(buf, dtype=np.float64).reshape(2, 148, 16) / R / 1e3
+raw = np.array(buf, dtype=np.float64).reshape(2, 148, 16)
+A = raw / R / 1e3
 for name, a in zip(("gate/up", "down"), A):
     lead = a[0::2]
     t = max(lead[:, 7].mean(), 1e-9)
@@ -40,5 +41,12 @@ for name, a in zip(("gate/up", "down"), A):
           % (lead[:, 2].mean(), lead[:, 0].mean(), lead[:, 1].mean(), (lead[:, 2] - lead[:, 0] - lead[:, 1]).mean()))
     print("  gather warp: wait_empty %.1f  issue %.1f (leader) / %.1f %.1f (peer)"
           % (lead[:, 10].mean(), lead[:, 11].mean(), a[1::2, 10].mean(), a[1::2, 11].mean()))
+    r = raw[0 if name == "gate/up" else 1]
+    live = r[:, 14] > 0
+    if live.any():
+        st, en = r[live, 14], r[live, 15]
+        print("  CTA lifetime %.1f us (mean), max %.1f us; last call: CTA starts spread %.1f us, ends spread %.1f us,"
+              " span %.1f us" % (a[:, 13].mean(), a[:, 13].max(), (st.max() - st.min()) / 1e3,
+                                 (en.max() - en.min()) / 1e3, (en.max() - st.min()) / 1e3))
     print("  epilogue: wait_acc_full %.1f  work %.1f (tmem_ld %.1f, zero %.1f)   producer wait_empty %.1f"
           % tuple(a[:, i].mean() for i in (3, 4, 8, 9, 5)))
