@@ -264,8 +264,21 @@ smy_status samoyeds_ssmm(const smy_weight* w, const smy_weight* w2, const void* 
   a.ldo = ldo;
   a.sel_out = sel;
   a.scale = scale;
-  a.max_tiles = g.m_tiles * ((n_sel + nt - 1) / nt);
   a.weights_stream = n_sel <= nt;
+  // >= 64 tokens of a (1,2,V) weight: CTA-pair tiles (M = 256, cta_group::2), as in the layer
+  const smy_weight* w0a[1] = {w};
+  const smy_weight* w1a[1] = {nw == 2 ? w2 : nullptr};
+  const size_t img = (size_t)g.m_tiles * g.k_stages * g.block;
+  const int cl = ssmm_pair_images_ok(w0a, nw == 2 ? w1a : nullptr, 1, img)
+                     ? ssmm_pair_cluster(nt, nw, g.ms, g.rep, g.m_tiles, n_sel)
+                     : 0;
+  if (cl) {
+    a.max_tiles = ((g.m_tiles + 1) / 2) * ((n_sel + nt - 1) / nt);
+    a.k_splits = 1;  // scatter-add balance comes from the stream-K tail
+    if ((st = make_x_tmap(&a.tmap_x, x_bf16, w->d.cols, x_rows, ldx, nt / 2)) != SMY_OK) return st;
+    return ssmm_launch_pair(a, nt, nw, cl, static_cast<cudaStream_t>(stream));
+  }
+  a.max_tiles = g.m_tiles * ((n_sel + nt - 1) / nt);
   a.k_splits = a.epi == kEpiScatter ? ssmm_pick_ksplit(a.max_tiles, g.k_stages) : 1;
   a.max_tiles *= a.k_splits;
   if ((st = make_x_tmap(&a.tmap_x, x_bf16, w->d.cols, x_rows, ldx, nt)) != SMY_OK) return st;
