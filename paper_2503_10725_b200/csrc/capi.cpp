@@ -265,6 +265,20 @@ smy_status samoyeds_ssmm(const smy_weight* w, const smy_weight* w2, const void* 
   a.sel_out = sel;
   a.scale = scale;
   a.weights_stream = n_sel <= nt;
+  // Too few tiles to fill the GPU with an fp32 COMPACT output (small M, long K): zero the
+  // output and run it as a scatter-add into rows 0..n_sel-1 -- K is then split over the
+  // SMs (split-K / stream-K tail) and the partial sums add.
+  {
+    const int64_t tiles = (int64_t)g.m_tiles * ((n_sel + nt - 1) / nt);
+    if (a.epi == kEpiCompact && !a.out_bf16 && tiles < 74 && g.k_stages >= 16) {
+      cudaError_t ce = cudaMemset2DAsync(out, (size_t)ldo * 4, 0, (size_t)w->d.rows * 4, (size_t)n_sel,
+                                         static_cast<cudaStream_t>(stream));
+      if (ce != cudaSuccess) return cuda_status(ce);
+      a.epi = kEpiScatter;
+      a.sel_out = nullptr;  // destination row = compact row
+      a.scale = nullptr;
+    }
+  }
   // >= 64 tokens of a (1,2,V) weight: CTA-pair tiles (M = 256, cta_group::2), as in the layer
   const smy_weight* w0a[1] = {w};
   const smy_weight* w1a[1] = {nw == 2 ? w2 : nullptr};
@@ -276,7 +290,7 @@ smy_status samoyeds_ssmm(const smy_weight* w, const smy_weight* w2, const void* 
     a.max_tiles = ((g.m_tiles + 1) / 2) * ((n_sel + nt - 1) / nt);
     a.k_splits = 1;  // scatter-add balance comes from the stream-K tail
     if ((st = make_x_tmap(&a.tmap_x, x_bf16, w->d.cols, x_rows, ldx, nt / 2)) != SMY_OK) return st;
-    return ssmm_launch_pair(a, nt, nw, cl, static_cast<cudaStream_t>(stream));
+    return ssmm_launch_pair(a, nt, nw, g.ms, cl, static_cast<cudaStream_t>(stream));
   }
   a.max_tiles = g.m_tiles * ((n_sel + nt - 1) / nt);
   a.k_splits = a.epi == kEpiScatter ? ssmm_pick_ksplit(a.max_tiles, g.k_stages) : 1;

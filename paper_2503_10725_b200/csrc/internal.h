@@ -85,7 +85,7 @@ smy_status ssmm_launch(const SsmmArgs& a, int nt, int nw, int ms, int rep, cudaS
 // CTA-pair (cta_group::2) kernel: a.m_tiles / tile prefixes count m-tile PAIRS, tmap box = nt/2 rows
 // returns the cluster size to use (2: one MMA pair, 4: two pairs sharing weights) or 0 (single CTA)
 int ssmm_pair_cluster(int nt, int nw, int ms, int rep, int m_tiles, int64_t tokens_per_group);
-smy_status ssmm_launch_pair(const SsmmArgs& a, int nt, int nw, int cl, cudaStream_t s);
+smy_status ssmm_launch_pair(const SsmmArgs& a, int nt, int nw, int ms, int cl, cudaStream_t s);
 // can one tensor map address all these images (else: single-CTA kernel)
 bool ssmm_pair_images_ok(const smy_weight* const* w0, const smy_weight* const* w1, int groups, size_t img_bytes);
 

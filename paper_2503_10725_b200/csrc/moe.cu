@@ -133,7 +133,7 @@ static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* 
   a.k_splits = k_splits;
   smy_status st = make_x_tmap(&a.tmap_x, x, k_cols, x_rows, ldx, cl ? nt / 2 : nt);
   if (st != SMY_OK) return st;
-  return cl ? ssmm_launch_pair(a, nt, nw, cl, s) : ssmm_launch(a, nt, nw, g.ms, g.rep, s);
+  return cl ? ssmm_launch_pair(a, nt, nw, g.ms, cl, s) : ssmm_launch(a, nt, nw, g.ms, g.rep, s);
 }
 
 // The expert computation over T rows of x.  Routing either comes from router

@@ -30,10 +30,12 @@ extern template smy_status launch_t<16,1,16,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<32,2,4,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<16,2,8,1>(const SsmmArgs&, cudaStream_t);
 
-extern template smy_status launch_pair_t<64, 2>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<112, 2>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<128, 1>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<224, 1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<64, 2, 2>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<112, 2, 2>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<128, 1, 2>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<224, 1, 2>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<128, 1, 1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<256, 1, 1>(const SsmmArgs&, cudaStream_t);
 
 namespace {
 struct Entry { int nt, nw, ms, rep; smy_status (*fn)(const SsmmArgs&, cudaStream_t); };
@@ -81,8 +83,10 @@ int ssmm_pick_nt(int nw, int ms, int rep, int64_t tpg) {
 int ssmm_pair_cluster(int nt, int nw, int ms, int rep, int m_tiles, int64_t tokens_per_group) {
   if (debug_flags() & 16) return 0;  // SMY_DEBUG=16: force the single-CTA kernel
   // an odd m-tile count gives the last pair a phantom peer tile (loads repeated, stores masked)
-  if (ms != 2 || rep != 1 || m_tiles < 2 || tokens_per_group < 64) return 0;
-  if (!(nw == 2 ? (nt == 64 || nt == 112) : (nt == 128 || nt == 224))) return 0;
+  if (rep != 1 || m_tiles < 2 || tokens_per_group < 64) return 0;
+  if (ms == 2 && !(nw == 2 ? (nt == 64 || nt == 112) : (nt == 128 || nt == 224))) return 0;
+  if (ms == 1 && !(nw == 1 && (nt == 128 || nt == 256))) return 0;  // N == M: plain 2:4
+  if (ms != 1 && ms != 2) return 0;
   // (4-CTA clusters sharing weight stages by multicast measured 2x slower on
   // B200 -- probes/mcast_bench.cu -- and were removed)
   return 2;
@@ -110,12 +114,12 @@ bool ssmm_pair_images_ok(const smy_weight* const* w0, const smy_weight* const* w
   return (hi - lo) / 128 < ((uint64_t)1 << 31);
 }
 
-smy_status ssmm_launch_pair(const SsmmArgs& a0, int nt, int nw, int cl, cudaStream_t s) {
+smy_status ssmm_launch_pair(const SsmmArgs& a0, int nt, int nw, int ms, int cl, cudaStream_t s) {
   SsmmArgs a = a0;
   a.debug = debug_flags();
   a.prof = (a.debug & 128) ? debug_prof_buffer(148) : nullptr;
-  if (cl != 2 || a.planes != 1 || (a.block & 127)) {
-    set_last_error("ssmm: pair kernel needs (N,M) = (1,2) tiles of 128-B rows");
+  if (cl != 2 || a.planes != (ms == 2 ? 1 : 0) || (a.block & 127)) {
+    set_last_error("ssmm: pair kernel needs (N,M) = (1,2) or N == M tiles of 128-B rows");
     return SMY_E_CONFIG;
   }
   // one tensor map over every weight image of the launch (rows of 128 B)
@@ -144,10 +148,12 @@ smy_status ssmm_launch_pair(const SsmmArgs& a0, int nt, int nw, int cl, cudaStre
   a.wbase = reinterpret_cast<const uint8_t*>(lo);
   smy_status st = make_w_tmap(&a.tmap_w, a.wbase, (int64_t)((hi - lo) / 128), (kABytes + kEBytes + 64 + 127) / 128);
   if (st != SMY_OK) return st;
-  if (nw == 2 && nt == 64) return launch_pair_t<64, 2>(a, s);
-  if (nw == 2 && nt == 112) return launch_pair_t<112, 2>(a, s);
-  if (nw == 1 && nt == 128) return launch_pair_t<128, 1>(a, s);
-  if (nw == 1 && nt == 224) return launch_pair_t<224, 1>(a, s);
+  if (ms == 2 && nw == 2 && nt == 64) return launch_pair_t<64, 2, 2>(a, s);
+  if (ms == 2 && nw == 2 && nt == 112) return launch_pair_t<112, 2, 2>(a, s);
+  if (ms == 2 && nw == 1 && nt == 128) return launch_pair_t<128, 1, 2>(a, s);
+  if (ms == 2 && nw == 1 && nt == 224) return launch_pair_t<224, 1, 2>(a, s);
+  if (ms == 1 && nw == 1 && nt == 128) return launch_pair_t<128, 1, 1>(a, s);
+  if (ms == 1 && nw == 1 && nt == 256) return launch_pair_t<256, 1, 1>(a, s);
   set_last_error("ssmm: unsupported pair (nt, nw)");
   return SMY_E_CONFIG;
 }

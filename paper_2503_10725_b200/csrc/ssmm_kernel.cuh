@@ -602,10 +602,10 @@ smy_status launch_t(const SsmmArgs& a, cudaStream_t s) {
     configured = true;
   }
   if (a.max_tiles <= 0) return SMY_OK;
-  const int grid = a.max_tiles < num_sms ? a.max_tiles : num_sms;
   SsmmArgs b = a;
-  b.workers = grid;
   b.streamk = a.epi == kEpiScatter && a.k_splits <= 1 && !(a.debug & 512);
+  const int grid = (b.streamk || a.max_tiles >= num_sms) ? num_sms : a.max_tiles;
+  b.workers = grid;
   b.m_fastest = a.epi == kEpiScatter && !(a.debug & 2048);
   kern<<<grid, kThreads, C::kSmemBytes, s>>>(b);
   count_launch();

@@ -128,14 +128,16 @@ constexpr int kPairEpiWarps = 8;                    // warps 0-3 and 10-13
 __device__ __forceinline__ int pair_half(int n) { return ((n + 15) >> 4) << 3; }
 constexpr int kPairThreads = 32 * (11 + kPairEpiWarps - 4);  // + producer, 2 MMA issuers, 4 gather
 
-template <int NT, int NW>
+// MS = accumulator slots per weight: 2 for (1,2,V) (the lane-masked remap), 1 for
+// N == M (plain 2:4, no remap -- the weight-only-sparse baseline formats)
+template <int NT, int NW, int MS_ = 2>
 struct PairCfg {
-  static constexpr int MS = 2;
+  static constexpr int MS = MS_;
   static constexpr int kHalf = NT / 2;                      // tokens per CTA
   static constexpr int kWStride = 19456;                    // A|E|planes (kWRows rows of 128 B)
   static constexpr int kWRows = (kABytes + kEBytes + 64 + 127) / 128;  // TMA box rows of one weight tile
   static constexpr int kBBytes = kHalf * 256;               // 2 K-atoms x kHalf rows x 128 B
-  static constexpr int kPeerPl = 128;                       // the peer m-tile's index planes (leader)
+  static constexpr int kPeerPl = MS == 2 ? 128 : 0;         // the peer m-tile's index planes (leader)
   static constexpr int kStageBytes = (NW * kWStride + kBBytes + kPeerPl + 1023) / 1024 * 1024;
   static constexpr int kAccCols = NW * MS * NT;
   // two accumulator sets when they fit (NT <= 112 at NW = 1): the epilogue drains
@@ -155,12 +157,12 @@ struct PairCfg {
   static_assert(NT % 16 == 0 && (NT / 2) % 8 == 0 && NT >= 32 && NT <= 256, "UMMA N (cta_group::2) / 8-row halves");
 };
 
-template <int NT, int NW>
+template <int NT, int NW, int MS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     ssmm_pair_kernel(const __grid_constant__ SsmmArgs a) {
-  using C = PairCfg<NT, NW>;
+  using C = PairCfg<NT, NW, MS>;
   constexpr int S = C::kStages;
-  constexpr int MS = 2;
+  constexpr int kIssuers = (NW == 2 || MS == 2) ? 2 : 1;  // MMA-issuing warps
   constexpr int H = C::kHalf;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -181,10 +183,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       // leader: its producer's expect_tx (all TMA bytes of both CTAs) + its gather
       // threads + the peer's gather relay; peer: its gather threads (relayed)
       mbar_init(&full[s], leader ? 1 + (gather ? kGatherThreads + 1 : 0) : (gather ? kGatherThreads : 1));
-      mbar_init(&empty[s], 2);  // both issuer warps' commits
+      mbar_init(&empty[s], kIssuers);  // every issuer warp's commit
     }
     for (int b = 0; b < AB; ++b) {
-      mbar_init(&acc_full[b], 2);                  // both issuer warps' commits
+      mbar_init(&acc_full[b], kIssuers);           // every issuer warp's commit
       mbar_init(&acc_empty[b], 2 * kPairEpiWarps);  // every epilogue warp of both CTAs
     }
     fence_mbar_init();
@@ -212,7 +214,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     // the leader's full) + (leader) the peer m-tile's index planes =========
     if (lane == 0) {
       const uint32_t wbytes = (a.debug & 2) ? 0u : (uint32_t)C::kWRows * 128;
-      const uint32_t pair_bytes = 2 * (NW * wbytes + (gather ? 0u : (uint32_t)C::kBBytes)) + NW * 64u;
+      const uint32_t pair_bytes = 2 * (NW * wbytes + (gather ? 0u : (uint32_t)C::kBBytes)) + (MS == 2 ? NW * 64u : 0u);
       // prefill: the pairs on the same m-tile read its weights at about the same
       // time; evict_normal measured better than evict_first (fewer re-reads)
       const uint64_t pol_w = a.weights_stream ? policy_evict_first() : policy_evict_normal();
@@ -240,7 +242,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 #pragma unroll
           for (int w = 0; w < NW; ++w) {
             if (!(a.debug & 2)) tma2d_pair(wsm(st, w), &a.tmap_w, 0, wrow[w] + k * brows, bar, pol_w);
-            if (leader)
+            if (MS == 2 && leader)
               bulk_g2s(psm(st) + 64 * w, src[w] + ((size_t)m_peer * ks + k) * a.block + kABytes + kEBytes, 64,
                        &full[st], pol_w);
           }
@@ -253,7 +255,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       }
     }
   } else if (warp == 5 || warp == 14) {
-    if (leader) {
+    if (leader && (warp == 5 || kIssuers == 2)) {
       // ==================== MMA issuers (leader CTA, warps 5 and 14) ====================
       // The per-stage issue work (plane words -> uniform lane masks, descriptors,
       // elect) costs about as much as the tensor work itself, so two warps split
@@ -290,7 +292,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           tc_cp2_elect(tm + ecol, desc_interleave(sbase + w * C::kWStride + kABytes));
           uint32_t pl[4][8];  // lane planes: words 0-3 this CTA's 128 lanes, 4-7 the peer's
 #pragma unroll
-          for (int kb = 0; kb < 4; ++kb) {
+          for (int kb = 0; kb < 4 && MS == 2; ++kb) {
             const uint4 v = *reinterpret_cast<const uint4*>(wsm(st, w) + kABytes + kEBytes + kb * 16);
             const uint4 u = *reinterpret_cast<const uint4*>(psm(st) + 64 * w + kb * 16);
             pl[kb][0] = __reduce_or_sync(0xffffffffu, v.x);
@@ -312,7 +314,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
               const int p = NW == 2 ? pp : mi;
               uint32_t mask[8];
 #pragma unroll
-              for (int q = 0; q < 8; ++q) mask[q] = p ? ~pl[kb][q] : pl[kb][q];  // disable lanes idx != p
+              for (int q = 0; q < 8; ++q) mask[q] = MS == 1 ? 0u : p ? ~pl[kb][q] : pl[kb][q];  // disable idx != p
               if (!(a.debug & 4))
                 tc_mma_sp2_elect(tacc + (w * MS + p) * NT, adesc, bdesc, idesc | (uint32_t)(kb & 1), mask,
                                  tm + ecol + (kb & 2));
@@ -324,7 +326,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         pc[7] += 1;
       }
       if (prof) pc[2] = clk() - tstart;
-    } else if (warp == 5 && lane == 0 && gather) {
+    } else if (!leader && warp == 5 && lane == 0 && gather) {
       // ============== peer: forward "gather landed" to the leader's full ==============
       uint32_t it = 0;
       TileInfo ti;
@@ -448,7 +450,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           const int rl = ti.row0 + ti.t0 + c0 + (lane & 15);
           const int my_dst = (lane & 15) < jmax ? (a.sel_out ? a.sel_out[rl] : rl) : 0;
           const float my_s = (lane & 15) < jmax ? (a.scale ? a.scale[rl] : 1.f) : 0.f;
-          scatter_chunk_v4(v[0][0], v[0][1], my_dst, my_s, n, static_cast<float*>(a.out), a.ldo, grp, lane);
+          if constexpr (MS == 2) {
+            scatter_chunk_v4(v[0][0], v[0][1], my_dst, my_s, n, static_cast<float*>(a.out), a.ldo, grp, lane);
+          } else {  // N == M: lane = output row
+            float* ob = static_cast<float*>(a.out) + cr;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int dst = __shfl_sync(0xffffffffu, my_dst, j);
+              const float sc = __shfl_sync(0xffffffffu, my_s, j);
+              if (j < n) atomicAdd(ob + (int64_t)dst * a.ldo, sc * v[0][0][j]);
+            }
+          }
+          continue;
+        }
+        if constexpr (MS == 1) {  // N == M compact: lane = output row, fp32 or bf16
+          const int64_t r0 = ti.row0 + ti.t0 + c0;
+          if (a.out_bf16) {
+            uint16_t* o = static_cast<uint16_t*>(a.out) + r0 * a.ldo + cr;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (j < n) *o = __bfloat16_as_ushort(__float2bfloat16_rn(v[0][0][j]));
+              o += a.ldo;
+            }
+          } else {
+            float* o = static_cast<float*>(a.out) + r0 * a.ldo + cr;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (j < n) *o = v[0][0][j];
+              o += a.ldo;
+            }
+          }
           continue;
         }
         // compact epilogues: values first, then predicated stores walking one row pointer
@@ -458,12 +489,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         for (int j = 0; j < 16; ++j) {
           if (NW == 2) {
             const __nv_bfloat162 h2 = __floats2bfloat162_rn(silu_mul(v[0][0][j], v[NW - 1][0][j]),
-                                                            silu_mul(v[0][1][j], v[NW - 1][1][j]));
+                                                            silu_mul(v[0][1 % MS][j], v[NW - 1][1 % MS][j]));
             packed[j] = *reinterpret_cast<const uint32_t*>(&h2);
           } else {
-            const __nv_bfloat162 h2 = __floats2bfloat162_rn(v[0][0][j], v[0][1][j]);
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(v[0][0][j], v[0][1 % MS][j]);
             packed[j] = *reinterpret_cast<const uint32_t*>(&h2);
-            f2[j] = make_float2(v[0][0][j], v[0][1][j]);
+            f2[j] = make_float2(v[0][0][j], v[0][1 % MS][j]);
           }
         }
         const int64_t r0 = ti.row0 + ti.t0 + c0;
@@ -515,12 +546,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   if (warp == 5) tmem_dealloc2(tmem, C::kTmemCols);
 }
 
-template <int NT, int NW>
+template <int NT, int NW, int MS>
 smy_status launch_pair_t(const SsmmArgs& a, cudaStream_t s) {
-  using C = PairCfg<NT, NW>;
+  using C = PairCfg<NT, NW, MS>;
   static bool configured = false;
   static int num_sms = 0;
-  auto kern = ssmm_pair_kernel<NT, NW>;
+  auto kern = ssmm_pair_kernel<NT, NW, MS>;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return cuda_status(e);
@@ -530,10 +561,11 @@ smy_status launch_pair_t(const SsmmArgs& a, cudaStream_t s) {
     configured = true;
   }
   if (a.max_tiles <= 0) return SMY_OK;
-  const int pairs = a.max_tiles < num_sms / 2 ? a.max_tiles : num_sms / 2;
   SsmmArgs b = a;
-  b.workers = pairs;
   b.streamk = a.epi == kEpiScatter && a.k_splits <= 1 && !(a.debug & 512);
+  // stream-K launches use every pair: with fewer tiles than pairs the K pieces fill them
+  const int pairs = (b.streamk || a.max_tiles >= num_sms / 2) ? num_sms / 2 : a.max_tiles;
+  b.workers = pairs;
   b.m_fastest = a.epi == kEpiScatter && !(a.debug & 2048);
   kern<<<2 * pairs, kPairThreads, C::kSmemBytes, s>>>(b);
   count_launch();
