@@ -375,3 +375,63 @@ def test_moe_layer_all_tokens_one_expert(smy):
     fmt = F.SparseFormat(1, 2, 32)
     got, ref, S = _layer_case(smy, fmt, E=4, d=128, f=256, T=200, k=1, skew=50.0)
     check_tol(got, ref, S, "hot expert")
+
+
+# ------------------------------------------------ full size, bench launch configuration
+
+def _prune_rows(w_bits, fmt, chunk=512):
+    """oracle prune, row-chunked (pruning acts on M-row groups independently)."""
+    return np.concatenate([F.prune(w_bits[i:i + chunk], fmt) for i in range(0, w_bits.shape[0], chunk)])
+
+
+@pytest.mark.parametrize("T", [4096, 64])
+def test_moe_layer_full_size_sampled(smy, T):
+    """The bench's N=1 workload itself -- Mixtral-8x7B layer, T=4096 (interleaved
+    gate/up + stream-K down on CTA pairs) and its T=64 decode point (single-CTA
+    kernels), built by bench.build_layer -- checked
+    against the fp64 oracle on sampled outputs: every token routed to the most
+    common expert pair (up to 6 of them), 24 sampled output row pairs.  The
+    oracle regenerates the weights it needs by index (counter-based generator)
+    and prunes them itself."""
+    import bench
+    d, f, E, k, _ = bench.MODELS["mixtral"]
+    fmt = F.SparseFormat(1, 2, 32)
+    dev = torch.device("cuda")
+    layer = smy.MoELayer(smy.MoEConfig(E, k, d, f, 0, "renorm_topk", smy.Format(1, 2, 32)),
+                         bench.build_layer(smy, "mixtral", dev), max_tokens=T, device=dev)
+    x = torch.empty(T, d, dtype=torch.int16, device=dev)
+    smy.synth_fill(x, synth.SEED_X, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
+    lg = torch.empty(T, E, dtype=torch.float32, device=dev)
+    smy.synth_fill(lg, synth.SEED_LOGITS, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
+    out = layer(x, lg).cpu().numpy().astype(np.float64)
+    xh, lgh = host16(x), lg.cpu().numpy()
+    del layer
+    torch.cuda.empty_cache()
+
+    ids, gw = moe.route(lgh, k, moe.RENORM_TOPK)
+    pairs = [tuple(sorted(r)) for r in ids]
+    pair = max(set(pairs), key=pairs.count)
+    toks = np.array([t for t in range(T) if pairs[t] == pair][:6])
+    xs = bf16.to_f64(xh[toks])
+    rng = np.random.default_rng(3)
+    groups = rng.choice(d // 2, 24, replace=False)
+    orow = np.sort(np.concatenate([2 * groups, 2 * groups + 1]))
+
+    def dense(seed, rows, cols, idx0=0):
+        t = torch.empty(rows, cols, dtype=torch.int16, device=dev)
+        smy.synth_fill(t, seed, synth.DIST_UNIFORM, float(synth.uniform_scale(np.sqrt(3.0 / cols))), idx0=idx0)
+        return host16(t)
+
+    ref = np.zeros((len(toks), len(orow)))
+    S = np.zeros_like(ref)
+    for e in pair:
+        wg = bf16.to_f64(_prune_rows(dense(synth.weight_seed(e, 0), f, d), fmt))
+        wu = bf16.to_f64(_prune_rows(dense(synth.weight_seed(e, 1), f, d), fmt))
+        a = bf16.to_f64(OS.silu_mul_bf16(xs @ wg.T, xs @ wu.T))             # [toks x f] bf16 intermediate
+        del wg, wu
+        wd = np.concatenate([dense(synth.weight_seed(e, 2), 2, f, idx0=int(2 * g) * f) for g in np.sort(groups)])
+        wd = bf16.to_f64(F.prune(wd, fmt))                                    # rows orow
+        g_e = np.array([gw[t][list(ids[t]).index(e)] for t in toks])[:, None]
+        ref += g_e * (a @ wd.T)
+        S += np.abs(g_e) * (np.abs(a) @ np.abs(wd).T)
+    check_tol(out[np.ix_(toks, orow)], ref, S, f"Mixtral T={T} layer, tokens {toks.tolist()} (experts {pair})")
