@@ -19,6 +19,10 @@
 // `acc_full`; both epilogues arrive on the leader's `acc_empty`.
 #include "ssmm_kernel.cuh"
 
+#ifndef SMY_CLUSTER_ACQ_ALL
+#define SMY_CLUSTER_ACQ_ALL 0
+#endif
+
 namespace smy {
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -54,6 +58,25 @@ __device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t pa
         : "r"(addr), "r"(parity)
         : "memory");
 #endif
+  } while (!done);
+}
+// CTA-scope acquire (no L1 invalidation): waits whose consumers are tcgen05 /
+// TMA / cp.async operations ordered by the tcgen05 fences, not generic loads of
+// the peer CTA's writes (the pattern CUTLASS's 2-SM pipelines use)
+__device__ __forceinline__ void mbar_wait_cta(uint64_t* bar, uint32_t parity) {
+  if (SMY_CLUSTER_ACQ_ALL) {
+    mbar_wait_acq_cluster(bar, parity);
+    return;
+  }
+  uint32_t addr = smem_u32(bar), done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
   } while (!done);
 }
 // non-suspending poll: the stage relay forwards completions with minimum latency
@@ -235,7 +258,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % S;
           const unsigned long long t0 = prof ? clk() : 0;
-          mbar_wait_acq_cluster(&empty[st], ((it / S) & 1) ^ 1);
+          mbar_wait_cta(&empty[st], ((it / S) & 1) ^ 1);
           if (prof) pc[5] += clk() - t0;
           const uint32_t bar = full_lead + st * 8;
           if (leader) mbar_arrive_expect_tx(&full[st], pair_bytes);
@@ -277,7 +300,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         unsigned long long t0 = prof ? clk() : 0;
         const int ab = tcount % AB;
         const uint32_t tacc = tm + ab * C::kAccCols;
-        mbar_wait_acq_cluster(&acc_empty[ab], (tcount / AB) & 1);  // both epilogues drained and re-zeroed
+        mbar_wait_cta(&acc_empty[ab], (tcount / AB) & 1);  // both epilogues drained and re-zeroed
         if (prof) pc[1] += clk() - t0;
         tc_fence_after();
         const uint32_t idesc = __reduce_or_sync(0xffffffffu, idesc0 | ((uint32_t)(2 * pair_half(ti.n_local)) >> 3) << 17);
@@ -366,7 +389,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % S;
           unsigned long long tg0 = prof ? clk() : 0;
-          mbar_wait_acq_cluster(&empty[st], ((it / S) & 1) ^ 1);
+          mbar_wait_cta(&empty[st], ((it / S) & 1) ^ 1);
           if (prof) { const unsigned long long t1 = clk(); pc[10] += t1 - tg0; tg0 = t1; }
           const int64_t kcol0 = (int64_t)k * 128;
           const uint32_t bs = smem_u32(bsm(st)) + dst0;
@@ -414,7 +437,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       unsigned long long t0 = prof ? clk() : 0;
       const int ab = tcount % AB;
       const uint32_t tacc = tmem + ab * C::kAccCols;
-      mbar_wait_acq_cluster(&acc_full[ab], (tcount / AB) & 1);
+      mbar_wait_cta(&acc_full[ab], (tcount / AB) & 1);
       if (prof) { const unsigned long long t1 = clk(); pc[3] += t1 - t0; t0 = t1; }
       tc_fence_after();
       if (ilv) {
