@@ -221,6 +221,30 @@ SMY_API smy_status samoyeds_moe_experts(const smy_moe_config* cfg, const smy_wei
 SMY_API smy_status samoyeds_ep_combine(const float* back, int64_t hidden, const int32_t* send_offsets, int32_t world,
                                        const int32_t* send_sel, int64_t max_rows, float* out, void* stream);
 
+/* ------------------------------ expert parallelism over NVLink peer memory
+ * The token rows and the partial outputs do not travel as dispatched copies:
+ * the owner's gate/up SSMM gathers each routed token row straight from its
+ * source rank's activations (cp.async over NVLink), and the down SSMM's
+ * scatter-add reduces straight into the source rank's fp32 output (P2P
+ * red.add) -- the all-to-all dispatch/combine fused into the two GEMMs.  Only
+ * the small routing metadata (per destination: row ids + tags) is exchanged
+ * by the caller (all_to_all_v), plus two stream-ordered barriers: after every
+ * rank zeroed its output and published its x, and after the owners' adds.
+ * ep_row_ids: row_ids[i] = (rank << 24) | send_sel[i] for the send rows
+ *   i < send_offsets[world] (max_rows bounds the buffer; T < 2^24).
+ * moe_experts_peer: rows received rows; row_map dev [rows] = the senders'
+ *   row ids; keys/vals dev [rows x k] their tags; x_peers / out_peers: host
+ *   arrays [world] of device pointers valid on THIS device (peer-mapped, e.g.
+ *   torch symmetric memory) to every rank's bf16 x [T x ldx] and fp32 out
+ *   [T x ldo] (zeroed by its owner before; this call only adds).  world <= 8,
+ *   cfg->num_shared == 0.  Workspace from smy_moe_workspace_bytes(cfg, rows). */
+SMY_API smy_status samoyeds_ep_row_ids(const int32_t* send_sel, const int32_t* send_offsets, int32_t world,
+                                       int32_t rank, int64_t max_rows, int32_t* row_ids, void* stream);
+SMY_API smy_status samoyeds_moe_experts_peer(const smy_moe_config* cfg, const smy_weight* experts, int32_t world,
+                                             const void* const* x_peers, int64_t ldx, float* const* out_peers,
+                                             int64_t ldo, int64_t rows, const int32_t* row_map, const int32_t* keys,
+                                             const float* vals, void* workspace, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------ diagnostics
  * smy_moe_set_phase_events: when events != NULL (n >= 6 cudaEvent_t handles,
  * passed as void*), samoyeds_moe_layer records events[0..5] on its stream at

@@ -67,6 +67,12 @@ SIGNATURES = {
                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "samoyeds_ep_combine": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64,
                                       C.c_void_p, C.c_void_p]),
+    "samoyeds_ep_row_ids": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_void_p,
+                                      C.c_void_p]),
+    "samoyeds_moe_experts_peer": (C.c_int, [C.POINTER(smy_moe_config), C.POINTER(smy_weight), C.c_int32,
+                                            C.POINTER(C.c_void_p), C.c_int64, C.POINTER(C.c_void_p), C.c_int64,
+                                            C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
+                                            C.c_void_p]),
     "smy_moe_set_phase_events": (C.c_int, [C.c_void_p, C.c_int]),
     "smy_launch_count": (C.c_uint64, []),
     "smy_debug_prof": (C.c_int, [C.c_void_p, C.c_int]),

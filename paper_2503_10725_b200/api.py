@@ -277,6 +277,15 @@ def ep_pack(x: torch.Tensor, offsets: torch.Tensor, sel: torch.Tensor, rows: int
     return out
 
 
+def ep_row_ids(sel: torch.Tensor, offsets: torch.Tensor, rank: int, rows: int, stream=None) -> torch.Tensor:
+    """samoyeds_ep_row_ids: (rank << 24) | token id of every send row."""
+    lib = _lib.load()
+    out = torch.empty(max(rows, 1), dtype=torch.int32, device=sel.device)
+    check(lib.samoyeds_ep_row_ids(_ptr(sel), _ptr(offsets), offsets.numel() - 1, rank, rows,
+                                  _ptr(out), _stream(stream)), "samoyeds_ep_row_ids")
+    return out
+
+
 def ep_combine(back: torch.Tensor, offsets: torch.Tensor, sel: torch.Tensor, out: torch.Tensor, stream=None):
     lib = _lib.load()
     rows = back.shape[0]
@@ -314,3 +323,19 @@ class MoEExperts:
                                        _ptr(self.workspace), self.workspace.numel(), _stream(stream)),
               "samoyeds_moe_experts")
         return out
+
+    def peer(self, world: int, x_ptrs, ldx: int, out_ptrs, ldo: int, row_map: torch.Tensor, keys: torch.Tensor,
+             vals: torch.Tensor, stream=None) -> None:
+        """samoyeds_moe_experts_peer: received rows read from / reduced into the
+        ranks' peer-mapped buffers (x_ptrs / out_ptrs: device pointers valid on
+        this device, one per rank)."""
+        lib = _lib.load()
+        R = row_map.shape[0]
+        if R > self.max_rows:
+            raise ValueError("rows exceed the workspace's max_rows")
+        xp = (C.c_void_p * world)(*[C.c_void_p(p) for p in x_ptrs])
+        op = (C.c_void_p * world)(*[C.c_void_p(p) for p in out_ptrs])
+        check(lib.samoyeds_moe_experts_peer(C.byref(self._cfg), self._arr, world, xp, ldx, op, ldo, R,
+                                            _ptr(row_map) if R else None, _ptr(keys) if R else None,
+                                            _ptr(vals) if R else None, _ptr(self.workspace),
+                                            self.workspace.numel(), _stream(stream)), "samoyeds_moe_experts_peer")

@@ -390,6 +390,47 @@ smy_status samoyeds_moe_experts(const smy_moe_config* cfg, const smy_weight* exp
                   static_cast<cudaStream_t>(stream));
 }
 
+smy_status samoyeds_ep_row_ids(const int32_t* send_sel, const int32_t* send_offsets, int32_t world, int32_t rank,
+                               int64_t max_rows, int32_t* row_ids, void* stream) {
+  if (max_rows > 0 && (!send_sel || !send_offsets || !row_ids)) return SMY_E_NULL;
+  if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world || max_rows >= (1 << 24)) return SMY_E_SHAPE;
+  smy_status st;
+  if ((st = check_arch()) != SMY_OK) return st;
+  return ep_row_ids_launch(send_sel, send_offsets, world, rank, max_rows, row_ids, static_cast<cudaStream_t>(stream));
+}
+
+smy_status samoyeds_moe_experts_peer(const smy_moe_config* cfg, const smy_weight* experts, int32_t world,
+                                     const void* const* x_peers, int64_t ldx, float* const* out_peers, int64_t ldo,
+                                     int64_t rows, const int32_t* row_map, const int32_t* keys, const float* vals,
+                                     void* workspace, size_t ws_bytes, void* stream) {
+  if (!cfg || !experts || !x_peers || !out_peers || !workspace) return SMY_E_NULL;
+  if (rows > 0 && (!row_map || !keys || !vals)) return SMY_E_NULL;
+  if (world < 1 || world > kMaxPeers) return SMY_E_SHAPE;
+  for (int p = 0; p < world; ++p)
+    if (!x_peers[p] || !out_peers[p]) return SMY_E_NULL;
+  if (cfg->num_experts < 1 || cfg->top_k < 1 || cfg->top_k > 8 || cfg->num_experts > kMaxGroups ||
+      cfg->num_shared != 0)
+    return SMY_E_CONFIG;
+  if (cfg->hidden % 128 || cfg->ffn % 128 || rows < 0 || ldx < cfg->hidden || ldx % 8 || ldo < cfg->hidden ||
+      ldo % 4)
+    return SMY_E_SHAPE;
+  smy_status st;
+  if ((st = check_experts(cfg, experts, cfg->num_experts)) != SMY_OK) return st;
+  if ((st = check_arch()) != SMY_OK) return st;
+  PeerRows pr;
+  memset(&pr, 0, sizeof(pr));
+  pr.world = world;
+  pr.row_map = row_map;
+  for (int p = 0; p < world; ++p) {
+    pr.x_peers[p] = static_cast<const uint16_t*>(x_peers[p]);
+    pr.out_peers[p] = out_peers[p];
+  }
+  pr.ldx = ldx;
+  pr.ldo = ldo;
+  return moe_core(cfg, experts, nullptr, x_peers[0], nullptr, keys, vals, rows, out_peers[0], workspace, ws_bytes,
+                  static_cast<cudaStream_t>(stream), &pr);
+}
+
 smy_status samoyeds_ep_combine(const float* back, int64_t hidden, const int32_t* send_offsets, int32_t world,
                                const int32_t* send_sel, int64_t max_rows, float* out, void* stream) {
   if (max_rows > 0 && (!back || !send_offsets || !send_sel || !out)) return SMY_E_NULL;

@@ -96,6 +96,26 @@ size_t ep_plan_ws_bytes(int64_t T, int world, int k) {
   return route_ws_bytes(T, world) + 2 * (size_t)T * k * 4 + 1024;
 }
 
+// row_ids[i] = (rank << 24) | sel[i] for the send rows i < offsets[world]: the id under
+// which the destination reads this token's row from, and adds its output into, this
+// rank's peer-mapped buffers (expert parallelism over NVLink peer memory)
+__global__ void ep_row_ids_kernel(const int32_t* __restrict__ sel, const int32_t* __restrict__ offsets, int world,
+                                  int rank, int64_t max_rows, int32_t* __restrict__ row_ids) {
+  const int64_t n = min((int64_t)offsets[world], max_rows);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    row_ids[i] = (rank << 24) | sel[i];
+}
+
+smy_status ep_row_ids_launch(const int32_t* sel, const int32_t* offsets, int world, int rank, int64_t max_rows,
+                             int32_t* row_ids, cudaStream_t s) {
+  if (max_rows <= 0) return SMY_OK;
+  int blocks = (int)((max_rows + 255) / 256);
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  ep_row_ids_kernel<<<blocks, 256, 0, s>>>(sel, offsets, world, rank, max_rows, row_ids);
+  count_launch();
+  return cuda_status(cudaGetLastError());
+}
+
 smy_status ep_plan_launch(const int32_t* ids, const float* w, int64_t T, int k, int E, int world, int32_t* counts,
                           int32_t* offsets, int32_t* sel, int32_t* tag_ids, float* tag_w, void* ws, size_t ws_bytes,
                           cudaStream_t s) {

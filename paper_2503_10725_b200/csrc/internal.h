@@ -15,6 +15,7 @@ constexpr int kStageVK = 128;     // virtual logical K per pipeline stage (4 x K
 constexpr int kABytes = 16384;    // A smem image per stage
 constexpr int kEBytes = 2048;     // E TMEM image per stage
 constexpr int kMaxGroups = 128;   // experts per grouped launch
+constexpr int kMaxPeers = 8;      // ranks of one NVLink/NVSwitch node (expert parallelism)
 
 struct Geometry {
   int64_t R;        // compressed rows = rows * N / M
@@ -60,6 +61,12 @@ struct SsmmArgs {
   int streamk;             // 1: last partial wave of tiles split along K over all workers (SCATTER only)
   int workers;             // CTAs (single) / CTA pairs (pair kernel) of the launch; set by the launcher
   int m_fastest;           // tile order: m-tile fastest (B shared in L2) instead of n-tile fastest
+  // expert parallelism over peer memory (NVLink P2P): gathered row i is token
+  // row_map[i] & 0xFFFFFF of rank row_map[i] >> 24, read from x_peers[rank]; the
+  // scatter-add of row i goes to out_peers[rank] (ldo) -- no dispatched copies
+  const int32_t* row_map;
+  const uint16_t* x_peers[kMaxPeers];
+  float* out_peers[kMaxPeers];
   int debug;               // profiling switches (env SMY_DEBUG): 1 no gather copies, 2 no weight
                            // copies, 4 no MMAs, 8 no epilogue math/stores -- results are garbage;
                            // 128: per-role cycle counters into `prof` (results valid)
@@ -120,9 +127,19 @@ smy_status ep_pack_launch(const uint16_t* x, int64_t ldx, int64_t d, const int32
                           const int32_t* sel, int64_t max_rows, uint16_t* xs, cudaStream_t s);
 smy_status ep_combine_launch(const float* back, int64_t d, const int32_t* offsets, int world, const int32_t* sel,
                              int64_t max_rows, float* out, cudaStream_t s);
+// expert parallelism over peer memory: where a received row's token lives / its output goes
+struct PeerRows {
+  int world;
+  const int32_t* row_map;              // dev [rows]: (source rank << 24) | token id
+  const uint16_t* x_peers[kMaxPeers];  // source ranks' bf16 token rows (NVLink-mapped)
+  float* out_peers[kMaxPeers];         // source ranks' fp32 outputs (P2P reductions)
+  int64_t ldx, ldo;
+};
 smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const smy_weight* shared, const void* x,
                     const float* logits, const int32_t* keys, const float* vals, int64_t T, float* out,
-                    void* workspace, size_t ws_bytes, cudaStream_t s);
+                    void* workspace, size_t ws_bytes, cudaStream_t s, const PeerRows* peers = nullptr);
+smy_status ep_row_ids_launch(const int32_t* sel, const int32_t* offsets, int world, int rank, int64_t max_rows,
+                             int32_t* row_ids, cudaStream_t s);
 void record_phase(int i, cudaStream_t s);  // no-op unless bench hooks are set
 
 }  // namespace smy

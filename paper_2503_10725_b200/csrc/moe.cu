@@ -99,9 +99,16 @@ static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* 
                           const int32_t* sel_in, const int32_t* offsets, const int32_t* prefix, int max_tiles,
                           int epi, void* out, int64_t ldo, int out_bf16, const int32_t* sel_out,
                           const float* scale, int64_t k_cols, int stream_w, int k_splits, int cl,
-                          cudaStream_t s) {
+                          cudaStream_t s, const PeerRows* peers = nullptr) {
   SsmmArgs a;
   memset(&a, 0, sizeof(a));
+  if (peers != nullptr) {
+    a.row_map = peers->row_map;
+    for (int p = 0; p < peers->world; ++p) {
+      a.x_peers[p] = peers->x_peers[p];
+      a.out_peers[p] = peers->out_peers[p];
+    }
+  }
   for (int e = 0; e < groups; ++e) {
     a.img0[e] = static_cast<const uint8_t*>(w0[e]->image);
     a.img1[e] = w1 ? static_cast<const uint8_t*>(w1[e]->image) : nullptr;
@@ -141,7 +148,7 @@ static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* 
 // with weights vals[T x k] -- the expert-parallel receive side.
 smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const smy_weight* shared, const void* x,
                     const float* logits, const int32_t* keys, const float* vals, int64_t T, float* out,
-                    void* workspace, size_t ws_bytes, cudaStream_t s) {
+                    void* workspace, size_t ws_bytes, cudaStream_t s, const PeerRows* peers) {
   const int E = c->num_experts, k = c->top_k, d = c->hidden, f = c->ffn;
   // interleaved: experts[3e] is the [2f x d] gate/up weight (reading R20), experts[3e+1] unused
   const bool ilv = interleaved(c);
@@ -198,8 +205,10 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
                         mts, 2, w.prefix, s);
   if (st != SMY_OK) return st;
   record_phase(1, s);
-  cudaError_t ce = cudaMemsetAsync(out, 0, (size_t)T * d * sizeof(float), s);
-  if (ce != cudaSuccess) return cuda_status(ce);
+  if (peers == nullptr) {  // peer mode: every rank zeroed its own output before the exchange
+    cudaError_t ce = cudaMemsetAsync(out, 0, (size_t)T * d * sizeof(float), s);
+    if (ce != cudaSuccess) return cuda_status(ce);
+  }
   record_phase(2, s);
   if (T == 0) {
     for (int i = 3; i < 6; ++i) record_phase(i, s);
@@ -213,24 +222,24 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
 
   // gate/up: H = Wg x[SEL], U = Wu x[SEL], inter = bf16(silu(H) * U)
   if (ilv) {
-    st = grouped(wg, nullptr, E, ggu, f, nt_gu, 1, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiSiluMulIlv,
-                 w.inter, f, 1, nullptr, nullptr, d, tpg <= nt_gu, 1, cl_gu, s);
+    st = grouped(wg, nullptr, E, ggu, f, nt_gu, 1, xb, peers ? peers->ldx : d, T, w.sel, w.offsets, prefix_gu,
+                 max_gu, kEpiSiluMulIlv, w.inter, f, 1, nullptr, nullptr, d, tpg <= nt_gu, 1, cl_gu, s, peers);
   } else if (fused) {
-    st = grouped(wg, wu, E, ggu, f, nt_gu, 2, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiSiluMul, w.inter, f,
-                 1, nullptr, nullptr, d, tpg <= nt_gu, 1, cl_gu, s);
+    st = grouped(wg, wu, E, ggu, f, nt_gu, 2, xb, peers ? peers->ldx : d, T, w.sel, w.offsets, prefix_gu, max_gu,
+                 kEpiSiluMul, w.inter, f, 1, nullptr, nullptr, d, tpg <= nt_gu, 1, cl_gu, s, peers);
   } else {
-    st = grouped(wg, nullptr, E, ggu, f, nt_gu, 1, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiCompact,
-                 w.fallback_g, f, 0, nullptr, nullptr, d, tpg <= nt_gu, 1, 0, s);
+    st = grouped(wg, nullptr, E, ggu, f, nt_gu, 1, xb, peers ? peers->ldx : d, T, w.sel, w.offsets, prefix_gu,
+                 max_gu, kEpiCompact, w.fallback_g, f, 0, nullptr, nullptr, d, tpg <= nt_gu, 1, 0, s, peers);
     if (st == SMY_OK)
-      st = grouped(wu, nullptr, E, ggu, f, nt_gu, 1, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiCompact,
-                   w.fallback_u, f, 0, nullptr, nullptr, d, tpg <= nt_gu, 1, 0, s);
+      st = grouped(wu, nullptr, E, ggu, f, nt_gu, 1, xb, peers ? peers->ldx : d, T, w.sel, w.offsets, prefix_gu,
+                   max_gu, kEpiCompact, w.fallback_u, f, 0, nullptr, nullptr, d, tpg <= nt_gu, 1, 0, s, peers);
     if (st == SMY_OK) st = silu_mul_launch(w.fallback_g, w.fallback_u, Tk, f, w.inter, s);
   }
   if (st != SMY_OK) return st;
   record_phase(3, s);
   // down: out[sel[t]] += gw[t] * Wd inter[t]
   st = grouped(wd, nullptr, E, gdn, d, nt_dn, 1, w.inter, f, Tk, nullptr, w.offsets, prefix_dn, max_dn, kEpiScatter,
-               out, d, 0, w.sel, w.gw, f, tpg <= nt_dn, ks_dn, cl_dn, s);
+               out, peers ? peers->ldo : d, 0, w.sel, w.gw, f, tpg <= nt_dn, ks_dn, cl_dn, s, peers);
   if (st != SMY_OK) return st;
   record_phase(4, s);
 

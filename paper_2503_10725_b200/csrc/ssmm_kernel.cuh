@@ -146,26 +146,45 @@ __device__ __forceinline__ bool decode_tile(const SsmmArgs& a, int nt, int tile,
 // than a one-MUFU tanh form -- the epilogue is not MUFU-bound)
 __device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g, 1.f + __expf(-g)) * u; }
 
+// Row of gathered index rid: the local activations, or (expert parallelism over
+// peer memory) the source rank's token row through its NVLink-mapped pointer.
+__device__ __forceinline__ const uint16_t* x_row(const SsmmArgs& a, int rid) {
+  if (a.row_map != nullptr) {
+    const int m = a.row_map[rid];
+    return a.x_peers[m >> 24] + (int64_t)(m & 0xFFFFFF) * a.ldx;
+  }
+  return a.x + (int64_t)rid * a.ldx;
+}
+// fp32 destination row of a scatter-add (EP: the source rank's output, P2P reductions)
+__device__ __forceinline__ float* out_row(const SsmmArgs& a, int dst) {
+  if (a.row_map != nullptr) {
+    const int m = a.row_map[dst];
+    return a.out_peers[m >> 24] + (int64_t)(m & 0xFFFFFF) * a.ldo;
+  }
+  return static_cast<float*>(a.out) + (int64_t)dst * a.ldo;
+}
+
 // Scatter-add of one 16-token chunk for the default (1,2,V) weights: lane l holds
 // output columns (2 grp, 2 grp + 1) of 16 tokens (v0 / v1 = slot 0 / 1).  Lane pairs
 // (l even, l + 1) cover 4 adjacent columns, so each token pair (j, j + 1) costs one
 // shuffle of two values and ONE 16-byte red.add.v4 per lane -- even lanes write token
 // j, odd lanes token j + 1 -- instead of one 8-byte reduction per lane and token.
-// my_dst / my_s: destination row and routing weight of token (lane & 15); n: tokens
+// my_row / my_s: destination row and routing weight of token (lane & 15); n: tokens
 // of the chunk this lane may write (0 if its rows are invalid).
-__device__ __forceinline__ void scatter_chunk_v4(const float (&v0)[16], const float (&v1)[16], int my_dst, float my_s,
-                                                 int n, float* out, int64_t ldo, int grp, int lane) {
+__device__ __forceinline__ void scatter_chunk_v4(const float (&v0)[16], const float (&v1)[16], float* my_row,
+                                                 float my_s, int n, int grp, int lane) {
   const int odd = lane & 1;
-  float* base = out + 2 * (grp - odd);
+  const int col = 2 * (grp - odd);
 #pragma unroll
   for (int j = 0; j < 16; j += 2) {
     const int mine = j + odd;                                  // the token this lane writes
-    const int dst = __shfl_sync(0xffffffffu, my_dst, mine);
+    float* row = reinterpret_cast<float*>(
+        __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), mine));
     const float s = __shfl_sync(0xffffffffu, my_s, mine);
     const float r0 = __shfl_xor_sync(0xffffffffu, odd ? v0[j] : v0[j + 1], 1);
     const float r1 = __shfl_xor_sync(0xffffffffu, odd ? v1[j] : v1[j + 1], 1);
     if (mine < n) {
-      float* o = base + (int64_t)dst * ldo;
+      float* o = row + col;
       if (odd) red_add_v4(o, s * r0, s * r1, s * v0[j + 1], s * v1[j + 1]);
       else red_add_v4(o, s * v0[j], s * v1[j], s * r0, s * r1);
     }
@@ -385,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
         for (int i = 0; i < NI; ++i) {
           const int t = r0 + 8 * i;
           const int rid = t < ti.n_local ? a.sel_in[ti.row0 + ti.t0 + t] : -1;
-          src[i] = a.x + (rid >= 0 ? (int64_t)rid * a.ldx : 0) + ch * 8;
+          src[i] = (rid >= 0 ? x_row(a, rid) : a.x) + ch * 8;
           valid |= (rid >= 0 ? 1u : 0u) << i;
         }
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
@@ -428,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
             const int row = idx / CPR, ch = idx % CPR;
             const int atom = ch >> 3, c8 = ch & 7;
             const int rid = rows[row];
-            const uint16_t* src = rid >= 0 ? a.x + (int64_t)rid * a.ldx + kcol0 + ch * 8 : a.x;
+            const uint16_t* src = rid >= 0 ? x_row(a, rid) + kcol0 + ch * 8 : a.x;
             uint8_t* dst = bs + atom * (NT * 128) + (row >> 3) * 1024 + (row & 7) * 128 + ((c8 ^ (row & 7)) << 4);
             cp_async16(dst, src, rid >= 0 ? 16u : 0u);
           }
@@ -501,19 +520,19 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
           // destination rows / gate weights of these 16 tokens: one load per lane,
           // broadcast by shuffle (all lanes take part, so no early exit above)
           const int rl = ti.row0 + ti.t0 + c0 + (lane & 15);
-          const int my_dst = (lane & 15) < jmax ? (a.sel_out ? a.sel_out[rl] : rl) : 0;
+          float* my_row = (lane & 15) < jmax ? out_row(a, a.sel_out ? a.sel_out[rl] : rl) : nullptr;
           const float my_s = (lane & 15) < jmax ? (a.scale ? a.scale[rl] : 1.f) : 0.f;
           const int nv = (valid && !(a.debug & 8)) ? jmax : 0;
           if (MS == 2 && nf == 1) {  // the default (1,2,V): 16 independent predicated reductions
-            scatter_chunk_v4(v[0][0], v[0][1 % MS], my_dst, my_s, nv, static_cast<float*>(a.out), a.ldo, grp, lane);
+            scatter_chunk_v4(v[0][0], v[0][1 % MS], my_row, my_s, nv, grp, lane);
             continue;
           }
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            const int dst = __shfl_sync(0xffffffffu, my_dst, j);
+            float* o = reinterpret_cast<float*>(
+                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), j));
             const float s = __shfl_sync(0xffffffffu, my_s, j);
             if (j >= nv) continue;
-            float* o = static_cast<float*>(a.out) + (int64_t)dst * a.ldo;
             if (MS == 1) {
               atomicAdd(o + cr, s * v[0][0][j]);
             } else if (MS == 2 && nf == 1) {

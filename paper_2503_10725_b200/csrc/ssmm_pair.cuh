@@ -383,7 +383,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           const int tl = r0 + 8 * i;  // row within this CTA's half
           const int t = (int)cta * hh + tl;
           const int rid = (tl < hh && t < ti.n_local) ? a.sel_in[ti.row0 + ti.t0 + t] : -1;
-          src[i] = a.x + (rid >= 0 ? (int64_t)rid * a.ldx : 0) + ch * 8;
+          src[i] = (rid >= 0 ? x_row(a, rid) : a.x) + ch * 8;
           valid |= (rid >= 0 ? 1u : 0u) << i;
         }
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
@@ -471,17 +471,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           // destination rows / gate weights of these 16 tokens: one load per lane,
           // broadcast by shuffle; then 16 independent predicated reductions
           const int rl = ti.row0 + ti.t0 + c0 + (lane & 15);
-          const int my_dst = (lane & 15) < jmax ? (a.sel_out ? a.sel_out[rl] : rl) : 0;
+          float* my_row = (lane & 15) < jmax ? out_row(a, a.sel_out ? a.sel_out[rl] : rl) : nullptr;
           const float my_s = (lane & 15) < jmax ? (a.scale ? a.scale[rl] : 1.f) : 0.f;
           if constexpr (MS == 2) {
-            scatter_chunk_v4(v[0][0], v[0][1], my_dst, my_s, n, static_cast<float*>(a.out), a.ldo, grp, lane);
+            scatter_chunk_v4(v[0][0], v[0][1], my_row, my_s, n, grp, lane);
           } else {  // N == M: lane = output row
-            float* ob = static_cast<float*>(a.out) + cr;
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              const int dst = __shfl_sync(0xffffffffu, my_dst, j);
+              float* o = reinterpret_cast<float*>(
+                  __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), j));
               const float sc = __shfl_sync(0xffffffffu, my_s, j);
-              if (j < n) atomicAdd(ob + (int64_t)dst * a.ldo, sc * v[0][0][j]);
+              if (j < n) atomicAdd(o + cr, sc * v[0][0][j]);
             }
           }
           continue;

@@ -136,3 +136,78 @@ def test_ep_world1_nccl(smy):
         assert OS.rel_fro(got - ref, ref) <= 1e-3
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------ EP over NVLink peer memory
+
+def _build(smy, E, d, f):
+    fmt = F.SparseFormat(1, 2, 32)
+    encs, sws = [], []
+    for e in range(E):
+        te, ts = [], []
+        for i in range(3):
+            r, c = (f, d) if i < 2 else (d, f)
+            wb = synth.weight_bf16(synth.weight_seed(e, i), r, c)
+            te.append(F.encode(F.prune(wb, fmt), fmt))
+            ts.append(smy.compress(dev16(wb), smy.Format(1, 2, 32))[0])
+        encs.append(tuple(te))
+        sws.append(tuple(ts))
+    return encs, sws
+
+
+@pytest.mark.parametrize("world,E,k,gating,T", [(2, 8, 2, "renorm_topk", 100), (4, 8, 2, "renorm_topk", 300),
+                                               (4, 16, 6, "softmax_all", 100), (8, 16, 2, "renorm_topk", 64)])
+def test_peer_ep_layer_matches_oracle(smy, world, E, k, gating, T):
+    """Peer-memory EP (gate/up gathers token rows from the source rank's x, down
+    reduces into the source rank's output) for world ranks simulated on one GPU:
+    each rank's 'peer' buffers are separate device allocations, so every row
+    really goes through the row map / pointer table.  T=300 takes the CTA-pair
+    kernels on the owners."""
+    from paper_2503_10725_b200.ep import LocalPeers, PeerEPMoELayer
+    d, f = 256, 384
+    encs, sws = _build(smy, E, d, f)
+    cfg = smy.MoEConfig(E, k, d, f, 0, gating, smy.Format(1, 2, 32))
+    el = E // world
+    peers = LocalPeers(world, T, d, torch.device("cuda"))
+    layers = [PeerEPMoELayer(cfg, sws[r * el:(r + 1) * el], r, world, T, peers.view(r)) for r in range(world)]
+    xs_np = [synth.activations_bf16(synth.SEED_X + 100 * r, T, d) for r in range(world)]
+    lg_np = [synth.router_logits(synth.SEED_LOGITS + 100 * r, T, E, skew=0.5) for r in range(world)]
+    st = [layers[r].dispatch(dev16(xs_np[r]), torch.from_numpy(lg_np[r]).cuda()) for r in range(world)]
+    off = [np.concatenate([[0], np.cumsum(s["send_counts"])]) for s in st]
+    for dd in range(world):                                   # in-process all_to_all_v of the tags
+        layers[dd].compute(torch.cat([st[s]["tags"][off[s][dd]:off[s][dd + 1]] for s in range(world)]))
+    torch.cuda.synchronize()
+    mode = moe.SOFTMAX_ALL if gating == "softmax_all" else moe.RENORM_TOPK
+    single = smy.MoELayer(cfg, sws, max_tokens=T)
+    for r in range(world):
+        ref, S = moe.moe_layer(encs, xs_np[r], lg_np[r], k, mode)
+        got = peers.outs[r][:T].cpu().numpy().astype(np.float64)
+        assert OS.rel_fro(got - ref, ref) <= 1e-3
+        assert (np.abs(got - ref) <= 1e-2 * S + 1e-30).all()
+        one = single(dev16(xs_np[r]), torch.from_numpy(lg_np[r]).cuda()).cpu().numpy()
+        assert np.allclose(got, one, rtol=1e-4, atol=1e-5)      # == 1-GPU layer up to fp32 order
+
+
+def test_peer_ep_world1_symmetric_memory(smy):
+    """PeerEPMoELayer with torch symmetric memory (the NVLink peer mappings and
+    device barrier of a real multi-GPU run) over a one-rank NCCL group."""
+    import os
+    import torch.distributed as dist
+    from paper_2503_10725_b200.ep import PeerEPMoELayer, SymmetricPeers
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29534")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        E, k, d, f, T = 4, 2, 128, 256, 64
+        encs, sws = _build(smy, E, d, f)
+        peers = SymmetricPeers(dist.group.WORLD, T, d, torch.device("cuda"))
+        layer = PeerEPMoELayer(smy.MoEConfig(E, k, d, f), sws, 0, 1, T, peers)
+        x = synth.activations_bf16(synth.SEED_X, T, d)
+        lg = synth.router_logits(synth.SEED_LOGITS, T, E)
+        got = layer(dev16(x), torch.from_numpy(lg).cuda()).cpu().numpy().astype(np.float64)
+        ref, S = moe.moe_layer(encs, x, lg, k)
+        assert OS.rel_fro(got - ref, ref) <= 1e-3
+        assert (np.abs(got - ref) <= 1e-2 * S + 1e-30).all()
+    finally:
+        dist.destroy_process_group()
