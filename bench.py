@@ -242,25 +242,41 @@ def run_ours(args):
     if world > 1 or args.force_ep:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29541")
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=device)
+        with stdout_to_stderr():     # NCCL's version banner goes to fd 1: keep stdout to the JSON line
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=device)
+            dist.barrier()
     lib = P.load()
     model = args.model
     d, f, E, k, gating = MODELS[model]
     T = args.tokens
     ep = (world > 1 or args.force_ep) and args.parallel == "ep"
     cfg = P.MoEConfig(E, k, d, f, 0, gating, P.Format(*FMT))
+    transport = None
+    x = torch.empty(T, d, dtype=torch.int16, device=device)
     if ep:
-        from paper_2503_10725_b200.ep import EPMoELayer, TorchExchange
+        from paper_2503_10725_b200.ep import EPMoELayer, PeerEPMoELayer, SymmetricPeers, TorchExchange
         if E % world:
             raise SystemExit(f"--parallel ep needs world | num_experts ({E})")
         el = E // world
         experts = build_layer(P, model, device, experts=range(rank * el, (rank + 1) * el))
-        layer = EPMoELayer(cfg, experts, rank, world, max_tokens=T, device=device, exchange=TorchExchange())
+        peers = None
+        if args.ep_transport == "peer":
+            try:      # token rows / outputs over NVLink peer memory inside the SSMM kernels
+                with stdout_to_stderr():
+                    peers = SymmetricPeers(dist.group.WORLD, T, d, device)
+            except Exception as exc:  # no symmetric memory on this box: the NCCL all_to_all_v transport
+                print(f"symmetric memory unavailable ({exc}); using the NCCL transport", file=sys.stderr)
+        if peers is not None:
+            transport = "peer"
+            layer = PeerEPMoELayer(cfg, experts, rank, world, T, peers, device=device, exchange=TorchExchange())
+            x = peers.x[:T]               # inputs live in the symmetric buffer (no publish copy)
+        else:
+            transport = "nccl"
+            layer = EPMoELayer(cfg, experts, rank, world, max_tokens=T, device=device, exchange=TorchExchange())
     else:
         experts = build_layer(P, model, device)
         layer = P.MoELayer(cfg, experts, max_tokens=T, device=device)
 
-    x = torch.empty(T, d, dtype=torch.int16, device=device)
     P.synth_fill(x, synth.SEED_X + 100 * rank, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
     lg = torch.empty(T, E, dtype=torch.float32, device=device)
     P.synth_fill(lg, synth.SEED_LOGITS + 100 * rank, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
@@ -439,7 +455,9 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": WORKLOAD[model], "tokens_per_gpu": T, "global_tokens": T * world, "hidden": d,
                    "ffn": f, "experts": E, "top_k": k, "gating": gating, "format": "(N,M,V)=(1,2,32) + 2:4",
-                   "parallelism": (f"ep{world} (experts sharded, NCCL all_to_all_v dispatch/combine)" if ep
+                   "parallelism": ((f"ep{world} (experts sharded; token rows / outputs over NVLink peer memory "
+                                    "inside the SSMM kernels, tags over NCCL)" if transport == "peer" else
+                                    f"ep{world} (experts sharded, NCCL all_to_all_v dispatch/combine)") if ep
                                    else f"dp{world} (experts replicated per GPU)"),
                    "l2": "inputs larger than L2: %.0f MB of compressed expert weights streamed per step"
                          % (3 * active * f * d * BYTES_PER_ELEM / 1e6),
@@ -497,6 +515,21 @@ def ncu_traffic(model, T, kernel):
     return None
 
 
+class stdout_to_stderr:
+    """Point file descriptor 1 at stderr (native libraries print banners there)."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+        return False
+
+
 def C_void_p_array(events):
     import ctypes as C
     arr = (C.c_void_p * len(events))(*[C.c_void_p(ev.cuda_event) for ev in events])
@@ -514,6 +547,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-ep", action="store_true", help=argparse.SUPPRESS)  # EP code path at world 1 (tests)
     ap.add_argument("--parallel", default="ep", choices=["ep", "dp"], help="N>1: expert (default) or data parallel")
+    ap.add_argument("--ep-transport", default="peer", choices=["peer", "nccl"],
+                    help="EP token/output transport: NVLink peer memory in the kernels (default) or NCCL all_to_all_v")
     ap.add_argument("--decode-tokens", type=int, default=64, help="extra decode point on the same layer (0: off)")
     args = ap.parse_args()
     if args.warmup < 3:
