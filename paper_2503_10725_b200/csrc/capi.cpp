@@ -38,7 +38,15 @@ unsigned long long* debug_prof_buffer(int ctas) {
 
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 void record_phase(int i, cudaStream_t s) {
-  if (g_phase_on && i >= 0 && i < 6) cudaEventRecord(g_phase[i], s);
+  if (!g_phase_on || i < 0 || i >= 6) return;
+  // inside a stream capture the record must become an event-record NODE of the
+  // graph (external), so every replay timestamps it
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(g_phase[i], s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(g_phase[i], s);
 }
 
 void set_last_error(const char* msg) { g_last_error = msg ? msg : ""; }

@@ -159,12 +159,25 @@ smy_status ssmm_launch_pair(const SsmmArgs& a0, int nt, int nw, int ms, int cl, 
 }
 
 int ssmm_pick_ksplit(int64_t tiles, int k_stages) {
-  // aim for >= 4 tiles per SM while keeping >= 8 K-stages per tile
-  const int64_t want = 4 * 148;
-  if (tiles >= want || k_stages < 16) return 1;
-  int64_t ks = (want + tiles - 1) / tiles;
-  if (ks > k_stages / 8) ks = k_stages / 8;
-  return ks < 1 ? 1 : (int)ks;
+  // Split K so that tiles x splits fills whole waves of the 148 SMs: among the
+  // splits that keep >= 8 K-stages per piece and give >= 2 pieces per SM, take
+  // the one whose last wave is fullest (work / (waves x 148)), preferring fewer
+  // splits on ties (less partial-sum traffic).
+  const int64_t sms = 148;
+  if (tiles >= 4 * sms || k_stages < 16) return 1;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int ks = 1; ks <= k_stages / 8; ++ks) {
+    const int64_t n = tiles * ks;
+    if (n < 2 * sms && ks < k_stages / 8) continue;
+    const int64_t waves = (n + sms - 1) / sms;
+    const double eff = (double)n / (double)(waves * sms);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = ks;
+    }
+  }
+  return best;
 }
 
 smy_status ssmm_launch(const SsmmArgs& a0, int nt, int nw, int ms, int rep, cudaStream_t s) {
