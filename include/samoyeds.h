@@ -184,9 +184,28 @@ typedef struct {
 } smy_moe_config;
 typedef struct smy_ep_comm smy_ep_comm; /* opaque, library-owned (EP) */
 SMY_API smy_status smy_moe_workspace_bytes(const smy_moe_config* cfg, int64_t max_tokens, size_t* bytes);
+/* comm == NULL: the whole layer on this GPU.  comm != NULL (expert parallelism,
+ * SURVEY.md §8(e)): cfg->num_experts is the TOTAL E, `experts` holds this rank's
+ * E/world experts [r*E/W, (r+1)*E/W) (same layout), num_shared must be 0, and
+ * the workspace comes from smy_moe_ep_workspace_bytes.  The call routes over all
+ * E, sends each token once to every rank owning one of its experts (NCCL
+ * send/recv of rows + tags), runs this rank's experts on what it received,
+ * returns the fp32 partial rows and sums them into out.  It reads the [W]
+ * receive counts on the host once (one stream synchronisation). */
 SMY_API smy_status samoyeds_moe_layer(const smy_moe_config* cfg, const smy_weight* experts, const smy_weight* shared,
                               const void* x_bf16, const float* logits, int64_t T, float* out, void* workspace,
                               size_t ws_bytes, smy_ep_comm* comm, void* stream);
+
+/* The library-owned NCCL communicator of expert parallelism (libnccl.so.2 is
+ * loaded on first use; SMY_E_NCCL if it cannot be).  smy_ep_unique_id writes a
+ * 128-byte NCCL unique id on one rank; the caller broadcasts it (e.g. over its
+ * torch process group) and every rank calls smy_ep_comm_create(id, rank, world)
+ * with the current CUDA device set (blocks until all ranks joined). */
+SMY_API smy_status smy_ep_unique_id(void* id128 /* host, 128 B */);
+SMY_API smy_status smy_ep_comm_create(const void* id128, int32_t rank, int32_t world, smy_ep_comm** comm);
+SMY_API smy_status smy_ep_comm_destroy(smy_ep_comm* comm);
+SMY_API smy_status smy_moe_ep_workspace_bytes(const smy_moe_config* cfg, int64_t max_tokens, int32_t world,
+                                              size_t* bytes);
 
 /* ------------------------------------------------ expert parallelism (EP)
  * The layer shards over experts: rank r of P owns experts [r*E/P,(r+1)*E/P)

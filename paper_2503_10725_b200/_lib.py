@@ -73,6 +73,11 @@ SIGNATURES = {
                                             C.POINTER(C.c_void_p), C.c_int64, C.POINTER(C.c_void_p), C.c_int64,
                                             C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
                                             C.c_void_p]),
+    "smy_ep_unique_id": (C.c_int, [C.c_void_p]),
+    "smy_ep_comm_create": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "smy_ep_comm_destroy": (C.c_int, [C.c_void_p]),
+    "smy_moe_ep_workspace_bytes": (C.c_int, [C.POINTER(smy_moe_config), C.c_int64, C.c_int32,
+                                             C.POINTER(C.c_size_t)]),
     "smy_moe_set_phase_events": (C.c_int, [C.c_void_p, C.c_int]),
     "smy_launch_count": (C.c_uint64, []),
     "smy_debug_prof": (C.c_int, [C.c_void_p, C.c_int]),

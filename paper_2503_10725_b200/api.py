@@ -207,11 +207,40 @@ def prepare_experts(cfg: MoEConfig, triples, stream=None):
             for i, (g, u, d) in enumerate(triples)]
 
 
-class MoELayer:
-    """samoyeds_moe_layer with a persistent workspace (graph-capturable)."""
+class EPComm:
+    """smy_ep_comm: the library-owned NCCL communicator of expert parallelism.
+    Rank 0 draws the NCCL unique id (smy_ep_unique_id); it is broadcast over the
+    torch process group `group`, then every rank joins (smy_ep_comm_create)."""
 
-    def __init__(self, cfg: MoEConfig, experts, shared=(), max_tokens: int = 4096, device=None):
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        lib = _lib.load()
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        uid = (C.c_char * 128)()
+        if self.rank == 0:
+            check(lib.smy_ep_unique_id(uid), "smy_ep_unique_id")
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        uid = (C.c_char * 128).from_buffer_copy(box[0])
+        self.handle = C.c_void_p()
+        check(lib.smy_ep_comm_create(uid, self.rank, self.world, C.byref(self.handle)), "smy_ep_comm_create")
+
+    def close(self):
+        if self.handle:
+            _lib.load().smy_ep_comm_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+
+class MoELayer:
+    """samoyeds_moe_layer with a persistent workspace (graph-capturable).
+
+    comm (EPComm): expert parallelism through the C library's NCCL transport --
+    `experts` are then this rank's num_experts / world experts."""
+
+    def __init__(self, cfg: MoEConfig, experts, shared=(), max_tokens: int = 4096, device=None,
+                 comm: Optional["EPComm"] = None):
         self.cfg = cfg
+        self.comm = comm
         self.experts = experts = prepare_experts(cfg, experts)
         self.shared = shared = prepare_experts(cfg, shared) if shared else shared
         self._arr = _weight_array(experts)
@@ -219,7 +248,12 @@ class MoELayer:
         self._cfg = cfg.c()
         lib = _lib.load()
         b = C.c_size_t()
-        check(lib.smy_moe_workspace_bytes(C.byref(self._cfg), max_tokens, C.byref(b)), "smy_moe_workspace_bytes")
+        if comm is not None:
+            check(lib.smy_moe_ep_workspace_bytes(C.byref(self._cfg), max_tokens, comm.world, C.byref(b)),
+                  "smy_moe_ep_workspace_bytes")
+        else:
+            check(lib.smy_moe_workspace_bytes(C.byref(self._cfg), max_tokens, C.byref(b)),
+                  "smy_moe_workspace_bytes")
         self.max_tokens = max_tokens
         self.workspace = torch.empty(b.value, dtype=torch.uint8, device=device or torch.device("cuda"))
 
@@ -232,7 +266,8 @@ class MoELayer:
             out = torch.empty(T, self.cfg.hidden, dtype=torch.float32, device=x.device)
         xb = x.view(torch.int16) if x.dtype == torch.bfloat16 else x
         check(lib.samoyeds_moe_layer(C.byref(self._cfg), self._arr, self._sarr, _ptr(xb), _ptr(logits), T,
-                                     _ptr(out), _ptr(self.workspace), self.workspace.numel(), None,
+                                     _ptr(out), _ptr(self.workspace), self.workspace.numel(),
+                                     self.comm.handle if self.comm is not None else None,
                                      _stream(stream)), "samoyeds_moe_layer")
         return out
 

@@ -342,11 +342,17 @@ smy_status samoyeds_moe_layer(const smy_moe_config* cfg, const smy_weight* exper
       cfg->num_experts > kMaxGroups || cfg->num_shared < 0 || (cfg->num_shared > 0 && !shared))
     return SMY_E_CONFIG;
   if (cfg->hidden % 128 || cfg->ffn % 128) return SMY_E_SHAPE;
-  if (comm != nullptr) {
-    set_last_error("expert-parallel communicator: use the Python EP driver (parallel.ep)");
-    return SMY_E_CONFIG;
-  }
   smy_status st;
+  if (comm != nullptr) {  // expert parallelism: experts = this rank's E / world (NCCL transport)
+    const int W = ep_comm_world(comm);
+    if (cfg->num_experts % W || cfg->num_shared != 0) return SMY_E_CONFIG;
+    smy_moe_config lc = *cfg;
+    lc.num_experts = cfg->num_experts / W;
+    if ((st = check_experts(&lc, experts, lc.num_experts)) != SMY_OK) return st;
+    if ((st = check_arch()) != SMY_OK) return st;
+    return ep_layer(cfg, experts, x_bf16, logits, T, out, workspace, ws_bytes, comm,
+                    static_cast<cudaStream_t>(stream));
+  }
   if ((st = check_experts(cfg, experts, cfg->num_experts)) != SMY_OK) return st;
   if (cfg->num_shared > 0 && (st = check_experts(cfg, shared, cfg->num_shared)) != SMY_OK) return st;
   if ((st = check_arch()) != SMY_OK) return st;
@@ -396,6 +402,25 @@ smy_status samoyeds_moe_experts(const smy_moe_config* cfg, const smy_weight* exp
   if ((st = check_arch()) != SMY_OK) return st;
   return moe_core(cfg, experts, nullptr, x_bf16, nullptr, keys, vals, rows, out, workspace, ws_bytes,
                   static_cast<cudaStream_t>(stream));
+}
+
+smy_status smy_ep_unique_id(void* id128) {
+  if (!id128) return SMY_E_NULL;
+  return ep_unique_id(id128);
+}
+
+smy_status smy_ep_comm_create(const void* id128, int32_t rank, int32_t world, smy_ep_comm** comm) {
+  if (!id128 || !comm) return SMY_E_NULL;
+  if (world < 1 || world > 256 || rank < 0 || rank >= world) return SMY_E_SHAPE;
+  return ep_comm_create(id128, rank, world, comm);
+}
+
+smy_status smy_ep_comm_destroy(smy_ep_comm* comm) { return ep_comm_destroy(comm); }
+
+smy_status smy_moe_ep_workspace_bytes(const smy_moe_config* cfg, int64_t max_tokens, int32_t world, size_t* bytes) {
+  if (!cfg || !bytes) return SMY_E_NULL;
+  if (max_tokens < 0 || world < 1 || cfg->num_experts % world) return SMY_E_SHAPE;
+  return ep_workspace_bytes(cfg, max_tokens, world, bytes);
 }
 
 smy_status samoyeds_ep_row_ids(const int32_t* send_sel, const int32_t* send_offsets, int32_t world, int32_t rank,

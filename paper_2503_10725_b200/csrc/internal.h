@@ -138,6 +138,14 @@ struct PeerRows {
 smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const smy_weight* shared, const void* x,
                     const float* logits, const int32_t* keys, const float* vals, int64_t T, float* out,
                     void* workspace, size_t ws_bytes, cudaStream_t s, const PeerRows* peers = nullptr);
+smy_status moe_workspace_bytes(const smy_moe_config* c, int64_t T, size_t* bytes);
+smy_status ep_unique_id(void* out128);
+smy_status ep_comm_create(const void* id128, int rank, int world, smy_ep_comm** out);
+smy_status ep_comm_destroy(smy_ep_comm* c);
+int ep_comm_world(const smy_ep_comm* c);
+smy_status ep_workspace_bytes(const smy_moe_config* c, int64_t T, int world, size_t* bytes);
+smy_status ep_layer(const smy_moe_config* c, const smy_weight* experts, const void* x, const float* logits, int64_t T,
+                    float* out, void* workspace, size_t ws_bytes, smy_ep_comm* comm, cudaStream_t s);
 smy_status ep_row_ids_launch(const int32_t* sel, const int32_t* offsets, int world, int rank, int64_t max_rows,
                              int32_t* row_ids, cudaStream_t s);
 void record_phase(int i, cudaStream_t s);  // no-op unless bench hooks are set

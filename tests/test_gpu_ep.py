@@ -211,3 +211,30 @@ def test_peer_ep_world1_symmetric_memory(smy):
         assert (np.abs(got - ref) <= 1e-2 * S + 1e-30).all()
     finally:
         dist.destroy_process_group()
+
+
+def test_ep_c_abi_nccl_world1(smy):
+    """samoyeds_moe_layer with a library-owned NCCL communicator (smy_ep_comm,
+    the C ABI's EP path) over a one-rank group vs the oracle."""
+    import os
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29535")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    comm = None
+    try:
+        E, k, d, f, T = 8, 2, 256, 384, 200
+        encs, sws = _build(smy, E, d, f)
+        comm = smy.EPComm()
+        layer = smy.MoELayer(smy.MoEConfig(E, k, d, f), sws, max_tokens=T, comm=comm)
+        x = synth.activations_bf16(synth.SEED_X, T, d)
+        lg = synth.router_logits(synth.SEED_LOGITS, T, E, skew=0.5)
+        got = layer(dev16(x), torch.from_numpy(lg).cuda()).cpu().numpy().astype(np.float64)
+        ref, S = moe.moe_layer(encs, x, lg, k)
+        assert OS.rel_fro(got - ref, ref) <= 1e-3
+        assert (np.abs(got - ref) <= 1e-2 * S + 1e-30).all()
+    finally:
+        if comm is not None:
+            comm.close()
+        dist.destroy_process_group()
