@@ -65,6 +65,11 @@ struct SsmmArgs {
   // row_map[i] & 0xFFFFFF of rank row_map[i] >> 24, read from x_peers[rank]; the
   // scatter-add of row i goes to out_peers[rank] (ldo) -- no dispatched copies
   const int32_t* row_map;
+  // zero this fp32 buffer (zero_elems, multiple of 4) on the way: the layer's output,
+  // cleared by the gate/up launch's epilogue warps before their first tile instead
+  // of a separate memset launch (the down launch that adds into it runs after)
+  float* zero_ptr;
+  int64_t zero_elems;
   const uint16_t* x_peers[kMaxPeers];
   float* out_peers[kMaxPeers];
   int debug;               // profiling switches (env SMY_DEBUG): 1 no gather copies, 2 no weight

@@ -99,9 +99,12 @@ static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* 
                           const int32_t* sel_in, const int32_t* offsets, const int32_t* prefix, int max_tiles,
                           int epi, void* out, int64_t ldo, int out_bf16, const int32_t* sel_out,
                           const float* scale, int64_t k_cols, int stream_w, int k_splits, int cl,
-                          cudaStream_t s, const PeerRows* peers = nullptr) {
+                          cudaStream_t s, const PeerRows* peers = nullptr, float* zero_ptr = nullptr,
+                          int64_t zero_elems = 0) {
   SsmmArgs a;
   memset(&a, 0, sizeof(a));
+  a.zero_ptr = zero_ptr;
+  a.zero_elems = zero_elems;
   if (peers != nullptr) {
     a.row_map = peers->row_map;
     for (int p = 0; p < peers->world; ++p) {
@@ -205,10 +208,9 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
                         mts, 2, w.prefix, s);
   if (st != SMY_OK) return st;
   record_phase(1, s);
-  if (peers == nullptr) {  // peer mode: every rank zeroed its own output before the exchange
-    cudaError_t ce = cudaMemsetAsync(out, 0, (size_t)T * d * sizeof(float), s);
-    if (ce != cudaSuccess) return cuda_status(ce);
-  }
+  // the output is zeroed by the gate/up launch (SsmmArgs::zero_ptr); in peer mode every
+  // rank zeroed its own output before the exchange
+  float* zero_out = peers == nullptr && T > 0 ? out : nullptr;
   record_phase(2, s);
   if (T == 0) {
     for (int i = 3; i < 6; ++i) record_phase(i, s);
@@ -223,13 +225,15 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   // gate/up: H = Wg x[SEL], U = Wu x[SEL], inter = bf16(silu(H) * U)
   if (ilv) {
     st = grouped(wg, nullptr, E, ggu, f, nt_gu, 1, xb, peers ? peers->ldx : d, T, w.sel, w.offsets, prefix_gu,
-                 max_gu, kEpiSiluMulIlv, w.inter, f, 1, nullptr, nullptr, d, tpg <= nt_gu, 1, cl_gu, s, peers);
+                 max_gu, kEpiSiluMulIlv, w.inter, f, 1, nullptr, nullptr, d, tpg <= nt_gu, 1, cl_gu, s, peers,
+                 zero_out, T * d);
   } else if (fused) {
     st = grouped(wg, wu, E, ggu, f, nt_gu, 2, xb, peers ? peers->ldx : d, T, w.sel, w.offsets, prefix_gu, max_gu,
-                 kEpiSiluMul, w.inter, f, 1, nullptr, nullptr, d, tpg <= nt_gu, 1, cl_gu, s, peers);
+                 kEpiSiluMul, w.inter, f, 1, nullptr, nullptr, d, tpg <= nt_gu, 1, cl_gu, s, peers, zero_out, T * d);
   } else {
     st = grouped(wg, nullptr, E, ggu, f, nt_gu, 1, xb, peers ? peers->ldx : d, T, w.sel, w.offsets, prefix_gu,
-                 max_gu, kEpiCompact, w.fallback_g, f, 0, nullptr, nullptr, d, tpg <= nt_gu, 1, 0, s, peers);
+                 max_gu, kEpiCompact, w.fallback_g, f, 0, nullptr, nullptr, d, tpg <= nt_gu, 1, 0, s, peers, zero_out,
+                 T * d);
     if (st == SMY_OK)
       st = grouped(wu, nullptr, E, ggu, f, nt_gu, 1, xb, peers ? peers->ldx : d, T, w.sel, w.offsets, prefix_gu,
                    max_gu, kEpiCompact, w.fallback_u, f, 0, nullptr, nullptr, d, tpg <= nt_gu, 1, 0, s, peers);

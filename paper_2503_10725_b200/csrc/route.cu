@@ -267,7 +267,7 @@ smy_status route_launch(const float* logits, int64_t T, int E, int k, int gating
   if (T <= kRouteThreads) {  // one block for the compaction (decode sizes)
     // up to 4 tokens per warp: top-k inside the same launch; more: a grid-wide
     // top-k launch first (one warp per token) so the block only compacts
-    const bool fused_topk = T <= 4 * kRouteWarps;
+    const bool fused_topk = T <= 4 * kRouteWarps;  // (16 per warp measured slower than two launches)
     if (logits != nullptr && !fused_topk) {
       route_topk_kernel<<<(unsigned)((T + kRouteWarps - 1) / kRouteWarps), kRouteThreads, 0, s>>>(logits, T, E, k,
                                                                                                  gating, ids, w);

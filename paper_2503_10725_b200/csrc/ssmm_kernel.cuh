@@ -146,6 +146,13 @@ __device__ __forceinline__ bool decode_tile(const SsmmArgs& a, int nt, int tile,
 // than a one-MUFU tanh form -- the epilogue is not MUFU-bound)
 __device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g, 1.f + __expf(-g)) * u; }
 
+// grid-stride zeroing of a.zero_ptr by `nthreads` threads (16-byte stores)
+__device__ __forceinline__ void zero_slice(const SsmmArgs& a, int64_t tid, int64_t nthreads) {
+  float4* z = reinterpret_cast<float4*>(a.zero_ptr);
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t i = tid; i < a.zero_elems / 4; i += nthreads) z[i] = zero;
+}
+
 // Row of gathered index rid: the local activations, or (expert parallelism over
 // peer memory) the source rank's token row through its NVLink-mapped pointer.
 __device__ __forceinline__ const uint16_t* x_row(const SsmmArgs& a, int rid) {
@@ -460,6 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
     }
   } else {
     // ============ epilogue (warps 0-3): TMEM -> fused epilogue -> re-zero ============
+    if (a.zero_ptr != nullptr) zero_slice(a, (int64_t)blockIdx.x * 128 + threadIdx.x, (int64_t)gridDim.x * 128);
     const int q = warp;  // TMEM lane quarter
     const uint32_t lane_base = (uint32_t)(32 * q) << 16;
     const int nf = a.n_fmt;

@@ -413,6 +413,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     // epilogue's dependent-latency chains.
     const int q = warp & 3;
     const int h = warp >= 10 ? 1 : 0;
+    if (a.zero_ptr != nullptr)
+      zero_slice(a, (int64_t)blockIdx.x * 256 + (q + 4 * h) * 32 + lane, (int64_t)gridDim.x * 256);
     const uint32_t lane_base = (uint32_t)(32 * q) << 16;
     const uint32_t acc_empty_leader = mapa_shared(smem_u32(acc_empty), 0);
     auto zero_acc = [&](int b) {
