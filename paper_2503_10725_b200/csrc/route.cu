@@ -90,6 +90,54 @@ __device__ __forceinline__ void build_masks(const int32_t* __restrict__ ids, int
   __syncthreads();
 }
 
+// Warp 0: exclusive scans over experts e < E of the counts c[e] and of the two
+// SSMM launches' tile counts mt * ceil(c / nt) (lane l owns experts l*8 .. l*8+7,
+// so the order is kept); writes off[e] (smem) and prefix0/1 (global, nullable).
+__device__ __forceinline__ void scan_experts(const int32_t* __restrict__ cnt, int E, int lane, int32_t* __restrict__ off,
+                                             int nt0, int mt0, int32_t* __restrict__ prefix0, int nt1, int mt1,
+                                             int32_t* __restrict__ prefix1) {
+  constexpr int PER = kMaxE / 32;
+  int c[PER];
+  int s0 = 0, s1 = 0, s2 = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int e = lane * PER + j;
+    c[j] = e < E ? cnt[e] : 0;
+    s0 += c[j];
+    s1 += prefix0 ? mt0 * ((c[j] + nt0 - 1) / nt0) : 0;
+    s2 += prefix1 ? mt1 * ((c[j] + nt1 - 1) / nt1) : 0;
+  }
+  int i0 = s0, i1 = s1, i2 = s2;  // inclusive warp scans
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y0 = __shfl_up_sync(0xffffffffu, i0, o), y1 = __shfl_up_sync(0xffffffffu, i1, o),
+              y2 = __shfl_up_sync(0xffffffffu, i2, o);
+    if (lane >= o) {
+      i0 += y0;
+      i1 += y1;
+      i2 += y2;
+    }
+  }
+  int r0 = i0 - s0, r1 = i1 - s1, r2 = i2 - s2;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int e = lane * PER + j;
+    if (e < E) {
+      off[e] = r0;
+      if (prefix0) prefix0[e] = r1;
+      if (prefix1) prefix1[e] = r2;
+    }
+    r0 += c[j];
+    r1 += prefix0 ? mt0 * ((c[j] + nt0 - 1) / nt0) : 0;
+    r2 += prefix1 ? mt1 * ((c[j] + nt1 - 1) / nt1) : 0;
+  }
+  if (lane == 31) {
+    off[E] = i0;
+    if (prefix0) prefix0[E] = i1;
+    if (prefix1) prefix1[E] = i2;
+  }
+}
+
 // One warp per token over the whole grid (8 tokens per 256-thread block).
 __global__ void route_topk_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int gating,
                                   int32_t* __restrict__ ids, float* __restrict__ w) {
@@ -126,28 +174,20 @@ __global__ void route_small_kernel(const float* __restrict__ logits, int64_t T, 
   }
   __syncthreads();
   build_masks(ids, T, E, k, mask);
+  __shared__ int32_t cnt[kMaxE];
+  __shared__ int32_t off[kMaxE + 1];
   for (int e = threadIdx.x; e < E; e += kRouteThreads) {
     int c = 0;
     for (int ww = 0; ww < kRouteWarps; ++ww) c += __popc(mask[ww][e]);
-    wbase[0][e] = c;  // temporarily: the count
+    cnt[e] = c;
+    counts[e] = c;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0, p0 = 0, p1 = 0;
-    for (int e = 0; e < E; ++e) {
-      const int c = wbase[0][e];
-      counts[e] = c;
-      offsets[e] = acc;
-      if (prefix0) prefix0[e] = p0;
-      if (prefix1) prefix1[e] = p1;
-      if (prefix0) p0 += mt0 * ((c + nt0 - 1) / nt0);
-      if (prefix1) p1 += mt1 * ((c + nt1 - 1) / nt1);
-      wbase[0][e] = acc;  // now: the expert's first row
-      acc += c;
-    }
-    offsets[E] = acc;
-    if (prefix0) prefix0[E] = p0;
-    if (prefix1) prefix1[E] = p1;
+  if (wp == 0) scan_experts(cnt, E, lane, off, nt0, mt0, prefix0, nt1, mt1, prefix1);
+  __syncthreads();
+  for (int e = threadIdx.x; e <= E; e += kRouteThreads) {
+    offsets[e] = off[e];
+    if (e < E) wbase[0][e] = off[e];  // the expert's first row
   }
   __syncthreads();
   for (int e = threadIdx.x; e < E; e += kRouteThreads) {
@@ -182,21 +222,7 @@ __global__ void route_scan_kernel(const int32_t* __restrict__ blk_counts, int nb
     cnt[e] = c;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0, p0 = 0, p1 = 0;
-    for (int e = 0; e < E; ++e) {
-      off[e] = acc;
-      if (prefix0) prefix0[e] = p0;
-      if (prefix1) prefix1[e] = p1;
-      const int c = cnt[e];
-      acc += c;
-      if (prefix0) p0 += mt0 * ((c + nt0 - 1) / nt0);
-      if (prefix1) p1 += mt1 * ((c + nt1 - 1) / nt1);
-    }
-    off[E] = acc;
-    if (prefix0) prefix0[E] = p0;
-    if (prefix1) prefix1[E] = p1;
-  }
+  if (threadIdx.x < 32) scan_experts(cnt, E, threadIdx.x, off, nt0, mt0, prefix0, nt1, mt1, prefix1);
   __syncthreads();
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     counts[e] = cnt[e];
