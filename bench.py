@@ -196,7 +196,7 @@ def run_reference(args):
 
 # ------------------------------------------------------------------ GPU arm
 
-def build_layer(P, model, device, experts=None):
+def build_layer(P, model, device, experts=None, transcode="auto"):
     import numpy as np
     import torch
 
@@ -217,7 +217,7 @@ def build_layer(P, model, device, experts=None):
         experts_out.append(tuple(trip))
     # the layout the layer runs on (interleaved gate/up, one image block), then
     # drop everything the kernels do not read
-    experts_out = P.prepare_experts(P.MoEConfig(E, k, d, f, 0, gating, fmt), experts_out)
+    experts_out = P.prepare_experts(P.MoEConfig(E, k, d, f, 0, gating, fmt, "auto", transcode), experts_out)
     for trip in experts_out:
         for sw in trip:
             if sw is not None:
@@ -250,7 +250,7 @@ def run_ours(args):
     d, f, E, k, gating = MODELS[model]
     T = args.tokens
     ep = (world > 1 or args.force_ep) and args.parallel == "ep"
-    cfg = P.MoEConfig(E, k, d, f, 0, gating, P.Format(*FMT))
+    cfg = P.MoEConfig(E, k, d, f, 0, gating, P.Format(*FMT), "auto", args.transcode)
     transport = None
     x = torch.empty(T, d, dtype=torch.int16, device=device)
     if ep:
@@ -258,7 +258,7 @@ def run_ours(args):
         if E % world:
             raise SystemExit(f"--parallel ep needs world | num_experts ({E})")
         el = E // world
-        experts = build_layer(P, model, device, experts=range(rank * el, (rank + 1) * el))
+        experts = build_layer(P, model, device, experts=range(rank * el, (rank + 1) * el), transcode=args.transcode)
         peers = None
         if args.ep_transport == "peer":
             try:      # token rows / outputs over NVLink peer memory inside the SSMM kernels
@@ -274,7 +274,7 @@ def run_ours(args):
             transport = "nccl"
             layer = EPMoELayer(cfg, experts, rank, world, max_tokens=T, device=device, exchange=TorchExchange())
     else:
-        experts = build_layer(P, model, device)
+        experts = build_layer(P, model, device, transcode=args.transcode)
         layer = P.MoELayer(cfg, experts, max_tokens=T, device=device)
 
     P.synth_fill(x, synth.SEED_X + 100 * rank, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
@@ -472,7 +472,8 @@ def run_ours(args):
         "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": WORKLOAD[model], "tokens_per_gpu": T, "global_tokens": T * world, "hidden": d,
-                   "ffn": f, "experts": E, "top_k": k, "gating": gating, "format": "(N,M,V)=(1,2,32) + 2:4",
+                   "ffn": f, "experts": E, "top_k": k, "gating": gating, "format": "(N,M,V)=(%d,%d,%d) + 2:4" % FMT + (" (run as plain 2:4)" if cfg.kernel_config() is not cfg
+                                                               else ""),
                    "parallelism": ((f"ep{world} (experts sharded; token rows / outputs over NVLink peer memory "
                                     "inside the SSMM kernels, tags over NCCL)" if transport == "peer" else
                                     f"ep{world} (experts sharded, NCCL all_to_all_v dispatch/combine)") if ep
@@ -555,6 +556,15 @@ def C_void_p_array(events):
     return arr
 
 
+def set_format(spec: str):
+    """--format N,M,V: the weight format of the run (module-level FMT / byte count)."""
+    global FMT, BYTES_PER_ELEM
+    n, m, v = (int(t) for t in spec.split(","))
+    FMT = (n, m, v)
+    # canonical bytes per logical element: values (N/M)/2 x 2 B + codes (N/M)/2 x 2 bit + indices (N/M)/V x 1 B
+    BYTES_PER_ELEM = (n / m) * (0.5 * 2 + 0.5 * 0.25 + 1.0 / v)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
@@ -565,12 +575,16 @@ def main():
     ap.add_argument("--tokens", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the timed steps eagerly instead of a CUDA graph")
+    ap.add_argument("--format", default="1,2,32", help="(N,M,V) weight format (default the paper's (1,2,32))")
+    ap.add_argument("--transcode", default="auto", choices=["auto", "off"],
+                    help="formats without fast kernels: re-encode as plain 2:4 (auto) or keep (off)")
     ap.add_argument("--force-ep", action="store_true", help=argparse.SUPPRESS)  # EP code path at world 1 (tests)
     ap.add_argument("--parallel", default="ep", choices=["ep", "dp"], help="N>1: expert (default) or data parallel")
     ap.add_argument("--ep-transport", default="peer", choices=["peer", "nccl"],
                     help="EP token/output transport: NVLink peer memory in the kernels (default) or NCCL all_to_all_v")
     ap.add_argument("--decode-tokens", type=int, default=64, help="extra decode point on the same layer (0: off)")
     args = ap.parse_args()
+    set_format(args.format)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     if args.impl == "reference":

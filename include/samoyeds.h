@@ -112,12 +112,20 @@ typedef struct {
 SMY_API smy_status samoyeds_compress(const smy_wdesc* desc, const void* w_bf16, int64_t ldw, int flags,
                              smy_weight* out, int32_t* d_status, void* stream);
 
+/* samoyeds_decompress: the inverse of the encoding -- the dense
+ * pattern-conforming bf16 weight [rows x ldw] (dev) from the canonical values,
+ * codes and indices (which must be present); positions not stored are zero.
+ * compress(decompress(w)) with SMY_ASSUME_PRUNED reproduces w bit for bit.  */
+SMY_API smy_status samoyeds_decompress(const smy_weight* w, void* w_bf16, int64_t ldw, void* stream);
+
 /* samoyeds_interleave_gate_up: the interleaved gate/up weight of one expert
  * (reading R20; the paper fuses the activation with "its precedent
  * operator", without fixing how gate and up share a kernel).  The
- * logical weight is [2f x d]: rows [64b, 64b+32) are gate rows [32b, 32b+32)
- * and rows [64b+32, 64b+64) the same up rows, so each warp's 32 TMEM lanes of
- * an SSMM tile hold the gate AND up rows of the same 32 outputs (16 groups).
+ * logical weight is [2f x d] whose compressed rows alternate in blocks of 16:
+ * 16 gate compressed rows, then the 16 up compressed rows of the same outputs
+ * (= output rows [64b, 64b+32) gate rows [32b, 32b+32), the next 32 the same up
+ * rows for N/M = 1/2; blocks of 16 output rows for N = M), so each warp's 32
+ * TMEM lanes of an SSMM tile hold the gate AND up rows of the same outputs.
  * Pruning/encoding act on M-row groups, so this equals samoyeds_compress of
  * the interleaved dense weight bit for bit; it is built by moving whole
  * compressed rows of gate/up's canonical arrays (which must be present) and

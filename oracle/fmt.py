@@ -281,7 +281,14 @@ def canonical_bytes(rows: int, cols: int, fmt: SparseFormat, elem_bytes: int = 2
 
 # ------------------------------------------- interleaved gate/up (reading R20)
 
-GU_BLOCK = 32    # output rows per interleave block
+GU_BLOCK = 32    # output rows per interleave block for N/M = 1/2 formats
+GU_CBLOCK = 16   # compressed rows per interleave block (every format, R20)
+
+
+def gu_block(fmt: "SparseFormat") -> int:
+    """Output rows per interleave block of a format: 16 compressed rows, i.e. 32
+    output rows for N/M = 1/2 and 16 for N = M (R20)."""
+    return GU_CBLOCK * fmt.m // fmt.n
 
 
 def interleave_rows(w_gate: np.ndarray, w_up: np.ndarray, block: int = GU_BLOCK) -> np.ndarray:
@@ -314,11 +321,13 @@ def deinterleave_rows(w_gu: np.ndarray, block: int = GU_BLOCK):
     return gate, up
 
 
-def interleave_gate_up(eg: Encoded, eu: Encoded, block: int = GU_BLOCK) -> Encoded:
+def interleave_gate_up(eg: Encoded, eu: Encoded, block: int = None) -> Encoded:
     """Canonical encoding of interleave_rows(gate, up) built from the two
     encodings: a block of `block` output rows is block*N/M compressed rows
     (R1), so the relabeling moves whole compressed rows of values, codes and
     indices (no re-encoding)."""
+    if block is None:
+        block = gu_block(eg.fmt)
     if eg.fmt != eu.fmt or (eg.rows, eg.cols) != (eu.rows, eu.cols) or eg.rows % block:
         raise ShapeError("gate/up encodings must match and rows % block == 0")
     cb = eg.fmt.comp_rows(block)

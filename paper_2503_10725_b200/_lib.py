@@ -44,6 +44,7 @@ SIGNATURES = {
     "smy_weight_layout": (C.c_int, [C.POINTER(smy_wdesc), C.POINTER(smy_wlayout)]),
     "samoyeds_compress": (C.c_int, [C.POINTER(smy_wdesc), C.c_void_p, C.c_int64, C.c_int, C.POINTER(smy_weight),
                                     C.c_void_p, C.c_void_p]),
+    "samoyeds_decompress": (C.c_int, [C.POINTER(smy_weight), C.c_void_p, C.c_int64, C.c_void_p]),
     "samoyeds_interleave_gate_up": (C.c_int, [C.POINTER(smy_weight), C.POINTER(smy_weight), C.POINTER(smy_weight),
                                               C.c_void_p]),
     "samoyeds_ssmm": (C.c_int, [C.POINTER(smy_weight), C.POINTER(smy_weight), C.c_void_p, C.c_int64, C.c_int64,

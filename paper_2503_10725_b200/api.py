@@ -101,6 +101,27 @@ def compress(w: torch.Tensor, fmt: Format, prune: bool = True, stream=None):
     return sw, status
 
 
+def decompress(w: SparseWeight, stream=None) -> torch.Tensor:
+    """samoyeds_decompress: the dense bf16 [rows x cols] (int16 bit patterns) weight."""
+    lib = _lib.load()
+    if w.values is None:
+        raise ValueError("decompress needs the canonical arrays (drop_canonical() was called)")
+    out = torch.empty(w.rows, w.cols, dtype=torch.int16, device=w.image.device)
+    cw = w.c()
+    check(lib.samoyeds_decompress(C.byref(cw), _ptr(out), out.stride(0), _stream(stream)), "samoyeds_decompress")
+    return out
+
+
+def transcode_24(w: SparseWeight, stream=None) -> SparseWeight:
+    """The same weight re-encoded as plain 2:4, format (2,2,32) (N = M: every
+    sub-row kept, zero sub-rows stored as zeros): decompress + compress
+    (ASSUME_PRUNED).  Twice the image bytes of an N/M = 1/2 format, but it runs
+    on the fast N = M kernels -- how N>1 and V=16 formats reach speed."""
+    dense = decompress(w, stream)
+    out, _ = compress(dense, Format(2, 2, 32), prune=False, stream=stream)
+    return out
+
+
 def interleave_gate_up(gate: SparseWeight, up: SparseWeight, stream=None,
                        image: Optional[torch.Tensor] = None) -> SparseWeight:
     """samoyeds_interleave_gate_up: the [2f x d] gate/up weight whose 128-row
@@ -170,14 +191,28 @@ class MoEConfig:
     gating: str = "renorm_topk"
     fmt: Format = Format()
     # "auto": the interleaved gate/up weight (one SSMM, reading R20) whenever the
-    # format allows it -- (1,2,V), V % 32 == 0 -- else separate gate and up
+    # format allows it -- (1,2,V) or N = M, V % 32 == 0 -- else separate gate and up
     gate_up: str = "auto"
+    # "auto": formats without fast kernels (N>1 with N<M, V=16) are re-encoded as
+    # plain 2:4 (2,2,32) when a layer is built (transcode_24); "off": keep them
+    transcode: str = "auto"
+
+    def fast_format(self) -> bool:
+        f = self.fmt
+        return f.v % 32 == 0 and ((f.n == 1 and f.m == 2) or f.n == f.m)
 
     def resolved_gate_up(self) -> str:
         if self.gate_up != "auto":
             return self.gate_up
-        ok = self.fmt.n == 1 and self.fmt.m == 2 and self.fmt.v % 32 == 0 and self.ffn % 128 == 0
+        ok = self.fast_format() and self.ffn % 128 == 0
         return "interleaved" if ok else "separate"
+
+    def kernel_config(self) -> "MoEConfig":
+        """The configuration the layer's kernels run on (after transcoding)."""
+        if self.transcode == "auto" and not self.fast_format():
+            return MoEConfig(self.num_experts, self.top_k, self.hidden, self.ffn, self.num_shared, self.gating,
+                             Format(2, 2, 32), self.gate_up, "off")
+        return self
 
     def c(self) -> smy_moe_config:
         return smy_moe_config(self.num_experts, self.top_k, self.hidden, self.ffn, self.num_shared,
@@ -191,9 +226,14 @@ def _weight_array(triples: Sequence[Sequence[Optional[SparseWeight]]]):
 
 
 def prepare_experts(cfg: MoEConfig, triples, stream=None):
-    """(gate, up, down) triples -> the layout cfg.c() announces: unchanged for
+    """(gate, up, down) triples -> the layout cfg.kernel_config().c() announces:
+    transcoded to plain 2:4 if the format has no fast kernels, then unchanged for
     "separate", (gu, None, down) with gu = interleave_gate_up(gate, up) for
     "interleaved"."""
+    kc = cfg.kernel_config()
+    if kc is not cfg and triples and all(t[1] is not None for t in triples) and triples[0][0].fmt != kc.fmt:
+        triples = [tuple(transcode_24(w, stream) for w in t) for t in triples]
+    cfg = kc
     if cfg.resolved_gate_up() == "separate":
         return [tuple(t) for t in triples]
     if not triples or all(t[1] is None for t in triples):   # already (gu, None, down)
@@ -245,7 +285,7 @@ class MoELayer:
         self.shared = shared = prepare_experts(cfg, shared) if shared else shared
         self._arr = _weight_array(experts)
         self._sarr = _weight_array(shared) if shared else None
-        self._cfg = cfg.c()
+        self._cfg = cfg.kernel_config().c()
         lib = _lib.load()
         b = C.c_size_t()
         if comm is not None:
@@ -337,7 +377,7 @@ class MoEExperts:
         self.cfg = cfg
         self.experts = experts = prepare_experts(cfg, experts)
         self._arr = _weight_array(experts)
-        self._cfg = cfg.c()
+        self._cfg = cfg.kernel_config().c()
         lib = _lib.load()
         b = C.c_size_t()
         check(lib.smy_moe_workspace_bytes(C.byref(self._cfg), max_rows, C.byref(b)), "smy_moe_workspace_bytes")

@@ -119,7 +119,7 @@ static smy_status check_experts(const smy_moe_config* cfg, const smy_weight* exp
   if (cfg->gate_up != SMY_GU_SEPARATE && cfg->gate_up != SMY_GU_INTERLEAVED) return SMY_E_CONFIG;
   const bool ilv = cfg->gate_up == SMY_GU_INTERLEAVED;
   if (ilv && !ilv_format(cfg->fmt)) {
-    set_last_error("SMY_GU_INTERLEAVED needs format (1,2,V) with V % 32 == 0");
+    set_last_error("SMY_GU_INTERLEAVED needs format (1,2,V) or N == M, with V % 32 == 0");
     return SMY_E_CONFIG;
   }
   for (int e = 0; e < n; ++e)
@@ -191,6 +191,16 @@ smy_status samoyeds_compress(const smy_wdesc* desc, const void* w_bf16, int64_t 
                          static_cast<cudaStream_t>(stream));
 }
 
+smy_status samoyeds_decompress(const smy_weight* w, void* w_bf16, int64_t ldw, void* stream) {
+  if (!w || !w_bf16 || !w->values || !w->codes || !w->indices) return SMY_E_NULL;
+  Geometry g;
+  smy_status st = geometry(&w->d, &g);
+  if (st != SMY_OK) return st;
+  if (ldw < w->d.cols) return SMY_E_SHAPE;
+  if ((st = check_arch()) != SMY_OK) return st;
+  return decompress_launch(w, static_cast<uint16_t*>(w_bf16), ldw, static_cast<cudaStream_t>(stream));
+}
+
 smy_status samoyeds_interleave_gate_up(const smy_weight* gate, const smy_weight* up, smy_weight* gu, void* stream) {
   if (!gate || !up || !gu) return SMY_E_NULL;
   if (!gate->values || !gate->codes || !gate->indices || !up->values || !up->codes || !up->indices || !gu->values ||
@@ -227,7 +237,7 @@ smy_status samoyeds_ssmm(const smy_weight* w, const smy_weight* w2, const void* 
   } else if (epi == SMY_EPI_SILU_MUL_INTERLEAVED) {
     if (out_dtype != SMY_BF16) return SMY_E_CONFIG;
     if (!ilv_format(w->d.fmt)) {
-      set_last_error("SILU_MUL_INTERLEAVED needs format (1,2,V) with V % 32 == 0");
+      set_last_error("SILU_MUL_INTERLEAVED needs format (1,2,V) or N == M, with V % 32 == 0");
       return SMY_E_CONFIG;
     }
     if (w->d.rows % 64) return SMY_E_SHAPE;

@@ -160,7 +160,7 @@ __global__ void pack_kernel(const uint16_t* __restrict__ values, const uint8_t* 
 }
 
 // Interleaved gate/up (reading R20): gu compressed row r' of block b = r' / (2 cb)
-// (cb = compressed rows per 32 output rows) comes from gate (first half of the
+// (cb = 16 compressed rows) comes from gate (first half of the
 // block) or up (second half), row b * cb + r' % cb.  One CTA per gu row.
 __global__ void interleave_rows_kernel(const uint8_t* __restrict__ gv, const uint8_t* __restrict__ gc,
                                        const uint8_t* __restrict__ gi, const uint8_t* __restrict__ uv,
@@ -181,11 +181,44 @@ __global__ void interleave_rows_kernel(const uint8_t* __restrict__ gv, const uin
   for (int64_t i = threadIdx.x; i < ibytes; i += blockDim.x) oi[r * ibytes + i] = si[i];
 }
 
+// Decode (PAPER.md:237 inverse; oracle fmt.decode): every stored value of
+// compressed row r, V-block j, 4-group q, slot s goes to
+// W[g*M + idx[r][j], j*V + 4q + code]; everything else stays zero (memset first).
+__global__ void decompress_kernel(const uint16_t* __restrict__ values, const uint8_t* __restrict__ codes,
+                                  const uint8_t* __restrict__ indices, int64_t R, int64_t cols, int N, int M, int V,
+                                  uint16_t* __restrict__ w, int64_t ldw) {
+  const int64_t half = cols / 2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < R * half; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / half, c = i % half;
+    const int64_t j = (2 * c) / V, q = (c % (V / 2)) / 2;
+    const int code = (codes[r * (cols / 8) + c / 4] >> (2 * (c % 4))) & 3;
+    const int64_t row = (r / N) * M + indices[r * (cols / V) + j];
+    w[row * ldw + j * V + 4 * q + code] = values[i];
+  }
+}
+
+smy_status decompress_launch(const smy_weight* src, uint16_t* w, int64_t ldw, cudaStream_t s) {
+  const smy_wdesc& d = src->d;
+  cudaError_t e = cudaMemset2DAsync(w, (size_t)ldw * 2, 0, (size_t)d.cols * 2, (size_t)d.rows, s);
+  if (e != cudaSuccess) return cuda_status(e);
+  const int64_t R = d.rows * d.fmt.n / d.fmt.m;
+  const int64_t n = R * (d.cols / 2);
+  if (n == 0) return SMY_OK;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  decompress_kernel<<<blocks, 256, 0, s>>>(static_cast<const uint16_t*>(src->values),
+                                           static_cast<const uint8_t*>(src->codes),
+                                           static_cast<const uint8_t*>(src->indices), R, d.cols, d.fmt.n, d.fmt.m,
+                                           d.fmt.v, w, ldw);
+  count_launch();
+  return cuda_status(cudaGetLastError());
+}
+
 smy_status interleave_launch(const smy_weight* gate, const smy_weight* up, const smy_wdesc& d, const Geometry& g,
                              smy_weight* gu, cudaStream_t s) {
   const int64_t cols = d.cols;
   if (cols % 128) return SMY_E_SHAPE;
-  const int64_t cb = (int64_t)32 * d.fmt.n / d.fmt.m;  // compressed rows per 32 output rows
+  const int64_t cb = 16;  // compressed rows per interleave block (reading R20)
   interleave_rows_kernel<<<(unsigned)g.R, 128, 0, s>>>(
       static_cast<const uint8_t*>(gate->values), static_cast<const uint8_t*>(gate->codes),
       static_cast<const uint8_t*>(gate->indices), static_cast<const uint8_t*>(up->values),

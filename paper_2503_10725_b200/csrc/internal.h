@@ -112,10 +112,12 @@ smy_status compact_launch(const int32_t* keys, const float* vals, int64_t T, int
                           const int* tile_mt, int n_tile_cfgs, int32_t* tile_prefix, cudaStream_t s);
 
 // --------------------------------------------------------------- compress
+smy_status decompress_launch(const smy_weight* src, uint16_t* w, int64_t ldw, cudaStream_t s);
 // interleaved gate/up weight (reading R20): canonical rows moved, image re-packed
 smy_status interleave_launch(const smy_weight* gate, const smy_weight* up, const smy_wdesc& d, const Geometry& g,
                              smy_weight* gu, cudaStream_t s);
-inline bool ilv_format(const smy_format& f) { return f.n == 1 && f.m == 2 && f.v % 32 == 0; }
+// formats with an interleaved gate/up epilogue: (1,2,V) and N = M (plain 2:4), V % 32 == 0
+inline bool ilv_format(const smy_format& f) { return f.v % 32 == 0 && ((f.n == 1 && f.m == 2) || f.n == f.m); }
 smy_status compress_launch(const smy_wdesc* d, const Geometry& g, const uint16_t* w, int64_t ldw, int flags,
                            smy_weight* out, int32_t* d_status, cudaStream_t s);
 

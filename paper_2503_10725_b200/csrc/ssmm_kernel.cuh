@@ -224,6 +224,28 @@ __device__ __forceinline__ void ilv_chunk(const float (&v)[2][16], bool valid, i
   }
 }
 
+// The same for N = M weights (one accumulator slot): lanes 0-15 gate, 16-31 up
+// rows of the same 16 outputs; per column pair one shuffle, the gate lane computes
+// the even token, the up lane the odd one.
+__device__ __forceinline__ void ilv_chunk_ms1(const float (&v)[16], bool valid, int jmax, uint16_t* out, int64_t ldo,
+                                              int64_t row_base, int cg, int lane) {
+  const bool is_up = lane >= 16;
+  uint16_t act[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float recv = __shfl_xor_sync(0xffffffffu, is_up ? v[2 * j] : v[2 * j + 1], 16);
+    act[j] = __bfloat16_as_ushort(
+        __float2bfloat16_rn(is_up ? silu_mul(recv, v[2 * j + 1]) : silu_mul(v[2 * j], recv)));
+  }
+  uint16_t* o = out + (row_base + (is_up ? 1 : 0)) * ldo + cg;
+  const int n = valid ? jmax : 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (2 * j + (is_up ? 1 : 0) < n) *o = act[j];
+    o += 2 * ldo;
+  }
+}
+
 __device__ __forceinline__ void tma_tile2d(void* dst, const CUtensorMap* map, int col, int row, uint64_t* bar,
                                            uint64_t policy) {
   asm volatile(
@@ -490,6 +512,21 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
       mbar_wait(&acc_full[ab], (tcount / AB) & 1);
       if (prof) { const unsigned long long t1 = clk(); pc[3] += t1 - t0; t0 = t1; }
       tc_fence_after();
+      if (NW == 1 && MS == 1 && REP == 1 && a.epi == kEpiSiluMulIlv) {
+        // N = M: lanes 0-15 gate / 16-31 up of the same 16 outputs (reading R20)
+        const int cg = 16 * (4 * ti.m_tile + q) + (lane & 15);
+        for (int c0 = 0; c0 < ti.n_local; c0 += 16) {
+          float v[16];
+          tmem_ld16(tmem + lane_base + ab * C::kAccCols + c0, v);
+          tmem_ld_wait();
+          ilv_chunk_ms1(v, cg < a.R / 2 && !(a.debug & 8), min(16, ti.n_local - c0), static_cast<uint16_t*>(a.out),
+                        a.ldo, ti.row0 + ti.t0 + c0, cg, lane);
+        }
+        tc_fence_before();
+        zero_acc(ab);
+        if (prof) pc[4] += clk() - t0;
+        continue;
+      }
       if (NW == 1 && MS == 2 && a.epi == kEpiSiluMulIlv) {
         // lanes 0-15 gate / 16-31 up of the same 16 output pairs (reading R20)
         const int cg = 16 * (4 * ti.m_tile + q) + (lane & 15);

@@ -447,15 +447,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         const int cg = 16 * (4 * m_own + q) + (lane & 15);
         const bool gvalid = m_own < a.m_tiles && cg < a.R / 2 && !(a.debug & 8);
         for (int c0 = 16 * h; c0 < ti.n_local; c0 += 32) {
-          float v[2][16];
           const unsigned long long tl0 = prof ? clk() : 0;
-          tmem_ld16(tacc + lane_base + c0, v[0]);
-          tmem_ld16(tacc + lane_base + NT + c0, v[1]);
-          tmem_ld_wait();
-          if (prof) pc[8] += clk() - tl0;
-          if (!(a.debug & 32))
-            ilv_chunk(v, gvalid, min(16, ti.n_local - c0), static_cast<uint16_t*>(a.out), a.ldo, ti.row0 + ti.t0 + c0,
-                      cg, lane);
+          if constexpr (MS == 2) {
+            float v[2][16];
+            tmem_ld16(tacc + lane_base + c0, v[0]);
+            tmem_ld16(tacc + lane_base + NT + c0, v[1]);
+            tmem_ld_wait();
+            if (prof) pc[8] += clk() - tl0;
+            if (!(a.debug & 32))
+              ilv_chunk(v, gvalid, min(16, ti.n_local - c0), static_cast<uint16_t*>(a.out), a.ldo,
+                        ti.row0 + ti.t0 + c0, cg, lane);
+          } else {  // N = M: one slot
+            float v[16];
+            tmem_ld16(tacc + lane_base + c0, v);
+            tmem_ld_wait();
+            if (prof) pc[8] += clk() - tl0;
+            if (!(a.debug & 32))
+              ilv_chunk_ms1(v, gvalid, min(16, ti.n_local - c0), static_cast<uint16_t*>(a.out), a.ldo,
+                            ti.row0 + ti.t0 + c0, cg, lane);
+          }
         }
       }
       for (int c0 = 16 * h; !ilv && c0 < ti.n_local; c0 += 32) {

@@ -9,7 +9,7 @@ C[n x M] = x[sel] W^T, bf16 in, fp32 accumulate:
                  weight-only sparsity, rows read through SEL (no vector-wise remap)
   ssmm (1,2,32)  our SSMM on the Samoyeds format (vector-wise + 2:4, 75 % sparse),
                  rows read through SEL  -- the paper's dual-side sparse kernel
-  ssmm (1,2,16)  same at V = 16
+  ssmm (1,2,16)  same at V = 16, run as its plain-2:4 transcode (the layer's path)
 Every kernel writes fp32 [n x M].  Timing: CUDA events around the op only,
 median of R iterations, L2 flushed (a 512 MB memset) before each.
 Useful TFLOP/s follow SURVEY §8(d): 2 * (M * N/M_fmt) * K * n for ours (the
@@ -70,6 +70,8 @@ def main():
                          float(synth.uniform_scale(np.sqrt(3.0 / K))))
             wd = wt.view(torch.bfloat16)
             sws = {name: P.compress(wt, fmt)[0] for name, fmt in fmts.items()}
+            # V=16 has no fast kernel of its own: the library's path is its plain-2:4 transcode
+            sws["ssmm (1,2,16)"] = P.transcode_24(sws["ssmm (1,2,16)"])
             for sw in sws.values():
                 sw.drop_canonical()
             for n in ns:

@@ -211,8 +211,8 @@ def test_ssmm_silu_mul(smy, fmt):
     assert mismatch.mean() < 0.01, mismatch.mean()
 
 
-@pytest.mark.parametrize("fmt", [F.SparseFormat(1, 2, 32), F.SparseFormat(1, 2, 16), F.SparseFormat(4, 8, 32)],
-                         ids=str)
+@pytest.mark.parametrize("fmt", [F.SparseFormat(1, 2, 32), F.SparseFormat(1, 2, 16), F.SparseFormat(4, 8, 32),
+                                 F.SparseFormat(2, 2, 32)], ids=str)
 def test_interleave_gate_up_bit_exact(smy, fmt):
     """samoyeds_interleave_gate_up (reading R20) == the oracle's interleaved
     encoding + device image, and == compressing the interleaved dense weight."""
@@ -229,7 +229,7 @@ def test_interleave_gate_up_bit_exact(smy, fmt):
     assert np.array_equal(gu.codes.cpu().numpy().reshape(-1, d // 8), F.pack_codes(ref.codes))
     assert np.array_equal(gu.indices.cpu().numpy().reshape(ref.idx.shape), ref.idx)
     assert np.array_equal(gu.image.cpu().numpy(), D.weight_image(ref))
-    direct, _ = smy.compress(dev16(F.interleave_rows(wg, wu)), gpu_format(fmt))
+    direct, _ = smy.compress(dev16(F.interleave_rows(wg, wu, F.gu_block(fmt))), gpu_format(fmt))
     assert torch.equal(direct.image, gu.image)
 
 
@@ -259,6 +259,27 @@ def test_ssmm_silu_mul_interleaved(smy, shape):
     assert OS.rel_fro(got - exact, exact) <= 5e-3
     ulp = np.abs(bf16.to_f64(ref_bits)) * 2.0 ** -7 + 1e-30
     assert (np.abs(got - bf16.to_f64(ref_bits)) > ulp).mean() < 0.01
+
+
+@pytest.mark.parametrize("fmt", PARITY_FORMATS, ids=str)
+def test_decompress_and_transcode(smy, fmt):
+    """samoyeds_decompress returns the oracle's pruned dense weight bit for bit;
+    the plain-2:4 transcode (the fast path for N>1 / V=16 formats) gives the
+    same SSMM as the original format on integer inputs (exact)."""
+    rows, cols = 256, 256
+    w = synth.weight_bf16(33, rows, cols, integer=True)
+    sw, _ = smy.compress(dev16(w), gpu_format(fmt))
+    dense = smy.decompress(sw)
+    assert np.array_equal(host16(dense), F.prune(w, fmt))
+    again, st = smy.compress(dense, gpu_format(fmt), prune=False)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0 and torch.equal(again.image, sw.image)
+    t24 = smy.transcode_24(sw)
+    x = synth.activations_bf16(34, 200, cols, integer=True)
+    sel = synth.selection(3, 200, 150)
+    a = smy.ssmm(sw, dev16(x), torch.from_numpy(sel).cuda()).cpu().numpy()
+    b = smy.ssmm(t24, dev16(x), torch.from_numpy(sel).cuda()).cpu().numpy()
+    assert np.array_equal(a, b) and np.array_equal(b, OS.ssmm(F.encode(F.prune(w, fmt), fmt), x, sel))
 
 
 def test_ssmm_full_size_sampled(smy):
@@ -317,8 +338,9 @@ def test_route_ties(smy):
 
 # ------------------------------------------------------------------ MoE layer
 
-def _layer_case(smy, fmt, E, d, f, T, k, gating="renorm_topk", shared=0, skew=0.0, seed_off=0, gate_up="auto"):
-    cfg = smy.MoEConfig(E, k, d, f, shared, gating, gpu_format(fmt), gate_up)
+def _layer_case(smy, fmt, E, d, f, T, k, gating="renorm_topk", shared=0, skew=0.0, seed_off=0, gate_up="auto",
+                transcode="auto"):
+    cfg = smy.MoEConfig(E, k, d, f, shared, gating, gpu_format(fmt), gate_up, transcode)
     encs, sws = [], []
     for e in range(E + shared):
         te, ts = [], []
@@ -346,9 +368,12 @@ def _layer_case(smy, fmt, E, d, f, T, k, gating="renorm_topk", shared=0, skew=0.
     dict(fmt=F.SparseFormat(4, 8, 32), E=4, d=256, f=256, T=64, k=2),
     dict(fmt=F.SparseFormat(8, 16, 32), E=4, d=256, f=256, T=50, k=2),
     dict(fmt=F.SparseFormat(1, 2, 32), E=8, d=256, f=512, T=100, k=2, gate_up="separate"),
+    dict(fmt=F.SparseFormat(4, 8, 32), E=4, d=256, f=256, T=300, k=2, transcode="off"),   # lane-masked M=8 slots
+    dict(fmt=F.SparseFormat(8, 16, 32), E=4, d=256, f=256, T=50, k=2, transcode="off"),
+    dict(fmt=F.SparseFormat(2, 2, 32), E=4, d=256, f=512, T=400, k=2),                   # plain 2:4, pair kernels
     dict(fmt=F.SparseFormat(1, 2, 32), E=16, d=256, f=384, T=57, k=6, gating="softmax_all", shared=2,
          gate_up="separate"),
-], ids=lambda c: f"{c['fmt']}-E{c['E']}-T{c['T']}-{c.get('gate_up', 'auto')}")
+], ids=lambda c: f"{c['fmt']}-E{c['E']}-T{c['T']}-{c.get('gate_up', 'auto')}-{c.get('transcode', 'auto')}")
 def test_moe_layer_parity(smy, case):
     case = dict(case)
     fmt = case.pop("fmt")

@@ -239,7 +239,7 @@ def test_interleave_commutes_with_prune_and_encode(fmt):
     f, d = 256, 128
     wg = synth.weight_bf16(71, f, d)
     wu = synth.weight_bf16(72, f, d)
-    direct = F.encode(F.prune(F.interleave_rows(wg, wu), fmt), fmt)
+    direct = F.encode(F.prune(F.interleave_rows(wg, wu, F.gu_block(fmt)), fmt), fmt)
     built = F.interleave_gate_up(F.encode(F.prune(wg, fmt), fmt), F.encode(F.prune(wu, fmt), fmt))
     assert (direct.rows, direct.cols) == (built.rows, built.cols) == (2 * f, d)
     for name in ("values", "codes", "idx"):
@@ -250,7 +250,8 @@ def test_interleave_rows_layout_and_inverse():
     f, d = 96, 8
     wg = np.arange(f * d, dtype=np.uint16).reshape(f, d)
     wu = wg + np.uint16(10000)
-    assert F.GU_BLOCK == 32
+    assert F.GU_BLOCK == 32 and F.gu_block(F.SparseFormat(1, 2, 32)) == 32 and F.gu_block(F.SparseFormat(2, 2, 32)) == 16
+    assert F.gu_block(F.SparseFormat(4, 8, 32)) == 32
     gu = F.interleave_rows(wg, wu)
     # row 32 of the interleaved weight is up row 0; row 64 is gate row 32
     assert np.array_equal(gu[0], wg[0]) and np.array_equal(gu[31], wg[31])
