@@ -30,12 +30,13 @@ extern template smy_status launch_t<16,1,16,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<32,2,4,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<16,2,8,1>(const SsmmArgs&, cudaStream_t);
 
-extern template smy_status launch_pair_t<64, 2, 2>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<112, 2, 2>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<128, 1, 2>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<224, 1, 2>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<128, 1, 1>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<256, 1, 1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<64, 2, 2, 0>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<112, 2, 2, 0>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<128, 1, 2, 0>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<224, 1, 2, 0>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<224, 1, 2, 1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<128, 1, 1, 0>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<256, 1, 1, 0>(const SsmmArgs&, cudaStream_t);
 
 namespace {
 struct Entry { int nt, nw, ms, rep; smy_status (*fn)(const SsmmArgs&, cudaStream_t); };
@@ -148,12 +149,14 @@ smy_status ssmm_launch_pair(const SsmmArgs& a0, int nt, int nw, int ms, int cl, 
   a.wbase = reinterpret_cast<const uint8_t*>(lo);
   smy_status st = make_w_tmap(&a.tmap_w, a.wbase, (int64_t)((hi - lo) / 128), (kABytes + kEBytes + 64 + 127) / 128);
   if (st != SMY_OK) return st;
-  if (ms == 2 && nw == 2 && nt == 64) return launch_pair_t<64, 2, 2>(a, s);
-  if (ms == 2 && nw == 2 && nt == 112) return launch_pair_t<112, 2, 2>(a, s);
-  if (ms == 2 && nw == 1 && nt == 128) return launch_pair_t<128, 1, 2>(a, s);
-  if (ms == 2 && nw == 1 && nt == 224) return launch_pair_t<224, 1, 2>(a, s);
-  if (ms == 1 && nw == 1 && nt == 128) return launch_pair_t<128, 1, 1>(a, s);
-  if (ms == 1 && nw == 1 && nt == 256) return launch_pair_t<256, 1, 1>(a, s);
+  if (ms == 2 && nw == 2 && nt == 64) return launch_pair_t<64, 2, 2, 0>(a, s);
+  if (ms == 2 && nw == 2 && nt == 112) return launch_pair_t<112, 2, 2, 0>(a, s);
+  if (ms == 2 && nw == 1 && nt == 128) return launch_pair_t<128, 1, 2, 0>(a, s);
+  // SEL-gathered token rows (gate/up): separate, deeper token ring
+  if (ms == 2 && nw == 1 && nt == 224) return a.sel_in && !(a.debug & 16384) ? launch_pair_t<224, 1, 2, 1>(a, s)
+                                                                              : launch_pair_t<224, 1, 2, 0>(a, s);
+  if (ms == 1 && nw == 1 && nt == 128) return launch_pair_t<128, 1, 1, 0>(a, s);
+  if (ms == 1 && nw == 1 && nt == 256) return launch_pair_t<256, 1, 1, 0>(a, s);
   set_last_error("ssmm: unsupported pair (nt, nw)");
   return SMY_E_CONFIG;
 }

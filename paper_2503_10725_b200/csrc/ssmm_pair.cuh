@@ -153,7 +153,10 @@ constexpr int kPairThreads = 32 * (11 + kPairEpiWarps - 4);  // + producer, 2 MM
 
 // MS = accumulator slots per weight: 2 for (1,2,V) (the lane-masked remap), 1 for
 // N == M (plain 2:4, no remap -- the weight-only-sparse baseline formats)
-template <int NT, int NW, int MS_ = 2>
+// SPLIT: separate weight / token rings (own barriers, deeper token ring) -- the SEL
+// gather launches (gate/up), whose token-row loads show the longest latency; the
+// contiguous-row launches (down) keep both in one lock-step ring
+template <int NT, int NW, int MS_ = 2, int SPLIT = 0>
 struct PairCfg {
   static constexpr int MS = MS_;
   static constexpr int kHalf = NT / 2;                      // tokens per CTA
@@ -161,7 +164,8 @@ struct PairCfg {
   static constexpr int kWRows = (kABytes + kEBytes + 64 + 127) / 128;  // TMA box rows of one weight tile
   static constexpr int kBBytes = kHalf * 256;               // 2 K-atoms x kHalf rows x 128 B
   static constexpr int kPeerPl = MS == 2 ? 128 : 0;         // the peer m-tile's index planes (leader)
-  static constexpr int kStageBytes = (NW * kWStride + kBBytes + kPeerPl + 1023) / 1024 * 1024;
+  static constexpr int kWStage = (NW * kWStride + kPeerPl + 1023) / 1024 * 1024;  // weight slot (+ peer planes)
+  static constexpr int kBStage = (kBBytes + 1023) / 1024 * 1024;                  // token-row slot
   static constexpr int kAccCols = NW * MS * NT;
   // two accumulator sets when they fit (NT <= 112 at NW = 1): the epilogue drains
   // tile i while the MMAs of tile i+1 run -- for short-K launches whose epilogue is
@@ -172,28 +176,37 @@ struct PairCfg {
   static constexpr int kTmemCols = kColsNeeded <= 128 ? 128 : kColsNeeded <= 256 ? 256 : 512;
   static constexpr int kAux = 2048;
   static constexpr int kSmemCap = 232448 - 1024 - kAux;
-  static constexpr int kStagesRaw = kSmemCap / kStageBytes;
-  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + kAux;
+  static constexpr int kStagesRaw = kSmemCap / (kWStage + kBStage);
+  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;          // lock-step ring depth
+  // split rings: 5 token slots (measured: their depth matters more than the weights'),
+  // the rest of shared memory to weight slots
+  static constexpr int kBFit = (kSmemCap - 3 * kWStage) / kBStage;
+  static constexpr int kBStages = SPLIT ? (5 < kBFit ? 5 : kBFit) : kStages;
+  static constexpr int kWStagesRaw = SPLIT ? (kSmemCap - kBStages * kBStage) / kWStage : kStages;
+  static constexpr int kWStages = kWStagesRaw > 8 ? 8 : kWStagesRaw;
+  static constexpr int kSmemBytes = kWStages * kWStage + kBStages * kBStage + 1024 + kAux;
   static_assert(kColsNeeded <= 512, "TMEM budget");
-  static_assert(kStages >= 2, "smem budget");
+  static_assert(kBStages >= 2 && kWStages >= 2, "smem budget");
   static_assert(NT % 16 == 0 && (NT / 2) % 8 == 0 && NT >= 32 && NT <= 256, "UMMA N (cta_group::2) / 8-row halves");
 };
 
-template <int NT, int NW, int MS>
+template <int NT, int NW, int MS, int SPLIT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     ssmm_pair_kernel(const __grid_constant__ SsmmArgs a) {
-  using C = PairCfg<NT, NW, MS>;
-  constexpr int S = C::kStages;
+  using C = PairCfg<NT, NW, MS, SPLIT>;
+  constexpr int SW = C::kWStages, SB = C::kBStages;
   constexpr int kIssuers = (NW == 2 || MS == 2) ? 2 : 1;  // MMA-issuing warps
   constexpr int H = C::kHalf;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* aux = smem + S * C::kStageBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(aux);
-  uint64_t* empty = full + S;
+  uint8_t* aux = smem + SW * C::kWStage + SB * C::kBStage;
+  // lock-step: wfull / wempty serve both rings; split: bfull / bempty for the tokens
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(aux);  // [SW]
+  uint64_t* wempty = wfull + 8;                        // [SW]
+  uint64_t* bfull = SPLIT ? wempty + 8 : wfull;        // [SB]
+  uint64_t* bempty = SPLIT ? wempty + 16 : wempty;     // [SB]
   constexpr int AB = C::kAccBufs;
-  uint64_t* acc_full = empty + S;      // [AB]
+  uint64_t* acc_full = wempty + 24;    // [AB]
   uint64_t* acc_empty = acc_full + 2;  // [AB]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -202,11 +215,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   const bool gather = a.sel_in != nullptr;
   const int warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      // leader: its producer's expect_tx (all TMA bytes of both CTAs) + its gather
-      // threads + the peer's gather relay; peer: its gather threads (relayed)
-      mbar_init(&full[s], leader ? 1 + (gather ? kGatherThreads + 1 : 0) : (gather ? kGatherThreads : 1));
-      mbar_init(&empty[s], kIssuers);  // every issuer warp's commit
+    if constexpr (SPLIT) {
+      for (int s = 0; s < SW; ++s) {
+        mbar_init(&wfull[s], 1);          // the leader's expect_tx (both CTAs' weight bytes + planes)
+        mbar_init(&wempty[s], kIssuers);  // every issuer warp's commit
+      }
+      for (int s = 0; s < SB; ++s) {
+        // gather: own gather threads (+ the peer's relay on the leader); contiguous
+        // rows: the leader's expect_tx (both CTAs' TMA bytes)
+        mbar_init(&bfull[s], gather ? kGatherThreads + (leader ? 1 : 0) : 1);
+        mbar_init(&bempty[s], kIssuers);
+      }
+    } else {
+      for (int s = 0; s < SW; ++s) {
+        // leader: its producer's expect_tx (all TMA bytes of both CTAs) + its gather
+        // threads + the peer's gather relay; peer: its gather threads (relayed)
+        mbar_init(&wfull[s], leader ? 1 + (gather ? kGatherThreads + 1 : 0) : (gather ? kGatherThreads : 1));
+        mbar_init(&wempty[s], kIssuers);  // every issuer warp's commit
+      }
     }
     for (int b = 0; b < AB; ++b) {
       mbar_init(&acc_full[b], kIssuers);           // every issuer warp's commit
@@ -220,12 +246,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   cluster_sync_all();  // both CTAs' barriers exist before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  auto wsm = [&](int st, int w) { return smem + st * C::kStageBytes + w * C::kWStride; };
-  auto bsm = [&](int st) { return smem + st * C::kStageBytes + NW * C::kWStride; };
-  auto psm = [&](int st) { return smem + st * C::kStageBytes + NW * C::kWStride + C::kBBytes; };
+  auto wsm = [&](int st, int w) { return smem + st * C::kWStage + w * C::kWStride; };
+  auto psm = [&](int st) { return smem + st * C::kWStage + NW * C::kWStride; };
+  auto bsm = [&](int st) { return smem + SW * C::kWStage + st * C::kBStage; };
   const int ks = a.k_stages;
   const int pair0 = blockIdx.x >> 1, pstep = gridDim.x >> 1;
-  const uint32_t full_lead = mapa_shared(smem_u32(full), 0);  // the leader's full[0], cluster window
+  const uint32_t wfull_lead = mapa_shared(smem_u32(wfull), 0);  // the leader's barriers, cluster window
+  const uint32_t bfull_lead = mapa_shared(smem_u32(bfull), 0);
 
   const bool prof = a.prof != nullptr;
   unsigned long long pc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -237,7 +264,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     // the leader's full) + (leader) the peer m-tile's index planes =========
     if (lane == 0) {
       const uint32_t wbytes = (a.debug & 2) ? 0u : (uint32_t)C::kWRows * 128;
-      const uint32_t pair_bytes = 2 * (NW * wbytes + (gather ? 0u : (uint32_t)C::kBBytes)) + (MS == 2 ? NW * 64u : 0u);
+      const uint32_t w_pair_bytes = 2 * NW * wbytes + (MS == 2 ? NW * 64u : 0u);
+      const uint32_t b_pair_bytes = gather ? 0u : 2 * (uint32_t)C::kBBytes;
       // prefill: the pairs on the same m-tile read its weights at about the same
       // time; evict_normal measured better than evict_first (fewer re-reads)
       const uint64_t pol_w = a.weights_stream ? policy_evict_first() : policy_evict_normal();
@@ -256,23 +284,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         for (int w = 0; w < NW; ++w) wrow[w] = (int)((src[w] - a.wbase) >> 7) + m_own * ks * brows;
         const int xrow = ti.row0 + ti.t0 + (int)cta * hh;
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
-          const int st = it % S;
+          const int st = it % SW;
           const unsigned long long t0 = prof ? clk() : 0;
-          mbar_wait_cta(&empty[st], ((it / S) & 1) ^ 1);
+          mbar_wait_cta(&wempty[st], ((it / SW) & 1) ^ 1);
           if (prof) pc[5] += clk() - t0;
-          const uint32_t bar = full_lead + st * 8;
-          if (leader) mbar_arrive_expect_tx(&full[st], pair_bytes);
+          if (leader) mbar_arrive_expect_tx(&wfull[st], SPLIT ? w_pair_bytes : w_pair_bytes + b_pair_bytes);
 #pragma unroll
           for (int w = 0; w < NW; ++w) {
-            if (!(a.debug & 2)) tma2d_pair(wsm(st, w), &a.tmap_w, 0, wrow[w] + k * brows, bar, pol_w);
+            if (!(a.debug & 2)) tma2d_pair(wsm(st, w), &a.tmap_w, 0, wrow[w] + k * brows, wfull_lead + st * 8, pol_w);
             if (MS == 2 && leader)
               bulk_g2s(psm(st) + 64 * w, src[w] + ((size_t)m_peer * ks + k) * a.block + kABytes + kEBytes, 64,
-                       &full[st], pol_w);
+                       &wfull[st], pol_w);
           }
           if (!gather) {
+            const int sb = it % SB;
+            if constexpr (SPLIT) {
+              mbar_wait_cta(&bempty[sb], ((it / SB) & 1) ^ 1);
+              if (leader) mbar_arrive_expect_tx(&bfull[sb], b_pair_bytes);
+            }
 #pragma unroll
             for (int atom = 0; atom < 2; ++atom)
-              tma2d_pair(bsm(st) + atom * (H * 128), &a.tmap_x, k * 128 + atom * 64, xrow, bar, pol_x);
+              tma2d_pair(bsm(sb) + atom * (H * 128), &a.tmap_x, k * 128 + atom * 64, xrow, bfull_lead + sb * 8, pol_x);
           }
         }
       }
@@ -305,12 +337,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         tc_fence_after();
         const uint32_t idesc = __reduce_or_sync(0xffffffffu, idesc0 | ((uint32_t)(2 * pair_half(ti.n_local)) >> 3) << 17);
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
-          const int st = it % S;
+          const int st = it % SW, sb = it % SB;
           t0 = prof ? clk() : 0;
-          mbar_wait_acq_cluster(&full[st], (it / S) & 1);  // both CTAs' stage (peer bytes + relay)
+          if constexpr (SPLIT) {
+            // weight slots: TMA / bulk copies only (CTA-scope acquire); token slots
+            // include the peer's cp.async writes, made visible by its relay's release
+            mbar_wait_cta(&wfull[st], (it / SW) & 1);
+            mbar_wait_acq_cluster(&bfull[sb], (it / SB) & 1);
+          } else {
+            mbar_wait_acq_cluster(&wfull[st], (it / SW) & 1);  // both CTAs' stage (peer bytes + relay)
+          }
           if (prof) pc[0] += clk() - t0;
           tc_fence_after();
-          const uint32_t sbase = smem_base + st * C::kStageBytes;
+          const uint32_t sbase = smem_base + st * C::kWStage;
+          const uint32_t bbase = smem_base + SW * C::kWStage + sb * C::kBStage;
           const uint32_t ecol = C::kECol + (it & 1) * 8 + 4 * mi;
           tc_cp2_elect(tm + ecol, desc_interleave(sbase + w * C::kWStride + kABytes));
           uint32_t pl[4][8];  // lane planes: words 0-3 this CTA's 128 lanes, 4-7 the peer's
@@ -330,7 +370,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 #pragma unroll
           for (int kb = 0; kb < 4; ++kb) {
             const int e0 = kb * 32;
-            const uint64_t bdesc = desc_sw128(sbase + NW * C::kWStride + (e0 / 64) * (H * 128) + (e0 % 64) * 2);
+            const uint64_t bdesc = desc_sw128(bbase + (e0 / 64) * (H * 128) + (e0 % 64) * 2);
             const uint64_t adesc = desc_sw128(sbase + w * C::kWStride + kb * 32);
 #pragma unroll
             for (int pp = 0; pp < NP; ++pp) {
@@ -343,7 +383,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                                  tm + ecol + (kb & 2));
             }
           }
-          tc_commit2_mc_elect(&empty[st], 0x3);
+          tc_commit2_mc_elect(&wempty[st], 0x3);
+          if constexpr (SPLIT) tc_commit2_mc_elect(&bempty[sb], 0x3);
         }
         tc_commit2_mc_elect(&acc_full[ab], 0x3);
         pc[7] += 1;
@@ -355,9 +396,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       TileInfo ti;
       for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep)
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
-          const int st = it % S;
-          mbar_spin(&full[st], (it / S) & 1);
-          mbar_arrive_cluster(full_lead + st * 8);
+          const int sb = it % SB;
+          mbar_spin(&bfull[sb], (it / SB) & 1);
+          mbar_arrive_cluster(bfull_lead + sb * 8);
         }
     }
   } else if (warp >= 6 && warp < 10) {
@@ -387,9 +428,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           valid |= (rid >= 0 ? 1u : 0u) << i;
         }
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
-          const int st = it % S;
+          const int st = it % SB;
           unsigned long long tg0 = prof ? clk() : 0;
-          mbar_wait_cta(&empty[st], ((it / S) & 1) ^ 1);
+          mbar_wait_cta(&bempty[st], ((it / SB) & 1) ^ 1);
           if (prof) { const unsigned long long t1 = clk(); pc[10] += t1 - tg0; tg0 = t1; }
           const int64_t kcol0 = (int64_t)k * 128;
           const uint32_t bs = smem_u32(bsm(st)) + dst0;
@@ -401,7 +442,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(bs + 1024u * i), "l"(src[i] + kcol0)
                              : "memory");
           }
-          cp_async_mbar_arrive_noinc(&full[st]);
+          cp_async_mbar_arrive_noinc(&bfull[st]);
           if (prof) pc[11] += clk() - tg0;
         }
       }
@@ -581,12 +622,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   if (warp == 5) tmem_dealloc2(tmem, C::kTmemCols);
 }
 
-template <int NT, int NW, int MS>
+template <int NT, int NW, int MS, int SPLIT>
 smy_status launch_pair_t(const SsmmArgs& a, cudaStream_t s) {
-  using C = PairCfg<NT, NW, MS>;
+  using C = PairCfg<NT, NW, MS, SPLIT>;
   static bool configured = false;
   static int num_sms = 0;
-  auto kern = ssmm_pair_kernel<NT, NW, MS>;
+  auto kern = ssmm_pair_kernel<NT, NW, MS, SPLIT>;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return cuda_status(e);
