@@ -409,21 +409,22 @@ def _prune_rows(w_bits, fmt, chunk=512):
     return np.concatenate([F.prune(w_bits[i:i + chunk], fmt) for i in range(0, w_bits.shape[0], chunk)])
 
 
-@pytest.mark.parametrize("T", [4096, 64])
-def test_moe_layer_full_size_sampled(smy, T):
-    """The bench's N=1 workload itself -- Mixtral-8x7B layer, T=4096 (interleaved
-    gate/up + stream-K down on CTA pairs) and its T=64 decode point (single-CTA
-    kernels), built by bench.build_layer -- checked
-    against the fp64 oracle on sampled outputs: every token routed to the most
-    common expert pair (up to 6 of them), 24 sampled output row pairs.  The
-    oracle regenerates the weights it needs by index (counter-based generator)
-    and prunes them itself."""
+@pytest.mark.parametrize("model,T", [("mixtral", 4096), ("mixtral", 64), ("deepseek", 4096), ("qwen2", 4096),
+                                     ("qwen2", 64)])
+def test_moe_layer_full_size_sampled(smy, model, T):
+    """The bench's workloads themselves -- Mixtral-8x7B / DeepSeek-MoE-16B /
+    Qwen2-57B-A14B layers at T=4096 (interleaved gate/up + stream-K down on CTA
+    pairs) and T=64 decode points (single-CTA kernels), built by
+    bench.build_layer -- checked against the fp64 oracle on sampled outputs:
+    every token routed to the most common expert set (up to 6 of them), 24
+    sampled output row pairs.  The oracle regenerates the weights it needs by
+    index (counter-based generator) and prunes them itself."""
     import bench
-    d, f, E, k, _ = bench.MODELS["mixtral"]
+    d, f, E, k, gating = bench.MODELS[model]
     fmt = F.SparseFormat(1, 2, 32)
     dev = torch.device("cuda")
-    layer = smy.MoELayer(smy.MoEConfig(E, k, d, f, 0, "renorm_topk", smy.Format(1, 2, 32)),
-                         bench.build_layer(smy, "mixtral", dev), max_tokens=T, device=dev)
+    layer = smy.MoELayer(smy.MoEConfig(E, k, d, f, 0, gating, smy.Format(1, 2, 32)),
+                         bench.build_layer(smy, model, dev), max_tokens=T, device=dev)
     x = torch.empty(T, d, dtype=torch.int16, device=dev)
     smy.synth_fill(x, synth.SEED_X, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
     lg = torch.empty(T, E, dtype=torch.float32, device=dev)
@@ -433,7 +434,7 @@ def test_moe_layer_full_size_sampled(smy, T):
     del layer
     torch.cuda.empty_cache()
 
-    ids, gw = moe.route(lgh, k, moe.RENORM_TOPK)
+    ids, gw = moe.route(lgh, k, moe.SOFTMAX_ALL if gating == "softmax_all" else moe.RENORM_TOPK)
     pairs = [tuple(sorted(r)) for r in ids]
     pair = max(set(pairs), key=pairs.count)
     toks = np.array([t for t in range(T) if pairs[t] == pair][:6])
@@ -459,4 +460,4 @@ def test_moe_layer_full_size_sampled(smy, T):
         g_e = np.array([gw[t][list(ids[t]).index(e)] for t in toks])[:, None]
         ref += g_e * (a @ wd.T)
         S += np.abs(g_e) * (np.abs(a) @ np.abs(wd).T)
-    check_tol(out[np.ix_(toks, orow)], ref, S, f"Mixtral T={T} layer, tokens {toks.tolist()} (experts {pair})")
+    check_tol(out[np.ix_(toks, orow)], ref, S, f"{model} T={T} layer, tokens {toks.tolist()} (experts {pair})")
