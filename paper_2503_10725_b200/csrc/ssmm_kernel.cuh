@@ -207,20 +207,26 @@ __device__ __forceinline__ void scatter_chunk_v4(const float (&v0)[16], const fl
 __device__ __forceinline__ void ilv_chunk(const float (&v)[2][16], bool valid, int jmax, uint16_t* out, int64_t ldo,
                                           int64_t row_base, int cg, int lane) {
   const bool is_up = lane >= 16;
-  // all 16 columns' math first (independent chains, no branches), then the
-  // predicated stores walking one row pointer
-  uint16_t act[16];
+  // token pair (c, c+1): the gate lane finishes both slots of token c, the up lane
+  // both slots of token c+1 -- two shuffles swap what each lacks, and each lane
+  // stores its two adjacent outputs as one bf16x2 (the epilogue is issue-bound)
+  uint32_t packed[8];
 #pragma unroll
-  for (int c = 0; c < 16; ++c) {
-    const float recv = __shfl_xor_sync(0xffffffffu, is_up ? v[0][c] : v[1][c], 16);
-    act[c] = __bfloat16_as_ushort(__float2bfloat16_rn(is_up ? silu_mul(recv, v[1][c]) : silu_mul(v[0][c], recv)));
+  for (int j = 0; j < 8; ++j) {
+    const int c = 2 * j;
+    const float r0 = __shfl_xor_sync(0xffffffffu, is_up ? v[0][c] : v[0][c + 1], 16);
+    const float r1 = __shfl_xor_sync(0xffffffffu, is_up ? v[1][c] : v[1][c + 1], 16);
+    const float g0 = is_up ? r0 : v[0][c], u0 = is_up ? v[0][c + 1] : r0;
+    const float g1 = is_up ? r1 : v[1][c], u1 = is_up ? v[1][c + 1] : r1;
+    const __nv_bfloat162 h = __floats2bfloat162_rn(silu_mul(g0, u0), silu_mul(g1, u1));
+    packed[j] = *reinterpret_cast<const uint32_t*>(&h);
   }
-  uint16_t* o = out + row_base * ldo + 2 * cg + (is_up ? 1 : 0);
+  uint32_t* o = reinterpret_cast<uint32_t*>(out + (row_base + (is_up ? 1 : 0)) * ldo + 2 * cg);
   const int n = valid ? jmax : 0;
 #pragma unroll
-  for (int c = 0; c < 16; ++c) {
-    if (c < n) *o = act[c];
-    o += ldo;
+  for (int j = 0; j < 8; ++j) {
+    if (2 * j + (is_up ? 1 : 0) < n) *o = packed[j];
+    o += ldo;  // two rows of ldo bf16 = ldo 32-bit words
   }
 }
 
