@@ -22,9 +22,9 @@ for r in rows[1:]:
     name = re.sub(r"\(.*", "", r[ki])
     if "route_topk" in name:
         seen.clear()
-    if "ssmm" in name:       # gate/up and down may share an instantiation: label by call order
-        seen[name] += 1
-        name += " [%s]" % ("gate/up" if seen[name] == 1 else "down")
+    if "ssmm" in name:       # label by call order within the layer call: gate/up first, then down
+        seen["ssmm"] += 1
+        name += " [%s]" % ("gate/up" if seen["ssmm"] == 1 else "down")
     tot[name] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
     cnt[name] += 1
 setup = re.compile(sys.argv[2] if len(sys.argv) > 2 else r"synth_kernel|encode_kernel|pack_kernel|interleave_rows_kernel|native::|cuda::")
