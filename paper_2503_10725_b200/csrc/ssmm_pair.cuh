@@ -122,6 +122,16 @@ __device__ __forceinline__ void tc_mma_sp2_elect(uint32_t d_tmem, uint64_t adesc
       "r"(m[7]), "r"(e_tmem)
       : "memory");
 }
+// D = 0 over this pair's 256 lanes x N columns: a dense MMA of an all-zero A and B
+// (both descriptors alias one zeroed 128-B core matrix, LBO = SBO = 0) with
+// enable_input_d = 0 -- clears the accumulator the lane-masked MMAs then add into
+__device__ __forceinline__ void tc_mma2_zero_elect(uint32_t d_tmem, uint64_t zdesc, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %1, %2, 0;\n\t}" ::"r"(d_tmem),
+      "l"(zdesc), "r"(idesc)
+      : "memory");
+}
 // arrive on the same-offset mbarrier in every CTA of `cta_mask` once all prior
 // tcgen05 ops of this thread complete
 __device__ __forceinline__ void tc_commit2_mc_elect(uint64_t* bar, uint16_t cta_mask) {
@@ -214,6 +224,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   const bool leader = cta == 0;
   const bool gather = a.sel_in != nullptr;
   const int warp = warp_id(), lane = lane_id();
+  uint8_t* zbuf = aux + 1024;  // 1 KB of zeros: the operand of the accumulator-clearing MMA
+  if (threadIdx.x < 256) {
+    reinterpret_cast<uint32_t*>(zbuf)[threadIdx.x] = 0u;
+    fence_proxy_async_smem();
+  }
   if (threadIdx.x == 0) {
     if constexpr (SPLIT) {
       for (int s = 0; s < SW; ++s) {
@@ -323,6 +338,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       constexpr int NP = NW == 2 ? MS : 1;  // slots this warp issues
       // N of a tile = 2 * its per-CTA half (runtime: ragged tiles issue narrower MMAs)
       constexpr uint32_t idesc0 = (1u << 2) | (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 4) << 24);
+      constexpr uint32_t zidesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 4) << 24);  // dense
+      const uint64_t zdesc = (uint64_t)((smem_u32(zbuf) & 0x3FFFF) >> 4) | ((uint64_t)1 << 46);  // no swizzle, LBO = SBO = 0
       const uint32_t smem_base = smem_u32(smem);
       const uint32_t tm = __reduce_or_sync(0xffffffffu, tmem);
       uint32_t it = 0, tcount = 0;
@@ -332,10 +349,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         unsigned long long t0 = prof ? clk() : 0;
         const int ab = tcount % AB;
         const uint32_t tacc = tm + ab * C::kAccCols;
-        mbar_wait_cta(&acc_empty[ab], (tcount / AB) & 1);  // both epilogues drained and re-zeroed
+        mbar_wait_cta(&acc_empty[ab], (tcount / AB) & 1);  // both epilogues have read the accumulator
         if (prof) pc[1] += clk() - t0;
         tc_fence_after();
-        const uint32_t idesc = __reduce_or_sync(0xffffffffu, idesc0 | ((uint32_t)(2 * pair_half(ti.n_local)) >> 3) << 17);
+        const uint32_t nbits = __reduce_or_sync(0xffffffffu, ((uint32_t)(2 * pair_half(ti.n_local)) >> 3) << 17);
+        const uint32_t idesc = idesc0 | nbits;
+        // clear this warp's accumulator regions (the masked MMAs only add into the
+        // lanes they enable); ordered before them as MMAs of the same thread
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp)
+          tc_mma2_zero_elect(tacc + (w * MS + (NW == 2 ? pp : mi)) * NT, zdesc, zidesc | nbits);
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % SW, sb = it % SB;
           t0 = prof ? clk() : 0;
@@ -458,17 +481,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       zero_slice(a, (int64_t)blockIdx.x * 256 + (q + 4 * h) * 32 + lane, (int64_t)gridDim.x * 256);
     const uint32_t lane_base = (uint32_t)(32 * q) << 16;
     const uint32_t acc_empty_leader = mapa_shared(smem_u32(acc_empty), 0);
-    auto zero_acc = [&](int b) {
-      // the same (weight, slot, chunk) split as the reads: regions start at j*NT,
-      // and NT (e.g. 112) need not be a multiple of 32
-      for (int j = 0; j < NW * MS; ++j)
-        for (int c = 16 * h; c < NT; c += 32) tmem_st16_zero(tmem + lane_base + b * C::kAccCols + j * NT + c);
-      tmem_st_wait();
+    // the accumulator is cleared by the issuer's zero MMA at the start of each tile,
+    // so a warp hands its TMEM columns back right after its last load of a tile
+    auto release = [&](int b) {
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(acc_empty_leader + 8 * b);
     };
-    for (int b = 0; b < AB; ++b) zero_acc(b);
+    for (int b = 0; b < AB; ++b) release(b);
     uint32_t tcount = 0;
     TileInfo ti;
     const bool ilv = NW == 1 && a.epi == kEpiSiluMulIlv;
@@ -494,6 +514,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             tmem_ld16(tacc + lane_base + c0, v[0]);
             tmem_ld16(tacc + lane_base + NT + c0, v[1]);
             tmem_ld_wait();
+            if (c0 + 32 >= ti.n_local) release(ab);
             if (prof) pc[8] += clk() - tl0;
             if (!(a.debug & 32))
               ilv_chunk(v, gvalid, min(16, ti.n_local - c0), static_cast<uint16_t*>(a.out), a.ldo,
@@ -502,6 +523,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             float v[16];
             tmem_ld16(tacc + lane_base + c0, v);
             tmem_ld_wait();
+            if (c0 + 32 >= ti.n_local) release(ab);
             if (prof) pc[8] += clk() - tl0;
             if (!(a.debug & 32))
               ilv_chunk_ms1(v, gvalid, min(16, ti.n_local - c0), static_cast<uint16_t*>(a.out), a.ldo,
@@ -517,6 +539,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 #pragma unroll
           for (int p = 0; p < MS; ++p) tmem_ld16(tacc + lane_base + (w * MS + p) * NT + c0, v[w][p]);
         tmem_ld_wait();
+        if (c0 + 32 >= ti.n_local) release(ab);
         if (prof) pc[8] += clk() - tl0;
         const int jmax = min(16, ti.n_local - c0);
         const int n = (valid && !(a.debug & 8)) ? jmax : 0;
@@ -590,10 +613,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           }
         }
       }
-      const unsigned long long tz0 = prof ? clk() : 0;
-      tc_fence_before();
-      zero_acc(ab);
-      if (prof) { const unsigned long long t1 = clk(); pc[9] += t1 - tz0; pc[4] += t1 - t0; }
+      if (16 * h >= ti.n_local) release(ab);  // no chunk of this tile for this warp
+      if (prof) pc[4] += clk() - t0;
     }
   }
   if (prof) {
