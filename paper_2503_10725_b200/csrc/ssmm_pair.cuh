@@ -366,7 +366,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             // weight slots: TMA / bulk copies only (CTA-scope acquire); token slots
             // include the peer's cp.async writes, made visible by its relay's release
             mbar_wait_cta(&wfull[st], (it / SW) & 1);
+            if (prof) { const unsigned long long t1 = clk(); pc[0] += t1 - t0; t0 = t1; }
             mbar_wait_acq_cluster(&bfull[sb], (it / SB) & 1);
+            if (prof) { pc[6] += clk() - t0; t0 = clk(); }  // token-ring share of the operand waits
           } else {
             mbar_wait_acq_cluster(&wfull[st], (it / SW) & 1);  // both CTAs' stage (peer bytes + relay)
           }
@@ -620,7 +622,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   if (prof) {
     unsigned long long* o = a.prof + ((size_t)(a.epi == kEpiScatter) * 148 + blockIdx.x) * 16;
     if (warp == 5 && lane == 0) {
-      atomicAdd(o + 0, pc[0]); atomicAdd(o + 1, pc[1]); atomicAdd(o + 2, pc[2]); atomicAdd(o + 7, pc[7]);
+      atomicAdd(o + 0, pc[0] + pc[6]); atomicAdd(o + 1, pc[1]); atomicAdd(o + 2, pc[2]); atomicAdd(o + 6, pc[6]);
+      atomicAdd(o + 7, pc[7]);
     }
     if (warp == 6 && lane == 0) { atomicAdd(o + 10, pc[10]); atomicAdd(o + 11, pc[11]); }
     if (warp == 0 && lane == 0) { atomicAdd(o + 3, pc[3]); atomicAdd(o + 4, pc[4]); atomicAdd(o + 8, pc[8]); atomicAdd(o + 9, pc[9]); }

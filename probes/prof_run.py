@@ -37,8 +37,9 @@ for name, a in zip(("gate/up", "down"), A):
     lead = a[0::2]
     t = max(lead[:, 7].mean(), 1e-9)
     print(f"{model} T={T} {name}: kcycles per CTA per layer call; tiles/pair {lead[:, 7].mean() * 1e3:.1f}")
-    print("  MMA warp: total %.1f  wait_full %.1f  wait_acc_empty %.1f  issue %.1f"
-          % (lead[:, 2].mean(), lead[:, 0].mean(), lead[:, 1].mean(), (lead[:, 2] - lead[:, 0] - lead[:, 1]).mean()))
+    print("  MMA warp: total %.1f  wait_full %.1f (token ring %.1f)  wait_acc_empty %.1f  issue %.1f"
+          % (lead[:, 2].mean(), lead[:, 0].mean(), lead[:, 6].mean(), lead[:, 1].mean(),
+             (lead[:, 2] - lead[:, 0] - lead[:, 1]).mean()))
     print("  gather warp: wait_empty %.1f  issue %.1f (leader) / %.1f %.1f (peer)"
           % (lead[:, 10].mean(), lead[:, 11].mean(), a[1::2, 10].mean(), a[1::2, 11].mean()))
     r = raw[0 if name == "gate/up" else 1]
@@ -48,5 +49,5 @@ for name, a in zip(("gate/up", "down"), A):
         print("  CTA lifetime %.1f us (mean), max %.1f us; last call: CTA starts spread %.1f us, ends spread %.1f us,"
               " span %.1f us" % (a[:, 13].mean(), a[:, 13].max(), (st.max() - st.min()) / 1e3,
                                  (en.max() - en.min()) / 1e3, (en.max() - st.min()) / 1e3))
-    print("  epilogue: wait_acc_full %.1f  work %.1f (tmem_ld %.1f, zero %.1f)   producer wait_empty %.1f"
-          % tuple(a[:, i].mean() for i in (3, 4, 8, 9, 5)))
+    print("  epilogue: wait_acc_full %.1f  work %.1f (tmem_ld %.1f)   producer wait_empty %.1f"
+          % tuple(a[:, i].mean() for i in (3, 4, 8, 5)))
