@@ -250,7 +250,10 @@ def run_ours(args):
     d, f, E, k, gating = MODELS[model]
     T = args.tokens
     ep = (world > 1 or args.force_ep) and args.parallel == "ep"
-    cfg = P.MoEConfig(E, k, d, f, 0, gating, P.Format(*FMT), "auto", args.transcode)
+    NS = args.shared
+    if NS and (world > 1 or args.force_ep) and args.parallel == "ep":
+        raise SystemExit("--shared: shared experts are measured on the 1-GPU / data-parallel layer")
+    cfg = P.MoEConfig(E, k, d, f, NS, gating, P.Format(*FMT), "auto", args.transcode)
     transport = None
     x = torch.empty(T, d, dtype=torch.int16, device=device)
     if ep:
@@ -275,7 +278,10 @@ def run_ours(args):
             layer = EPMoELayer(cfg, experts, rank, world, max_tokens=T, device=device, exchange=TorchExchange())
     else:
         experts = build_layer(P, model, device, transcode=args.transcode)
-        layer = P.MoELayer(cfg, experts, max_tokens=T, device=device)
+        # shared experts: every token, weight 1 (reading R15);
+        # weights drawn like routed experts E, E+1, ...
+        shared = build_layer(P, model, device, experts=range(E, E + NS), transcode=args.transcode) if NS else ()
+        layer = P.MoELayer(cfg, experts, shared=shared, max_tokens=T, device=device)
 
     P.synth_fill(x, synth.SEED_X + 100 * rank, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
     lg = torch.empty(T, E, dtype=torch.float32, device=device)
@@ -466,25 +472,25 @@ def run_ours(args):
                  "algorithmic_flops": flops_gu, "algorithmic_bytes": bytes_gu,
                  "other_view": ({"achieved_gbs": ach_gbs, "hbm_frac": ach_gbs / hbm} if tensor_bound else
                                 {"achieved_tflops": ach_tf, "sparse_frac": ach_tf / sparse_peak})})
-    flops_layer = 3 * flops_gu / 2
+    flops_layer = 3 * flops_gu / 2 + NS * 3 * 2 * (f // 2) * d * T   # + shared experts (all T tokens each)
     line = {
         "metric": "moe_layer_tokens_per_s", "value": T * world / (ms * 1e-3), "unit": "tokens/s",
         "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": WORKLOAD[model], "tokens_per_gpu": T, "global_tokens": T * world, "hidden": d,
-                   "ffn": f, "experts": E, "top_k": k, "gating": gating, "format": "(N,M,V)=(%d,%d,%d) + 2:4" % FMT + (" (run as plain 2:4)" if cfg.kernel_config() is not cfg
+        "config": {"workload": WORKLOAD[model] + (f"+{NS}shared" if NS else ""), "tokens_per_gpu": T, "global_tokens": T * world, "hidden": d,
+                   "ffn": f, "experts": E, "top_k": k, "shared_experts": NS, "gating": gating, "format": "(N,M,V)=(%d,%d,%d) + 2:4" % FMT + (" (run as plain 2:4)" if cfg.kernel_config() is not cfg
                                                                else ""),
                    "parallelism": ((f"ep{world} (experts sharded; token rows / outputs over NVLink peer memory "
                                     "inside the SSMM kernels, tags over NCCL)" if transport == "peer" else
                                     f"ep{world} (experts sharded, NCCL all_to_all_v dispatch/combine)") if ep
                                    else f"dp{world} (experts replicated per GPU)"),
                    "l2": "inputs larger than L2: %.0f MB of compressed expert weights streamed per step"
-                         % (3 * active * f * d * BYTES_PER_ELEM / 1e6),
+                         % (3 * (active + NS) * f * d * BYTES_PER_ELEM / 1e6),
                    "weights": "random-init (counter-based synthetic), magnitude-pruned to (1,2,32)",
                    "launch": "cuda graph of the K timed layer calls" if use_graph else "eager launches"},
         "layer_tflops": flops_layer / (ms * 1e-3) / 1e12,
-        "phases_ms": {"route_compact": ph_ms[0], "zero_out": ph_ms[1], "gate_up_ssmm": ph_ms[2],
-                      "down_ssmm": ph_ms[3]},
+        "phases_ms": dict({"route_compact": ph_ms[0], "zero_out": ph_ms[1], "gate_up_ssmm": ph_ms[2],
+                           "down_ssmm": ph_ms[3]}, **({"shared_experts": ph_ms[4]} if NS else {})),
         "down_ssmm_tflops": (flops_gu / 2) / (ph_ms[3] * 1e-3) / 1e12,
         "roofline": roof,
         "e2e": {"value": T * world / (ms_e2e * 1e-3), "unit": "tokens/s",
@@ -582,6 +588,8 @@ def main():
     ap.add_argument("--parallel", default="ep", choices=["ep", "dp"], help="N>1: expert (default) or data parallel")
     ap.add_argument("--ep-transport", default="peer", choices=["peer", "nccl"],
                     help="EP token/output transport: NVLink peer memory in the kernels (default) or NCCL all_to_all_v")
+    ap.add_argument("--shared", type=int, default=0,
+                    help="shared experts (every token, weight 1) after the routed ones, e.g. 2 for DeepSeek-MoE")
     ap.add_argument("--decode-tokens", type=int, default=64, help="extra decode point on the same layer (0: off)")
     args = ap.parse_args()
     set_format(args.format)
