@@ -452,9 +452,10 @@ def run_ours(args):
         cnt = cnt[rank * el:(rank + 1) * el]
     else:
         cnt = cnt // max(world, 1) if world > 1 else cnt
-    Tk = int(cnt.sum())                      # (token, expert) pairs this GPU's gate/up SSMM processed
+    Tk = int(cnt.sum()) + NS * T             # (token, expert) pairs this GPU's gate/up SSMM processed
+    #                                          (shared experts run as groups of the same launches)
     flops_gu = 2 * 2 * (f // 2) * d * Tk     # 2 weights x 2 * (f*N/M) * d * tokens
-    active = int((cnt > 0).sum())
+    active = int((cnt > 0).sum()) + NS
     bytes_gu = (2 * active * f * d * BYTES_PER_ELEM + Tk * d * 2 + Tk * 4 + Tk * f * 2)
     t_gu = ph_ms[2] * 1e-3
     ach_tf = flops_gu / t_gu / 1e12
@@ -472,7 +473,7 @@ def run_ours(args):
                  "algorithmic_flops": flops_gu, "algorithmic_bytes": bytes_gu,
                  "other_view": ({"achieved_gbs": ach_gbs, "hbm_frac": ach_gbs / hbm} if tensor_bound else
                                 {"achieved_tflops": ach_tf, "sparse_frac": ach_tf / sparse_peak})})
-    flops_layer = 3 * flops_gu / 2 + NS * 3 * 2 * (f // 2) * d * T   # + shared experts (all T tokens each)
+    flops_layer = 3 * flops_gu / 2
     line = {
         "metric": "moe_layer_tokens_per_s", "value": T * world / (ms * 1e-3), "unit": "tokens/s",
         "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -485,12 +486,12 @@ def run_ours(args):
                                     f"ep{world} (experts sharded, NCCL all_to_all_v dispatch/combine)") if ep
                                    else f"dp{world} (experts replicated per GPU)"),
                    "l2": "inputs larger than L2: %.0f MB of compressed expert weights streamed per step"
-                         % (3 * (active + NS) * f * d * BYTES_PER_ELEM / 1e6),
+                         % (3 * active * f * d * BYTES_PER_ELEM / 1e6),
                    "weights": "random-init (counter-based synthetic), magnitude-pruned to (1,2,32)",
                    "launch": "cuda graph of the K timed layer calls" if use_graph else "eager launches"},
         "layer_tflops": flops_layer / (ms * 1e-3) / 1e12,
-        "phases_ms": dict({"route_compact": ph_ms[0], "zero_out": ph_ms[1], "gate_up_ssmm": ph_ms[2],
-                           "down_ssmm": ph_ms[3]}, **({"shared_experts": ph_ms[4]} if NS else {})),
+        "phases_ms": {"route_compact": ph_ms[0], "zero_out": ph_ms[1], "gate_up_ssmm": ph_ms[2],
+                      "down_ssmm": ph_ms[3]},
         "down_ssmm_tflops": (flops_gu / 2) / (ph_ms[3] * 1e-3) / 1e12,
         "roofline": roof,
         "e2e": {"value": T * world / (ms_e2e * 1e-3), "unit": "tokens/s",

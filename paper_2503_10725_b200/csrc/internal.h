@@ -105,7 +105,7 @@ bool ssmm_pair_images_ok(const smy_weight* const* w0, const smy_weight* const* w
 smy_status route_launch(const float* logits, int64_t T, int E, int k, int gating, int32_t* ids, float* w,
                         int32_t* counts, int32_t* offsets, int32_t* sel, float* gw, void* ws, size_t ws_bytes,
                         const int* tile_nt, const int* tile_mt, int n_tile_cfgs, int32_t* tile_prefix,
-                        cudaStream_t s);
+                        cudaStream_t s, int num_shared = 0);
 size_t route_ws_bytes(int64_t T, int E);
 smy_status compact_launch(const int32_t* keys, const float* vals, int64_t T, int nb, int k, int32_t* counts,
                           int32_t* offsets, int32_t* sel, float* gw, void* ws, size_t ws_bytes, const int* tile_nt,

@@ -40,8 +40,10 @@ LayerWs carve(const smy_moe_config* c, int64_t T, bool fallback, uint8_t* base) 
     off = align_up(off + bytes, 256);
     return p;
   };
-  const int64_t Tk = T * c->top_k;
-  const int E = c->num_experts;
+  // shared experts are compacted and run as extra groups (k + ns entries per token)
+  const int ns = c->num_shared > 0 ? c->num_shared : 0;
+  const int64_t Tk = T * (c->top_k + ns);
+  const int E = c->num_experts + ns;
   w.ids = reinterpret_cast<int32_t*>(take(Tk * 4));
   w.w = reinterpret_cast<float*>(take(Tk * 4));
   w.counts = reinterpret_cast<int32_t*>(take(E * 4));
@@ -152,7 +154,13 @@ static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* 
 smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const smy_weight* shared, const void* x,
                     const float* logits, const int32_t* keys, const float* vals, int64_t T, float* out,
                     void* workspace, size_t ws_bytes, cudaStream_t s, const PeerRows* peers) {
-  const int E = c->num_experts, k = c->top_k, d = c->hidden, f = c->ffn;
+  const int d = c->hidden, f = c->ffn;
+  // shared experts (weight 1, every token -- reading R15): with router logits
+  // they are appended to every token's routing entries (route_launch), so the two
+  // grouped launches run them as groups E_r .. E_r + ns - 1 (SEL = all tokens)
+  const int nsh = (shared != nullptr && keys == nullptr && c->num_shared > 0) ? c->num_shared : 0;
+  const int Er = c->num_experts, kr = c->top_k;
+  const int E = Er + nsh, k = kr + nsh;
   // interleaved: experts[3e] is the [2f x d] gate/up weight (reading R20), experts[3e+1] unused
   const bool ilv = interleaved(c);
   smy_wdesc dgu{ilv ? 2 * f : f, d, c->fmt}, ddn{d, f, c->fmt};
@@ -166,7 +174,7 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   LayerWs w = carve(c, T, !fused, static_cast<uint8_t*>(workspace));
   if (w.total > ws_bytes) return SMY_E_WORKSPACE;
 
-  const int64_t tpg = E ? (T * k + E - 1) / E : 0;
+  const int64_t tpg = Er ? (T * kr + Er - 1) / Er : 0;  // routed tokens per expert
   // tile width: the mean tokens per expert + 3 sigma of the (binomial) spread, so a
   // decode-sized expert rarely needs a second n-tile (which would re-stream its weights
   // through the SMs); ragged tiles issue MMAs of their own width
@@ -181,9 +189,10 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   const smy_weight* wu[kMaxGroups];
   const smy_weight* wd[kMaxGroups];
   for (int e = 0; e < E; ++e) {
-    wg[e] = &experts[3 * e + 0];
-    wu[e] = &experts[3 * e + 1];
-    wd[e] = &experts[3 * e + 2];
+    const smy_weight* t3 = e < Er ? &experts[3 * e] : &shared[3 * (e - Er)];
+    wg[e] = &t3[0];
+    wu[e] = &t3[1];
+    wd[e] = &t3[2];
   }
   const size_t img_gu = (size_t)ggu.m_tiles * ggu.k_stages * ggu.block;
   const size_t img_dn = (size_t)gdn.m_tiles * gdn.k_stages * gdn.block;
@@ -201,8 +210,8 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
 
   record_phase(0, s);
   if (keys == nullptr)
-    st = route_launch(logits, T, E, k, c->gating, w.ids, w.w, w.counts, w.offsets, w.sel, w.gw, w.route_ws,
-                      w.route_ws_bytes, nts, mts, 2, w.prefix, s);
+    st = route_launch(logits, T, Er, kr, c->gating, w.ids, w.w, w.counts, w.offsets, w.sel, w.gw, w.route_ws,
+                      w.route_ws_bytes, nts, mts, 2, w.prefix, s, nsh);
   else
     st = compact_launch(keys, vals, T, E, k, w.counts, w.offsets, w.sel, w.gw, w.route_ws, w.route_ws_bytes, nts,
                         mts, 2, w.prefix, s);
@@ -248,7 +257,8 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   record_phase(4, s);
 
   // shared experts: every token, weight 1 (reading R15)
-  for (int i = 0; shared && i < c->num_shared; ++i) {
+  // (the expert-parallel receive side, whose routing arrives as keys, runs them here)
+  for (int i = 0; shared && nsh == 0 && i < c->num_shared; ++i) {
     const smy_weight* sg[1] = {&shared[3 * i + 0]};
     const smy_weight* su[1] = {&shared[3 * i + 1]};
     const smy_weight* sd[1] = {&shared[3 * i + 2]};

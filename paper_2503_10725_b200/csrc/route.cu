@@ -11,7 +11,7 @@ namespace smy {
 
 constexpr int kRouteThreads = 256;  // tokens per block
 constexpr int kRouteWarps = kRouteThreads / 32;
-constexpr int kMaxK = 8;
+constexpr int kMaxK = 16;  // top-k plus appended shared experts
 constexpr int kMaxE = 256;
 
 // One warp per token: lane l holds logits l, l+32, ... (coalesced).  Each
@@ -67,12 +67,20 @@ __device__ __forceinline__ void topk_warp(const float* __restrict__ lg, int E, i
   }
 }
 
+// Writes the token's k routed entries, then its ns shared-expert entries (ids E..E+ns-1,
+// weight 1: every token passes through every shared expert; reading R15) --
+// the compaction then gives each shared expert a SEL of all tokens, so the grouped
+// SSMM launches run shared and routed experts together.
 __device__ __forceinline__ void topk_token(const float* __restrict__ lg, int E, int k, int gating, int lane,
-                                           int32_t* __restrict__ ids, float* __restrict__ w) {
+                                           int32_t* __restrict__ ids, float* __restrict__ w, int ns = 0) {
   if (E <= 32) topk_warp<1>(lg, E, k, gating, lane, ids, w);
   else if (E <= 64) topk_warp<2>(lg, E, k, gating, lane, ids, w);
   else if (E <= 128) topk_warp<4>(lg, E, k, gating, lane, ids, w);
   else topk_warp<8>(lg, E, k, gating, lane, ids, w);
+  if (lane < ns) {
+    ids[k + lane] = E + lane;
+    w[k + lane] = 1.f;
+  }
 }
 
 // Build per-warp expert masks for this block's tokens (from ids).
@@ -140,11 +148,12 @@ __device__ __forceinline__ void scan_experts(const int32_t* __restrict__ cnt, in
 
 // One warp per token over the whole grid (8 tokens per 256-thread block).
 __global__ void route_topk_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int gating,
-                                  int32_t* __restrict__ ids, float* __restrict__ w) {
+                                  int32_t* __restrict__ ids, float* __restrict__ w, int ns) {
   const int lane = threadIdx.x % 32;
   const int64_t t = (int64_t)blockIdx.x * kRouteWarps + threadIdx.x / 32;
   if (t >= T) return;
-  topk_token(logits + t * E, E, k, gating, lane, ids + t * k, w + t * k);
+  const int kk = k + ns;  // row stride: routed entries, then shared
+  topk_token(logits + t * E, E, k, gating, lane, ids + t * kk, w + t * kk, ns);
 }
 
 __global__ void route_count_kernel(const int32_t* __restrict__ ids, int64_t T, int E, int k,
@@ -160,7 +169,7 @@ __global__ void route_count_kernel(const int32_t* __restrict__ ids, int64_t T, i
 
 // T <= kRouteThreads: the whole routing + compaction in one block / one launch
 // (top-k, masks, counts, offsets, tile prefixes, scatter).
-__global__ void route_small_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int gating,
+__global__ void route_small_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int ns, int gating,
                                    int32_t* __restrict__ ids, float* __restrict__ w, int32_t* __restrict__ counts,
                                    int32_t* __restrict__ offsets, int nt0, int mt0, int32_t* __restrict__ prefix0,
                                    int nt1, int mt1, int32_t* __restrict__ prefix1, int32_t* __restrict__ sel,
@@ -169,8 +178,10 @@ __global__ void route_small_kernel(const float* __restrict__ logits, int64_t T, 
   __shared__ int32_t wbase[kRouteWarps][kMaxE];
   const int wp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (logits != nullptr) {
+    // E, k here include the ns shared experts; the router covers the first E - ns
     for (int t = wp; t < T; t += kRouteWarps)
-      topk_token(logits + (int64_t)t * E, E, k, gating, lane, ids + (int64_t)t * k, w + (int64_t)t * k);
+      topk_token(logits + (int64_t)t * (E - ns), E - ns, k - ns, gating, lane, ids + (int64_t)t * k,
+                 w + (int64_t)t * k, ns);
   }
   __syncthreads();
   build_masks(ids, T, E, k, mask);
@@ -274,14 +285,20 @@ smy_status compact_launch(const int32_t* keys, const float* vals, int64_t T, int
                           int32_t* offsets, int32_t* sel, float* gw, void* ws, size_t ws_bytes, const int* tile_nt,
                           const int* tile_mt, int n_tile_cfgs, int32_t* tile_prefix, cudaStream_t s) {
   return route_launch(nullptr, T, nb, k, 0, const_cast<int32_t*>(keys), const_cast<float*>(vals), counts, offsets, sel,
-                      gw, ws, ws_bytes, tile_nt, tile_mt, n_tile_cfgs, tile_prefix, s);
+                      gw, ws, ws_bytes, tile_nt, tile_mt, n_tile_cfgs, tile_prefix, s, 0);
 }
 
 smy_status route_launch(const float* logits, int64_t T, int E, int k, int gating, int32_t* ids, float* w,
                         int32_t* counts, int32_t* offsets, int32_t* sel, float* gw, void* ws, size_t ws_bytes,
                         const int* tile_nt, const int* tile_mt, int n_tile_cfgs, int32_t* tile_prefix,
-                        cudaStream_t s) {
-  if (E > kMaxE || k > kMaxK || k < 1 || (logits != nullptr && k > E)) return SMY_E_CONFIG;
+                        cudaStream_t s, int ns) {
+  // routed experts E, k; with ns shared experts appended the compaction runs over
+  // E + ns buckets and k + ns entries per token (ids / w rows of stride k + ns)
+  if (ns < 0 || ns > 32 || (ns > 0 && logits == nullptr)) return SMY_E_CONFIG;
+  if (E + ns > kMaxE || k + ns > kMaxK || k < 1 || (logits != nullptr && k > E)) return SMY_E_CONFIG;
+  const int Er = E, kr = k;
+  E += ns;
+  k += ns;
   if (ws_bytes < route_ws_bytes(T, E)) return SMY_E_WORKSPACE;
   const int nblk = (int)((T + kRouteThreads - 1) / kRouteThreads);
   int32_t* blk_counts = static_cast<int32_t*>(ws);
@@ -295,18 +312,18 @@ smy_status route_launch(const float* logits, int64_t T, int E, int k, int gating
     // top-k launch first (one warp per token) so the block only compacts
     const bool fused_topk = T <= 4 * kRouteWarps;  // (16 per warp measured slower than two launches)
     if (logits != nullptr && !fused_topk) {
-      route_topk_kernel<<<(unsigned)((T + kRouteWarps - 1) / kRouteWarps), kRouteThreads, 0, s>>>(logits, T, E, k,
-                                                                                                 gating, ids, w);
+      route_topk_kernel<<<(unsigned)((T + kRouteWarps - 1) / kRouteWarps), kRouteThreads, 0, s>>>(logits, T, Er, kr,
+                                                                                                 gating, ids, w, ns);
       count_launch();
     }
-    route_small_kernel<<<1, kRouteThreads, 0, s>>>(fused_topk ? logits : nullptr, T, E, k, gating, ids, w, counts,
+    route_small_kernel<<<1, kRouteThreads, 0, s>>>(fused_topk ? logits : nullptr, T, E, k, ns, gating, ids, w, counts,
                                                    offsets, nt0, mt0, pre0, nt1, mt1, pre1, sel, gw);
     count_launch();
     return cuda_status(cudaGetLastError());
   }
   if (logits != nullptr) {
-    route_topk_kernel<<<(unsigned)((T + kRouteWarps - 1) / kRouteWarps), kRouteThreads, 0, s>>>(logits, T, E, k,
-                                                                                               gating, ids, w);
+    route_topk_kernel<<<(unsigned)((T + kRouteWarps - 1) / kRouteWarps), kRouteThreads, 0, s>>>(logits, T, Er, kr,
+                                                                                               gating, ids, w, ns);
     count_launch();
   }
   route_count_kernel<<<nblk, kRouteThreads, 0, s>>>(ids, T, E, k, blk_counts);

@@ -373,7 +373,12 @@ def _layer_case(smy, fmt, E, d, f, T, k, gating="renorm_topk", shared=0, skew=0.
     dict(fmt=F.SparseFormat(2, 2, 32), E=4, d=256, f=512, T=400, k=2),                   # plain 2:4, pair kernels
     dict(fmt=F.SparseFormat(1, 2, 32), E=16, d=256, f=384, T=57, k=6, gating="softmax_all", shared=2,
          gate_up="separate"),
-], ids=lambda c: f"{c['fmt']}-E{c['E']}-T{c['T']}-{c.get('gate_up', 'auto')}-{c.get('transcode', 'auto')}")
+    # shared experts folded into the grouped launches: top-k fused into the one-block
+    # routing (T <= 32), and k + shared = 9 entries per token (Qwen2-like top-8 + 1)
+    dict(fmt=F.SparseFormat(1, 2, 32), E=16, d=256, f=384, T=20, k=8, gating="softmax_all", shared=1),
+    dict(fmt=F.SparseFormat(1, 2, 32), E=16, d=256, f=384, T=300, k=8, gating="softmax_all", shared=1),
+], ids=lambda c: (f"{c['fmt']}-E{c['E']}-T{c['T']}-{c.get('gate_up', 'auto')}-{c.get('transcode', 'auto')}"
+                  f"-sh{c.get('shared', 0)}"))
 def test_moe_layer_parity(smy, case):
     case = dict(case)
     fmt = case.pop("fmt")
@@ -389,7 +394,8 @@ def test_moe_layer_parity(smy, case):
     dict(E=4, d=256, f=640, T=400, k=2),                       # interleaved gate/up: 5 m-tiles (odd pair count)
     dict(E=4, d=512, f=512, T=512, k=2, gate_up="separate"),   # two-weight gate/up pair kernel
     dict(E=2, d=512, f=1024, T=300, k=2, skew=2.0, gate_up="separate"),
-], ids=lambda c: f"E{c['E']}-d{c['d']}-f{c['f']}-T{c['T']}-{c.get('gate_up', 'auto')}")
+    dict(E=4, d=512, f=512, T=512, k=2, shared=2),             # shared experts as groups of the pair launches
+], ids=lambda c: f"E{c['E']}-d{c['d']}-f{c['f']}-T{c['T']}-{c.get('gate_up', 'auto')}-sh{c.get('shared', 0)}")
 def test_moe_layer_prefill_pair_kernels(smy, case):
     case = dict(case)
     got, ref, S = _layer_case(smy, F.SparseFormat(1, 2, 32), **case)
