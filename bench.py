@@ -311,10 +311,13 @@ def run_ours(args):
     # host) and replay it as the timed region: identical kernels, no launch gaps.
     use_graph = not args.no_graph and not ep
 
-    def make_runner(xx, lgg, oo, hs):
+    def make_runner(xx, lgg, oo, hs, n):
+        # hs: per-step phase-event arrays, or None for the clean steps that are timed
+        # (each event-record node costs ~2.7 us inside the graph -- the empty
+        # "zero_out" interval measures it -- so step times come from clean replays)
         def eager():
-            for h in hs:
-                lib.smy_moe_set_phase_events(h, 6)
+            for i in range(n):
+                lib.smy_moe_set_phase_events(hs[i] if hs is not None else None, 6 if hs is not None else 0)
                 layer(xx, lgg, oo)
             lib.smy_moe_set_phase_events(None, 0)
         if not use_graph:
@@ -328,7 +331,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         return g.replay, n
 
-    run, graph_launches = make_runner(x, lg, out, handles)
+    run, graph_launches = make_runner(x, lg, out, None, K)
+    run_ph, _ = make_runner(x, lg, out, handles, K)
     clocks = ClockSampler(local)
     clocks.start()
     barrier()
@@ -345,6 +349,10 @@ def run_ours(args):
     launches = graph_launches if graph_launches is not None else lib.smy_launch_count() - launches0
     clk = clocks.stop(t_wall0, t_wall1)
     ms = ev0.elapsed_time(ev1) / K
+    # per-phase times (the roofline's kernel time): a second replay of the same steps
+    # recording the layer's phase events; outside the timed region
+    run_ph()
+    torch.cuda.synchronize()
     ph = np.array([[phase[s][i].elapsed_time(phase[s][i + 1]) for i in range(5)] for s in range(K)])
     ph_ms = ph.mean(0)
     if world > 1:
@@ -367,13 +375,16 @@ def run_ours(args):
                 ev.record(stream)
         torch.cuda.synchronize()
         dh = [C_void_p_array(ev) for ev in dph]
-        drun, _ = make_runner(xd, lgd, outd, dh)
+        drun, _ = make_runner(xd, lgd, outd, None, Kd)
+        drun_ph, _ = make_runner(xd, lgd, outd, dh, Kd)
         d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         d0.record(stream)
         drun()
         d1.record(stream)
         torch.cuda.synchronize()
         dms = d0.elapsed_time(d1) / Kd
+        drun_ph()
+        torch.cuda.synchronize()
         dpm = np.array([[dph[s][i].elapsed_time(dph[s][i + 1]) for i in range(5)] for s in range(Kd)]).mean(0)
         ids_d = P.route(lgd, k, gating)[0].flatten().long()
         act_d = int((torch.bincount(ids_d, minlength=E) > 0).sum().item())
@@ -488,7 +499,8 @@ def run_ours(args):
                    "l2": "inputs larger than L2: %.0f MB of compressed expert weights streamed per step"
                          % (3 * active * f * d * BYTES_PER_ELEM / 1e6),
                    "weights": "random-init (counter-based synthetic), magnitude-pruned to (1,2,32)",
-                   "launch": "cuda graph of the K timed layer calls" if use_graph else "eager launches"},
+                   "launch": ("cuda graph of the K timed layer calls (no phase-event nodes inside; per-phase "
+                              "times from a second replay that records them)") if use_graph else "eager launches"},
         "layer_tflops": flops_layer / (ms * 1e-3) / 1e12,
         "phases_ms": {"route_compact": ph_ms[0], "zero_out": ph_ms[1], "gate_up_ssmm": ph_ms[2],
                       "down_ssmm": ph_ms[3]},
