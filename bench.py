@@ -537,7 +537,7 @@ def gate_up_kernel(tokens_per_expert, f):
     ssmm.cu: ssmm_pick_nt, ssmm_pair_cluster) -- the key into the ncu summary."""
     nt = nt_pick(tokens_per_expert)
     if tokens_per_expert >= 64 and nt in (128, 224):
-        return "ssmm_pair_kernel<%d, 1, 2>" % nt
+        return "ssmm_pair_kernel<%d, 1, 2, 1>" % nt   # <NT, NW, MS, SPLIT>: SEL-gather launches split rings
     return "ssmm_kernel<%d, 1, 2, 1>" % nt
 
 

@@ -180,7 +180,10 @@ SMY_API smy_status samoyeds_route(const float* logits, int64_t T, int32_t E, int
  * cfg->gate_up == SMY_GU_SEPARATE, or (gu, unused, down) when SMY_GU_INTERLEAVED
  * (gu from samoyeds_interleave_gate_up; format (1,2,V), V % 32 == 0 -- the
  * prefill kernels read one 128-lane tile of gate+up rows per MMA); shared: host
- * array [num_shared][3] in the same layout, or NULL.  x dev bf16 [T x hidden]; logits dev fp32
+ * array [num_shared][3] in the same layout, or NULL (num_shared + top_k <= 16,
+ * num_experts + num_shared <= 128); the shared experts run as extra groups of the
+ * same two grouped SSMM launches (the routing appends ids E.. with weight 1 to
+ * every token).  x dev bf16 [T x hidden]; logits dev fp32
  * [T x E]; out dev fp32 [T x hidden] (overwritten).  The gate/up -> down
  * intermediate is bf16 (reading R12).                                     */
 #define SMY_GU_SEPARATE 0
