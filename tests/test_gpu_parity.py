@@ -415,29 +415,33 @@ def _prune_rows(w_bits, fmt, chunk=512):
     return np.concatenate([F.prune(w_bits[i:i + chunk], fmt) for i in range(0, w_bits.shape[0], chunk)])
 
 
-@pytest.mark.parametrize("model,T", [("mixtral", 4096), ("mixtral", 64), ("deepseek", 4096), ("qwen2", 4096),
-                                     ("qwen2", 64)])
-def test_moe_layer_full_size_sampled(smy, model, T):
+@pytest.mark.parametrize("model,T,NS", [("mixtral", 4096, 0), ("mixtral", 64, 0), ("deepseek", 4096, 0),
+                                        ("deepseek", 4096, 2), ("deepseek", 64, 2), ("qwen2", 4096, 0),
+                                        ("qwen2", 64, 0)])
+def test_moe_layer_full_size_sampled(smy, model, T, NS):
     """The bench's workloads themselves -- Mixtral-8x7B / DeepSeek-MoE-16B /
     Qwen2-57B-A14B layers at T=4096 (interleaved gate/up + stream-K down on CTA
     pairs) and T=64 decode points (single-CTA kernels), built by
     bench.build_layer -- checked against the fp64 oracle on sampled outputs:
     every token routed to the most common expert set (up to 6 of them), 24
     sampled output row pairs.  The oracle regenerates the weights it needs by
-    index (counter-based generator) and prunes them itself."""
+    index (counter-based generator) and prunes them itself.  NS > 0: the layer
+    also runs NS shared experts (bench.py --shared; every token, weight 1), drawn
+    like routed experts E, E+1, ..."""
     import bench
     d, f, E, k, gating = bench.MODELS[model]
     fmt = F.SparseFormat(1, 2, 32)
     dev = torch.device("cuda")
-    layer = smy.MoELayer(smy.MoEConfig(E, k, d, f, 0, gating, smy.Format(1, 2, 32)),
-                         bench.build_layer(smy, model, dev), max_tokens=T, device=dev)
+    shared = bench.build_layer(smy, model, dev, experts=range(E, E + NS)) if NS else ()
+    layer = smy.MoELayer(smy.MoEConfig(E, k, d, f, NS, gating, smy.Format(1, 2, 32)),
+                         bench.build_layer(smy, model, dev), shared=shared, max_tokens=T, device=dev)
     x = torch.empty(T, d, dtype=torch.int16, device=dev)
     smy.synth_fill(x, synth.SEED_X, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
     lg = torch.empty(T, E, dtype=torch.float32, device=dev)
     smy.synth_fill(lg, synth.SEED_LOGITS, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
     out = layer(x, lg).cpu().numpy().astype(np.float64)
     xh, lgh = host16(x), lg.cpu().numpy()
-    del layer
+    del layer, shared
     torch.cuda.empty_cache()
 
     ids, gw = moe.route(lgh, k, moe.SOFTMAX_ALL if gating == "softmax_all" else moe.RENORM_TOPK)
@@ -456,14 +460,16 @@ def test_moe_layer_full_size_sampled(smy, model, T):
 
     ref = np.zeros((len(toks), len(orow)))
     S = np.zeros_like(ref)
-    for e in pair:
+    for e in list(pair) + list(range(E, E + NS)):
         wg = bf16.to_f64(_prune_rows(dense(synth.weight_seed(e, 0), f, d), fmt))
         wu = bf16.to_f64(_prune_rows(dense(synth.weight_seed(e, 1), f, d), fmt))
         a = bf16.to_f64(OS.silu_mul_bf16(xs @ wg.T, xs @ wu.T))             # [toks x f] bf16 intermediate
         del wg, wu
         wd = np.concatenate([dense(synth.weight_seed(e, 2), 2, f, idx0=int(2 * g) * f) for g in np.sort(groups)])
         wd = bf16.to_f64(F.prune(wd, fmt))                                    # rows orow
-        g_e = np.array([gw[t][list(ids[t]).index(e)] for t in toks])[:, None]
+        g_e = (np.array([gw[t][list(ids[t]).index(e)] for t in toks])[:, None] if e < E
+               else np.ones((len(toks), 1)))                                 # shared expert: weight 1
         ref += g_e * (a @ wd.T)
         S += np.abs(g_e) * (np.abs(a) @ np.abs(wd).T)
-    check_tol(out[np.ix_(toks, orow)], ref, S, f"{model} T={T} layer, tokens {toks.tolist()} (experts {pair})")
+    check_tol(out[np.ix_(toks, orow)], ref, S,
+              f"{model} T={T} layer (+{NS} shared), tokens {toks.tolist()} (experts {pair})")
