@@ -351,6 +351,8 @@ smy_status samoyeds_moe_layer(const smy_moe_config* cfg, const smy_weight* exper
   if (cfg->num_experts < 1 || cfg->top_k < 1 || cfg->top_k > cfg->num_experts || cfg->top_k > 8 ||
       cfg->num_experts > kMaxGroups || cfg->num_shared < 0 || (cfg->num_shared > 0 && !shared))
     return SMY_E_CONFIG;
+  // shared experts run as extra groups with extra routing entries per token
+  if (cfg->num_experts + cfg->num_shared > kMaxGroups || cfg->top_k + cfg->num_shared > 16) return SMY_E_CONFIG;
   if (cfg->hidden % 128 || cfg->ffn % 128) return SMY_E_SHAPE;
   smy_status st;
   if (comm != nullptr) {  // expert parallelism: experts = this rank's E / world (NCCL transport)

@@ -66,6 +66,21 @@ def test_host_validation_without_gpu(lib):
     assert lib.smy_route_workspace_bytes(4096, 64, C.byref(b)) == 0 and b.value > 0
 
 
+def test_moe_layer_shared_expert_limits_without_gpu(lib):
+    """samoyeds_moe_layer validates on the host, before any device work: shared
+    experts become extra groups (E + shared <= 128) and extra routing entries per
+    token (top_k + shared <= 16) -- include/samoyeds.h."""
+    from paper_2503_10725_b200 import MoEConfig, Format
+    from paper_2503_10725_b200._lib import smy_weight
+    ws = (smy_weight * 2)()
+    dummy = (C.c_uint8 * 16)()
+    p = C.cast(dummy, C.c_void_p)
+    for E, k, ns in ((127, 2, 2), (64, 8, 9)):
+        cfg = MoEConfig(E, k, 256, 256, ns, fmt=Format(1, 2, 32)).c()
+        st = lib.samoyeds_moe_layer(C.byref(cfg), ws, ws, p, p, 16, p, p, 16, None, None)
+        assert st == 3, (E, k, ns, st)   # SMY_E_CONFIG
+
+
 def test_moe_workspace_query(lib):
     from paper_2503_10725_b200 import MoEConfig, Format
     from paper_2503_10725_b200._lib import check
