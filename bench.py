@@ -387,9 +387,10 @@ def run_ours(args):
         torch.cuda.synchronize()
         dpm = np.array([[dph[s][i].elapsed_time(dph[s][i + 1]) for i in range(5)] for s in range(Kd)]).mean(0)
         ids_d = P.route(lgd, k, gating)[0].flatten().long()
-        act_d = int((torch.bincount(ids_d, minlength=E) > 0).sum().item())
-        gu_bytes = 2 * act_d * f * d * BYTES_PER_ELEM + Td * k * d * 2 + Td * k * 4 + Td * k * f * 2
-        dn_bytes = act_d * f * d * BYTES_PER_ELEM + Td * k * f * 2 + Td * k * 8 + Td * k * d * 4
+        act_d = int((torch.bincount(ids_d, minlength=E) > 0).sum().item()) + NS   # + shared experts
+        kd = k + NS                                   # rows per token through the grouped launches
+        gu_bytes = 2 * act_d * f * d * BYTES_PER_ELEM + Td * kd * d * 2 + Td * kd * 4 + Td * kd * f * 2
+        dn_bytes = act_d * f * d * BYTES_PER_ELEM + Td * kd * f * 2 + Td * kd * 8 + Td * kd * d * 4
         hbm_, _, _, _ = peaks()
         dec = {"tokens_per_gpu": Td, "tokens_per_s": Td * world / (dms * 1e-3), "ms_per_step": dms,
                "phases_ms": {"route_compact": dpm[0], "zero_out": dpm[1], "gate_up_ssmm": dpm[2], "down_ssmm": dpm[3]},
