@@ -275,12 +275,33 @@ SMY_API smy_status samoyeds_moe_experts_peer(const smy_moe_config* cfg, const sm
                                              int64_t ldo, int64_t rows, const int32_t* row_map, const int32_t* keys,
                                              const float* vals, void* workspace, size_t ws_bytes, void* stream);
 
+/* smy_moe_workspace_view: where a single-GPU samoyeds_moe_layer call over T
+ * tokens (same cfg, same workspace) leaves its routing result and its
+ * gate/up -> down intermediate, for inspection after the call (tests compare the
+ * compact bf16 intermediate with the oracle at full size).  Pure pointer
+ * arithmetic on `workspace`, no device access.  groups = num_experts +
+ * num_shared; counts dev i32 [groups], offsets dev i32 [groups+1] (exclusive
+ * scan), sel dev i32 [T*(top_k+num_shared)] (expert-major, ascending token ids
+ * within an expert: the SEL arrays of P:303), gw dev fp32 aligned with sel;
+ * inter dev bf16 [inter_rows x ffn], row i = the intermediate of (expert, token
+ * sel[i]) -- the compressed output layout of P:374 (rows past offsets[groups]
+ * are unused).                                                            */
+typedef struct {
+  int32_t *counts, *offsets, *sel;
+  float* gw;
+  void* inter;
+  int64_t inter_rows;
+  int32_t groups;
+} smy_moe_view;
+SMY_API smy_status smy_moe_workspace_view(const smy_moe_config* cfg, int64_t T, void* workspace, size_t ws_bytes,
+                                          smy_moe_view* view);
+
 /* ------------------------------------------------------------ diagnostics
  * smy_moe_set_phase_events: when events != NULL (n >= 6 cudaEvent_t handles,
  * passed as void*), samoyeds_moe_layer records events[0..5] on its stream at
  * its phase boundaries: start | routing done | out zeroed | gate/up SSMM done |
- * down SSMM done | shared experts done.  NULL disables.  Process-global, not
- * thread-safe; used by bench.py to time the dominant kernel inside the timed
+ * down SSMM done | shared experts done.  NULL disables.  Per calling thread
+ * (thread-local); used by bench.py to time the dominant kernel inside the timed
  * region.  smy_launch_count: number of kernels this library has launched.  */
 SMY_API smy_status smy_moe_set_phase_events(void** events, int n);
 SMY_API uint64_t smy_launch_count(void);

@@ -36,6 +36,11 @@ class smy_moe_config(C.Structure):
                 ("num_shared", C.c_int32), ("gating", C.c_int32), ("fmt", smy_format), ("gate_up", C.c_int32)]
 
 
+class smy_moe_view(C.Structure):
+    _fields_ = [("counts", C.c_void_p), ("offsets", C.c_void_p), ("sel", C.c_void_p), ("gw", C.c_void_p),
+                ("inter", C.c_void_p), ("inter_rows", C.c_int64), ("groups", C.c_int32)]
+
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "smy_status_str": (C.c_char_p, [C.c_int]),
@@ -79,6 +84,8 @@ SIGNATURES = {
     "smy_ep_comm_destroy": (C.c_int, [C.c_void_p]),
     "smy_moe_ep_workspace_bytes": (C.c_int, [C.POINTER(smy_moe_config), C.c_int64, C.c_int32,
                                              C.POINTER(C.c_size_t)]),
+    "smy_moe_workspace_view": (C.c_int, [C.POINTER(smy_moe_config), C.c_int64, C.c_void_p, C.c_size_t,
+                                         C.POINTER(smy_moe_view)]),
     "smy_moe_set_phase_events": (C.c_int, [C.c_void_p, C.c_int]),
     "smy_launch_count": (C.c_uint64, []),
     "smy_debug_prof": (C.c_int, [C.c_void_p, C.c_int]),

@@ -311,6 +311,28 @@ class MoELayer:
                                      _stream(stream)), "samoyeds_moe_layer")
         return out
 
+    def view(self, T: int):
+        """smy_moe_workspace_view: the routing result and the compact bf16 gate/up
+        intermediate the last single-GPU call over T tokens left in the
+        workspace, as views of it: dict counts / offsets / sel / gw / inter
+        ([inter_rows x ffn], int16 bf16 bits)."""
+        if self.comm is not None:
+            raise ValueError("view() describes the single-GPU layer's workspace")
+        lib = _lib.load()
+        v = _lib.smy_moe_view()
+        check(lib.smy_moe_workspace_view(C.byref(self._cfg), T, _ptr(self.workspace), self.workspace.numel(),
+                                         C.byref(v)), "smy_moe_workspace_view")
+        base = self.workspace.data_ptr()
+
+        def at(ptr, n, dtype, esize):
+            off = ptr - base
+            return self.workspace[off:off + n * esize].view(dtype)
+
+        g, rows = v.groups, v.inter_rows
+        return {"counts": at(v.counts, g, torch.int32, 4), "offsets": at(v.offsets, g + 1, torch.int32, 4),
+                "sel": at(v.sel, rows, torch.int32, 4), "gw": at(v.gw, rows, torch.float32, 4),
+                "inter": at(v.inter, rows * self.cfg.ffn, torch.int16, 2).view(rows, self.cfg.ffn)}
+
 
 def synth_fill(out: torch.Tensor, seed: int, dist: int, scale: float, lo: int = -2, hi: int = 2,
                idx0: int = 0, stream=None) -> torch.Tensor:

@@ -12,8 +12,8 @@ namespace smy {
 
 static thread_local std::string g_last_error;
 static std::atomic<uint64_t> g_launches{0};
-static cudaEvent_t g_phase[6];
-static bool g_phase_on = false;
+static thread_local cudaEvent_t g_phase[6];
+static thread_local bool g_phase_on = false;
 
 int debug_flags() {
   static int v = -1;
@@ -110,6 +110,7 @@ smy_status synth_launch(uint64_t seed, int dist, float scale, int lo, int hi, in
 smy_status moe_workspace_bytes(const smy_moe_config* c, int64_t T, size_t* bytes);
 smy_status moe_layer(const smy_moe_config* c, const smy_weight* experts, const smy_weight* shared, const void* x,
                      const float* logits, int64_t T, float* out, void* workspace, size_t ws_bytes, cudaStream_t s);
+smy_status moe_view(const smy_moe_config* c, int64_t T, void* workspace, size_t ws_bytes, smy_moe_view* v);
 
 }  // namespace smy
 
@@ -372,6 +373,14 @@ smy_status samoyeds_moe_layer(const smy_moe_config* cfg, const smy_weight* exper
                    static_cast<cudaStream_t>(stream));
 }
 
+
+smy_status smy_moe_workspace_view(const smy_moe_config* cfg, int64_t T, void* workspace, size_t ws_bytes,
+                                  smy_moe_view* view) {
+  if (!cfg || !workspace || !view) return SMY_E_NULL;
+  if (T < 0) return SMY_E_SHAPE;
+  if (cfg->num_experts < 1 || cfg->top_k < 1 || cfg->num_shared < 0) return SMY_E_CONFIG;
+  return moe_view(cfg, T, workspace, ws_bytes, view);
+}
 
 smy_status smy_ep_plan_workspace_bytes(int64_t T, int32_t k, int32_t world, size_t* bytes) {
   if (!bytes) return SMY_E_NULL;

@@ -312,6 +312,25 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   return SMY_OK;
 }
 
+smy_status moe_view(const smy_moe_config* c, int64_t T, void* workspace, size_t ws_bytes, smy_moe_view* v) {
+  smy_wdesc dgu{interleaved(c) ? 2 * c->ffn : c->ffn, c->hidden, c->fmt};
+  Geometry ggu;
+  smy_status st = geometry(&dgu, &ggu);
+  if (st != SMY_OK) return st;
+  const bool fused = interleaved(c) || gate_up_fused(ggu);
+  LayerWs w = carve(c, T, !fused, static_cast<uint8_t*>(workspace));
+  if (w.total > ws_bytes) return SMY_E_WORKSPACE;
+  const int ns = c->num_shared > 0 ? c->num_shared : 0;
+  v->counts = w.counts;
+  v->offsets = w.offsets;
+  v->sel = w.sel;
+  v->gw = w.gw;
+  v->inter = w.inter;
+  v->inter_rows = T * (c->top_k + ns) > T ? T * (c->top_k + ns) : T;
+  v->groups = c->num_experts + ns;
+  return SMY_OK;
+}
+
 smy_status moe_layer(const smy_moe_config* c, const smy_weight* experts, const smy_weight* shared, const void* x,
                      const float* logits, int64_t T, float* out, void* workspace, size_t ws_bytes, cudaStream_t s) {
   return moe_core(c, experts, shared, x, logits, nullptr, nullptr, T, out, workspace, ws_bytes, s);

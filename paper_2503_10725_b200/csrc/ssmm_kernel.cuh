@@ -386,17 +386,17 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
         // the previous stage's MMAs may still be reading
         const uint32_t ecol = C::kECol + (it & 1) * 8 + 4 * mi;
         tc_cp_128x128b_elect(tm + ecol, desc_interleave(sbase + we * C::kWStride + kABytes));
-        // index bit-planes of this stage (this warp's weight), made explicitly warp-uniform
+        // index bit-planes of this stage (this warp's weight): LDS, no redux (see ssmm_pair.cuh)
         uint32_t pl[4][C::kPlanes > 0 ? C::kPlanes : 1][4];
 #pragma unroll
         for (int kb = 0; kb < 4; ++kb)
 #pragma unroll
           for (int b = 0; b < C::kPlanes; ++b) {
-            const uint4 v = *reinterpret_cast<const uint4*>(wsm(st, we) + kABytes + kEBytes + (kb * C::kPlanes + b) * 16);
-            pl[kb][b][0] = __reduce_or_sync(0xffffffffu, v.x);
-            pl[kb][b][1] = __reduce_or_sync(0xffffffffu, v.y);
-            pl[kb][b][2] = __reduce_or_sync(0xffffffffu, v.z);
-            pl[kb][b][3] = __reduce_or_sync(0xffffffffu, v.w);
+            const uint4 v = lds_v4(smem_u32(wsm(st, we)) + kABytes + kEBytes + (kb * C::kPlanes + b) * 16);
+            pl[kb][b][0] = v.x;
+            pl[kb][b][1] = v.y;
+            pl[kb][b][2] = v.z;
+            pl[kb][b][3] = v.w;
           }
 #pragma unroll
         for (int kb = 0; kb < 4; ++kb) {

@@ -378,19 +378,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           const uint32_t bbase = smem_base + SW * C::kWStage + sb * C::kBStage;
           const uint32_t ecol = C::kECol + (it & 1) * 8 + 4 * mi;
           tc_cp2_elect(tm + ecol, desc_interleave(sbase + w * C::kWStride + kABytes));
-          uint32_t pl[4][8];  // lane planes: words 0-3 this CTA's 128 lanes, 4-7 the peer's
+          // lane planes: words 0-3 this CTA's 128 lanes, 4-7 the peer's.  Plain LDS into
+          // registers (the same value in every lane); the masks reach the MMA through
+          // the elected lane's R2UR -- redux.sync per word made the issuer warp the
+          // bottleneck (probes/pair_mma_bench.cu: 122 vs 113 clk per MMA)
+          uint32_t pl[4][8];
 #pragma unroll
           for (int kb = 0; kb < 4 && MS == 2; ++kb) {
-            const uint4 v = *reinterpret_cast<const uint4*>(wsm(st, w) + kABytes + kEBytes + kb * 16);
-            const uint4 u = *reinterpret_cast<const uint4*>(psm(st) + 64 * w + kb * 16);
-            pl[kb][0] = __reduce_or_sync(0xffffffffu, v.x);
-            pl[kb][1] = __reduce_or_sync(0xffffffffu, v.y);
-            pl[kb][2] = __reduce_or_sync(0xffffffffu, v.z);
-            pl[kb][3] = __reduce_or_sync(0xffffffffu, v.w);
-            pl[kb][4] = __reduce_or_sync(0xffffffffu, u.x);
-            pl[kb][5] = __reduce_or_sync(0xffffffffu, u.y);
-            pl[kb][6] = __reduce_or_sync(0xffffffffu, u.z);
-            pl[kb][7] = __reduce_or_sync(0xffffffffu, u.w);
+            const uint4 v = lds_v4(sbase + w * C::kWStride + kABytes + kEBytes + kb * 16);
+            const uint4 u = lds_v4(sbase + NW * C::kWStride + 64 * w + kb * 16);
+            pl[kb][0] = v.x;
+            pl[kb][1] = v.y;
+            pl[kb][2] = v.z;
+            pl[kb][3] = v.w;
+            pl[kb][4] = u.x;
+            pl[kb][5] = u.y;
+            pl[kb][6] = u.z;
+            pl[kb][7] = u.w;
           }
 #pragma unroll
           for (int kb = 0; kb < 4; ++kb) {

@@ -45,6 +45,30 @@ def check_tol(got, ref, scale, what):
     assert not bad.any(), f"{what}: {bad.sum()} elements beyond 1e-2*sum|wx|, first at {np.argwhere(bad)[:3]}"
 
 
+def bf16_ulp(v):
+    """one bf16 ulp at |v| (8 significant bits); 0 at v = 0"""
+    a = np.abs(v)
+    e = np.floor(np.log2(np.where(a > 0, a, 1.0)))
+    return np.where(a > 0, np.exp2(e - 7), 0.0)
+
+
+def check_silu_mul(got, cg, cu, Sg, Su, what):
+    """The gate/up intermediate at the north-star bar against the oracle's bf16
+    output bf16(silu(C_g) * C_u) (P:337 fused activation, R12 bf16 intermediate):
+    rel Frobenius <= 1e-3 and EVERY element within one bf16 ulp (the two
+    roundings of the stored value) plus the 1e-2 * sum|w*x| bound on C_g / C_u
+    propagated through silu(g) * u: |silu'(g) u| * 1e-2 S_g + |silu(g)| * 1e-2 S_u."""
+    ref = bf16.to_f64(OS.silu_mul_bf16(cg, cu))
+    sig = 1.0 / (1.0 + np.exp(-cg))
+    dsilu = sig * (1.0 + cg * (1.0 - sig))
+    bound = (np.maximum(bf16_ulp(ref), bf16_ulp(got)) + ELEM * (np.abs(dsilu * cu) * Sg + np.abs(cg * sig) * Su)
+             + 1e-30)
+    rf = OS.rel_fro(got - ref, ref)
+    assert rf <= REL_FRO, f"{what}: rel Frobenius {rf:.3e} > {REL_FRO}"
+    bad = np.abs(got - ref) > bound
+    assert not bad.any(), f"{what}: {bad.sum()} of {bad.size} elements beyond the bound, first at {np.argwhere(bad)[:3]}"
+
+
 PARITY_FORMATS = [F.SparseFormat(1, 2, 32), F.SparseFormat(1, 2, 16), F.SparseFormat(4, 8, 32),
                   F.SparseFormat(8, 16, 32), F.SparseFormat(2, 2, 32), F.SparseFormat(1, 1, 32)]
 
@@ -201,14 +225,7 @@ def test_ssmm_silu_mul(smy, fmt):
     got = smy.ssmm(sg, dev16(x), torch.from_numpy(sel).cuda(), epi="silu_mul", w2=su)
     got = bf16.to_f64(host16(got.view(torch.int16)))
     cg, cu = OS.ssmm(eg, x, sel), OS.ssmm(eu, x, sel)
-    exact = cg / (1 + np.exp(-cg)) * cu
-    ref_bits = OS.silu_mul_bf16(cg, cu)
-    # within the bf16 rounding of the stored intermediate + fp32 accumulation
-    rf = OS.rel_fro(got - exact, exact)
-    assert rf <= 5e-3, rf
-    ulp = np.abs(bf16.to_f64(ref_bits)) * 2.0 ** -7 + 1e-30
-    mismatch = np.abs(got - bf16.to_f64(ref_bits)) > ulp
-    assert mismatch.mean() < 0.01, mismatch.mean()
+    check_silu_mul(got, cg, cu, OS.ssmm_abs(eg, x, sel), OS.ssmm_abs(eu, x, sel), f"silu_mul {fmt}")
 
 
 @pytest.mark.parametrize("fmt", [F.SparseFormat(1, 2, 32), F.SparseFormat(1, 2, 16), F.SparseFormat(4, 8, 32),
@@ -255,10 +272,8 @@ def test_ssmm_silu_mul_interleaved(smy, shape):
     got = bf16.to_f64(host16(got_t.view(torch.int16)))
     ref_bits = OS.silu_mul_interleaved_bf16(OS.ssmm(F.interleave_gate_up(eg, eu), x, sel))
     cg, cu = OS.ssmm(eg, x, sel), OS.ssmm(eu, x, sel)
-    exact = cg / (1 + np.exp(-cg)) * cu
-    assert OS.rel_fro(got - exact, exact) <= 5e-3
-    ulp = np.abs(bf16.to_f64(ref_bits)) * 2.0 ** -7 + 1e-30
-    assert (np.abs(got - bf16.to_f64(ref_bits)) > ulp).mean() < 0.01
+    assert np.array_equal(ref_bits, OS.silu_mul_bf16(cg, cu))
+    check_silu_mul(got, cg, cu, OS.ssmm_abs(eg, x, sel), OS.ssmm_abs(eu, x, sel), f"silu_mul_interleaved {shape}")
 
 
 @pytest.mark.parametrize("fmt", PARITY_FORMATS, ids=str)
@@ -415,6 +430,12 @@ def _prune_rows(w_bits, fmt, chunk=512):
     return np.concatenate([F.prune(w_bits[i:i + chunk], fmt) for i in range(0, w_bits.shape[0], chunk)])
 
 
+def _tile_positions(n):
+    """positions in an expert's SEL that fall in its first, a middle and its last
+    (ragged) token tile: the first two, the middle two and the last two rows"""
+    return sorted({p for p in (0, 1, n // 2, n // 2 + 1, n - 2, n - 1) if 0 <= p < n})
+
+
 @pytest.mark.parametrize("model,T,NS", [("mixtral", 4096, 0), ("mixtral", 64, 0), ("deepseek", 4096, 0),
                                         ("deepseek", 4096, 2), ("deepseek", 64, 2), ("qwen2", 4096, 0),
                                         ("qwen2", 64, 0)])
@@ -422,12 +443,19 @@ def test_moe_layer_full_size_sampled(smy, model, T, NS):
     """The bench's workloads themselves -- Mixtral-8x7B / DeepSeek-MoE-16B /
     Qwen2-57B-A14B layers at T=4096 (interleaved gate/up + stream-K down on CTA
     pairs) and T=64 decode points (single-CTA kernels), built by
-    bench.build_layer -- checked against the fp64 oracle on sampled outputs:
-    every token routed to the most common expert set (up to 6 of them), 24
-    sampled output row pairs.  The oracle regenerates the weights it needs by
-    index (counter-based generator) and prunes them itself.  NS > 0: the layer
-    also runs NS shared experts (bench.py --shared; every token, weight 1), drawn
-    like routed experts E, E+1, ..."""
+    bench.build_layer -- checked against the fp64 oracle on samples that cover
+    every part of the tile schedule: for 4 routed experts spread over the expert
+    range (+ every shared expert), the tokens at the first two, middle two and
+    last two positions of the expert's SEL (its first, a middle and its last,
+    ragged token tile -- and so the stream-K pieces of the down launch).
+      * gate/up intermediate: the layer's own compact bf16 buffer
+        (MoELayer.view) on 32 sampled channel pairs of those (expert, token)
+        rows, at the north-star bar (check_silu_mul);
+      * layer output: those tokens x 24 sampled output row pairs.
+    The oracle regenerates the weights it needs by index (counter-based
+    generator) and prunes them itself.  NS > 0: the layer also runs NS shared
+    experts (bench.py --shared; every token, weight 1), drawn like routed experts
+    E, E+1, ..."""
     import bench
     d, f, E, k, gating = bench.MODELS[model]
     fmt = F.SparseFormat(1, 2, 32)
@@ -440,36 +468,69 @@ def test_moe_layer_full_size_sampled(smy, model, T, NS):
     lg = torch.empty(T, E, dtype=torch.float32, device=dev)
     smy.synth_fill(lg, synth.SEED_LOGITS, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
     out = layer(x, lg).cpu().numpy().astype(np.float64)
+    v = layer.view(T)
+    offsets = v["offsets"].cpu().numpy()
+    sel_all = v["sel"].cpu().numpy()
+    inter = host16(v["inter"])
     xh, lgh = host16(x), lg.cpu().numpy()
-    del layer, shared
+    del layer, shared, v
     torch.cuda.empty_cache()
 
     ids, gw = moe.route(lgh, k, moe.SOFTMAX_ALL if gating == "softmax_all" else moe.RENORM_TOPK)
-    pairs = [tuple(sorted(r)) for r in ids]
-    pair = max(set(pairs), key=pairs.count)
-    toks = np.array([t for t in range(T) if pairs[t] == pair][:6])
-    xs = bf16.to_f64(xh[toks])
-    rng = np.random.default_rng(3)
-    groups = rng.choice(d // 2, 24, replace=False)
-    orow = np.sort(np.concatenate([2 * groups, 2 * groups + 1]))
+    _, r_off, r_sel, _ = moe.compact(ids, gw, E)
+    assert np.array_equal(offsets[:E + 1], r_off) and np.array_equal(sel_all[:r_off[E]], r_sel)
 
     def dense(seed, rows, cols, idx0=0):
         t = torch.empty(rows, cols, dtype=torch.int16, device=dev)
         smy.synth_fill(t, seed, synth.DIST_UNIFORM, float(synth.uniform_scale(np.sqrt(3.0 / cols))), idx0=idx0)
         return host16(t)
 
+    def pruned_rows(seed, cols, groups):
+        """rows 2g, 2g+1 of a weight with `cols` columns, pruned by the oracle"""
+        w = np.concatenate([dense(seed, 2, cols, idx0=int(2 * g) * cols) for g in groups])
+        return bf16.to_f64(F.prune(w, fmt))
+
+    rng = np.random.default_rng(3)
+    routed = sorted({int(e) for e in np.linspace(0, E - 1, 4).round()})
+    picks = {}                                          # expert -> [(row in the compact buffer, token)]
+    for e in routed + list(range(E, E + NS)):
+        o0, n = int(offsets[e]), int(offsets[e + 1] - offsets[e])
+        picks[e] = [(o0 + p, int(sel_all[o0 + p])) for p in _tile_positions(n)]
+    assert sum(len(p) for p in picks.values()) >= 4
+
+    # ---- gate/up intermediate of those (expert, token) rows, sampled channel pairs
+    cgroups = np.sort(rng.choice(f // 2, 32, replace=False))
+    chan = np.sort(np.concatenate([2 * cgroups, 2 * cgroups + 1]))
+    for e, pk in picks.items():
+        if not pk:
+            continue
+        xs = bf16.to_f64(xh[[t for _, t in pk]])
+        wg = pruned_rows(synth.weight_seed(e, 0), d, cgroups)
+        wu = pruned_rows(synth.weight_seed(e, 1), d, cgroups)
+        got = bf16.to_f64(inter[np.ix_([r for r, _ in pk], chan)])
+        check_silu_mul(got, xs @ wg.T, xs @ wu.T, np.abs(xs) @ np.abs(wg).T, np.abs(xs) @ np.abs(wu).T,
+                       f"{model} T={T} gate/up intermediate, expert {e}, SEL rows {[r for r, _ in pk]}")
+
+    # ---- layer output of those tokens
+    toks = np.array(sorted({t for pk in picks.values() for _, t in pk}))
+    xs = bf16.to_f64(xh[toks])
+    groups = np.sort(rng.choice(d // 2, 24, replace=False))
+    orow = np.sort(np.concatenate([2 * groups, 2 * groups + 1]))
     ref = np.zeros((len(toks), len(orow)))
     S = np.zeros_like(ref)
-    for e in list(pair) + list(range(E, E + NS)):
+    need = sorted({int(e) for t in toks for e in ids[t]}) + list(range(E, E + NS))
+    for e in need:
+        rows = [i for i, t in enumerate(toks) if e >= E or e in ids[t]]
         wg = bf16.to_f64(_prune_rows(dense(synth.weight_seed(e, 0), f, d), fmt))
         wu = bf16.to_f64(_prune_rows(dense(synth.weight_seed(e, 1), f, d), fmt))
-        a = bf16.to_f64(OS.silu_mul_bf16(xs @ wg.T, xs @ wu.T))             # [toks x f] bf16 intermediate
+        xe = xs[rows]
+        a = bf16.to_f64(OS.silu_mul_bf16(xe @ wg.T, xe @ wu.T))             # [rows x f] bf16 intermediate
         del wg, wu
-        wd = np.concatenate([dense(synth.weight_seed(e, 2), 2, f, idx0=int(2 * g) * f) for g in np.sort(groups)])
-        wd = bf16.to_f64(F.prune(wd, fmt))                                    # rows orow
-        g_e = (np.array([gw[t][list(ids[t]).index(e)] for t in toks])[:, None] if e < E
-               else np.ones((len(toks), 1)))                                 # shared expert: weight 1
-        ref += g_e * (a @ wd.T)
-        S += np.abs(g_e) * (np.abs(a) @ np.abs(wd).T)
+        wd = pruned_rows(synth.weight_seed(e, 2), f, groups)                 # rows orow
+        g_e = (np.array([gw[toks[i]][list(ids[toks[i]]).index(e)] for i in rows])[:, None] if e < E
+               else np.ones((len(rows), 1)))                                 # shared expert: weight 1
+        ref[rows] += g_e * (a @ wd.T)
+        S[rows] += np.abs(g_e) * (np.abs(a) @ np.abs(wd).T)
     check_tol(out[np.ix_(toks, orow)], ref, S,
-              f"{model} T={T} layer (+{NS} shared), tokens {toks.tolist()} (experts {pair})")
+              f"{model} T={T} layer (+{NS} shared), {len(toks)} tokens from the first/middle/last tiles of "
+              f"experts {sorted(picks)}")

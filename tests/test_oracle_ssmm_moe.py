@@ -157,6 +157,88 @@ def test_route_golden_and_invariants():
     assert np.array_equal(ids, ids3) and (w3.sum(1) < 1).all()
 
 
+def test_route_gate_weights_closed_form():
+    """Hand-computed gate weights (P:151 weighted sum; readings R9, R10): with
+    logits ln(c_e) the softmax of a subset is c_e / sum(c).  Pins the SOFTMAX_ALL
+    weights (denominator over ALL E, values taken at the selected ids) and
+    RENORM_TOPK (denominator over the selected k) -- a wrong index into the
+    exponentials (e.g. the first k instead of the selected ones) fails."""
+    lg = np.log(np.array([[1.0, 2.0, 3.0], [1.0, 2.0, 3.0]], dtype=np.float64)).astype(np.float32)
+    ids, w = moe.route(lg, 2, moe.SOFTMAX_ALL)
+    assert ids[0].tolist() == [2, 1]
+    assert np.allclose(w[0], [3 / 6, 2 / 6], rtol=1e-6, atol=0)
+    ids, w = moe.route(lg, 2, moe.RENORM_TOPK)
+    assert ids[0].tolist() == [2, 1]
+    assert np.allclose(w[0], [3 / 5, 2 / 5], rtol=1e-6, atol=0)
+    # E = 5, k = 3, selected ids not a prefix: c = [4, 1, 5, 2, 3]
+    c = np.array([4.0, 1.0, 5.0, 2.0, 3.0])
+    lg = np.log(c)[None, :].astype(np.float32)
+    ids, w = moe.route(lg, 3, moe.SOFTMAX_ALL)
+    assert ids[0].tolist() == [2, 0, 4]
+    assert np.allclose(w[0], [5 / 15, 4 / 15, 3 / 15], rtol=1e-6, atol=0)
+    ids, w = moe.route(lg, 3, moe.RENORM_TOPK)
+    assert np.allclose(w[0], [5 / 12, 4 / 12, 3 / 12], rtol=1e-6, atol=0)
+    # ties -> lower id (R10), weights equal
+    ids, w = moe.route(np.zeros((1, 4), dtype=np.float32), 2, moe.SOFTMAX_ALL)
+    assert ids[0].tolist() == [0, 1] and np.allclose(w[0], [0.25, 0.25], rtol=1e-12)
+
+
+def _bf16_rne(v: float) -> float:
+    """Round-to-nearest-even to 8 significant bits, written out (independent of
+    oracle/bf16.py): v = q * 2^(e-8) with q scaled to [128, 256); Python's
+    round() is round-half-even and q is exact in fp64."""
+    import math
+    if v == 0.0:
+        return 0.0
+    _, e = math.frexp(v)               # v = m * 2^e, 0.5 <= |m| < 1
+    step = math.ldexp(1.0, e - 8)
+    return round(v / step) * step
+
+
+def test_layer_error_scale_brute_force():
+    """The per-element error scale S of the layer (north star: |err| <= 1e-2 *
+    sum |g * w * a|), pinned from above and below by an element loop over the
+    pruned dense weights: S[t,o] = sum_(e,g in route(t)) |g| sum_j |Wd_e[o,j]|
+    |a_e[t,j]|, with a_e[t] = bf16(silu(Wg_e x_t) * (Wu_e x_t)) -- and the
+    output itself, same loop, for good measure."""
+    import math
+    fmt = F.SparseFormat(1, 2, 32)
+    E, d, f, T, k = 3, 64, 64, 4, 2
+    dense = []
+    for e in range(E):
+        trip = []
+        for i in range(3):
+            r, c = (f, d) if i < 2 else (d, f)
+            trip.append(bf16.to_f64(F.prune(synth.weight_bf16(700 + 3 * e + i, r, c), fmt)))
+        dense.append(trip)
+    ex = [tuple(F.encode(F.prune(synth.weight_bf16(700 + 3 * e + i, *((f, d) if i < 2 else (d, f))), fmt), fmt)
+                for i in range(3)) for e in range(E)]
+    xb = synth.activations_bf16(5, T, d)
+    x = bf16.to_f64(xb)
+    lg = synth.router_logits(6, T, E)
+    for mode in (moe.RENORM_TOPK, moe.SOFTMAX_ALL):
+        out, S = moe.moe_layer(ex, xb, lg, k, mode)
+        out_bf = np.zeros((T, d))
+        S_bf = np.zeros((T, d))
+        for t in range(T):
+            l = [float(v) for v in lg[t]]
+            order = sorted(range(E), key=lambda e: (-l[e], e))[:k]
+            den = sum(math.exp(l[e] - max(l)) for e in (order if mode == moe.RENORM_TOPK else range(E)))
+            for e in order:
+                g = math.exp(l[e] - max(l)) / den
+                wg, wu, wd = dense[e]
+                a = []
+                for j in range(f):
+                    h = sum(wg[j, c] * x[t, c] for c in range(d))
+                    u = sum(wu[j, c] * x[t, c] for c in range(d))
+                    a.append(_bf16_rne(h / (1.0 + math.exp(-h)) * u))
+                for o in range(d):
+                    out_bf[t, o] += g * sum(wd[o, j] * a[j] for j in range(f))
+                    S_bf[t, o] += abs(g) * sum(abs(wd[o, j] * a[j]) for j in range(f))
+        assert np.allclose(S, S_bf, rtol=1e-9, atol=0), np.abs(S / S_bf - 1).max()
+        assert np.allclose(out, out_bf, rtol=1e-9, atol=1e-12)
+
+
 def test_compaction_partition():
     lg = synth.router_logits(2, 64, 8)
     ids, w = moe.route(lg, 2)
