@@ -10,9 +10,11 @@ in the (1,2,32) format (75% weight sparsity).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--model mixtral|deepseek|qwen2] [--tokens T]
 
-N > 1 is launched by torchrun; every rank runs its own token batch on a full
-replica of the experts ("scaling": "weak"; no data-path collective yet).
-Rank 0 prints one JSON line.
+N > 1: one process per GPU (launched by torchrun, or spawned here when
+WORLD_SIZE is unset); every rank runs its own batch of T tokens ("scaling":
+"weak") through the expert-parallel layer -- experts sharded over the ranks,
+token dispatch / combine over NCCL (default) or NVLink peer memory.  Rank 0
+prints one JSON line.
 """
 from __future__ import annotations
 
@@ -226,6 +228,77 @@ def build_layer(P, model, device, experts=None, transcode="auto"):
     return experts_out
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        return s_.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N > 1 without a torchrun environment: re-launch this command as N
+    ranks of one node through torch.distributed.run (one process per GPU,
+    rendezvous on 127.0.0.1); rank 0's JSON line comes back on stdout."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.run(cmd, env=env).returncode
+
+
+def init_ranks(args, device=None):
+    """The process group of an N-rank run (torchrun environment).  The rank count
+    must equal --gpus.  NCCL's INFO log (communicator ranks: "nranks N") goes to
+    stderr, so stdout keeps only the JSON line."""
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1 or args.force_ep:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29541")
+        backend = "gloo" if args.dry_run else "nccl"
+        with stdout_to_stderr():     # NCCL's version banner goes to fd 1: keep stdout to the JSON line
+            if backend == "nccl":
+                dist.init_process_group(backend, rank=rank, world_size=world, device_id=device)
+            else:
+                dist.init_process_group(backend, rank=rank, world_size=world)
+            dist.barrier()
+        print(f"[bench] rank {rank}: process group backend={backend} nranks={dist.get_world_size()}",
+              file=sys.stderr, flush=True)
+    return world, rank
+
+
+def run_dry(args):
+    """--dry-run: the N-rank launch path without a GPU (gloo): every rank joins the
+    process group, runs the barrier + max-over-ranks timing of the contract on a
+    stand-in step, and rank 0 prints the contract line ("dry_run": true, no
+    measurement).  Used by the CPU tests of the multi-GPU launcher."""
+    import torch
+    import torch.distributed as dist
+    world, rank = init_ranks(args)
+    d, f, E, k, gating = MODELS[args.model]
+    t0 = time.perf_counter()
+    if world > 1:
+        dist.barrier()
+    ms = torch.tensor([(time.perf_counter() - t0) * 1e3])
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": "moe_layer_tokens_per_s", "value": None, "unit": "tokens/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+                          "data": "synthetic", "dry_run": True,
+                          "config": {"workload": WORKLOAD[args.model], "tokens_per_gpu": args.tokens,
+                                     "global_tokens": args.tokens * world, "experts": E, "top_k": k,
+                                     "parallelism": f"ep{world}" if world > 1 else "dp1"},
+                          "barrier_ms_max_over_ranks": float(ms.item())}), flush=True)
+    if dist.is_initialized():
+        dist.destroy_process_group()
+    return 0
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -234,17 +307,10 @@ def run_ours(args):
     import synth
     import paper_2503_10725_b200 as P
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
-    if world > 1 or args.force_ep:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29541")
-        with stdout_to_stderr():     # NCCL's version banner goes to fd 1: keep stdout to the JSON line
-            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=device)
-            dist.barrier()
+    world, rank = init_ranks(args, device)
     lib = P.load()
     model = args.model
     d, f, E, k, gating = MODELS[model]
@@ -255,6 +321,7 @@ def run_ours(args):
         raise SystemExit("--shared: shared experts are measured on the 1-GPU / data-parallel layer")
     cfg = P.MoEConfig(E, k, d, f, NS, gating, P.Format(*FMT), "auto", args.transcode)
     transport = None
+    comm = None
     x = torch.empty(T, d, dtype=torch.int16, device=device)
     if ep:
         from paper_2503_10725_b200.ep import EPMoELayer, PeerEPMoELayer, SymmetricPeers, TorchExchange
@@ -267,15 +334,24 @@ def run_ours(args):
             try:      # token rows / outputs over NVLink peer memory inside the SSMM kernels
                 with stdout_to_stderr():
                     peers = SymmetricPeers(dist.group.WORLD, T, d, device)
-            except Exception as exc:  # no symmetric memory on this box: the NCCL all_to_all_v transport
+            except Exception as exc:  # no symmetric memory on this box: the NCCL transport
                 print(f"symmetric memory unavailable ({exc}); using the NCCL transport", file=sys.stderr)
         if peers is not None:
             transport = "peer"
             layer = PeerEPMoELayer(cfg, experts, rank, world, T, peers, device=device, exchange=TorchExchange())
             x = peers.x[:T]               # inputs live in the symmetric buffer (no publish copy)
-        else:
-            transport = "nccl"
+        elif args.ep_transport == "torch":
+            transport = "torch"
             layer = EPMoELayer(cfg, experts, rank, world, max_tokens=T, device=device, exchange=TorchExchange())
+        else:
+            # default: the library's own NCCL communicator behind samoyeds_moe_layer(..., comm)
+            # -- route, plan, grouped ncclSend/Recv of rows + tags, experts, fp32 partial
+            # rows back, combine, all inside the C call (one host read of the counts)
+            transport = "nccl"
+            with stdout_to_stderr():
+                comm = P.EPComm()
+            print(f"[bench] rank {rank}: samoyeds EP communicator nranks={comm.world}", file=sys.stderr, flush=True)
+            layer = P.MoELayer(cfg, experts, max_tokens=T, device=device, comm=comm)
     else:
         experts = build_layer(P, model, device, transcode=args.transcode)
         # shared experts: every token, weight 1 (reading R15);
@@ -495,7 +571,10 @@ def run_ours(args):
                                                                else ""),
                    "parallelism": ((f"ep{world} (experts sharded; token rows / outputs over NVLink peer memory "
                                     "inside the SSMM kernels, tags over NCCL)" if transport == "peer" else
-                                    f"ep{world} (experts sharded, NCCL all_to_all_v dispatch/combine)") if ep
+                                    f"ep{world} (experts sharded; dispatch/combine by torch all_to_all_single)"
+                                    if transport == "torch" else
+                                    f"ep{world} (experts sharded; dispatch/combine by the library's NCCL "
+                                    "communicator, grouped ncclSend/Recv inside samoyeds_moe_layer)") if ep
                                    else f"dp{world} (experts replicated per GPU)"),
                    "l2": "inputs larger than L2: %.0f MB of compressed expert weights streamed per step"
                          % (3 * active * f * d * BYTES_PER_ELEM / 1e6),
@@ -518,6 +597,8 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_baseline(model)
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if dist.is_initialized():
         dist.destroy_process_group()
     return 0
@@ -600,8 +681,11 @@ def main():
                     help="formats without fast kernels: re-encode as plain 2:4 (auto) or keep (off)")
     ap.add_argument("--force-ep", action="store_true", help=argparse.SUPPRESS)  # EP code path at world 1 (tests)
     ap.add_argument("--parallel", default="ep", choices=["ep", "dp"], help="N>1: expert (default) or data parallel")
-    ap.add_argument("--ep-transport", default="peer", choices=["peer", "nccl"],
-                    help="EP token/output transport: NVLink peer memory in the kernels (default) or NCCL all_to_all_v")
+    ap.add_argument("--ep-transport", default="nccl", choices=["nccl", "torch", "peer"],
+                    help="EP token/output transport: the library's NCCL communicator (default), torch "
+                         "all_to_all_single, or NVLink peer memory inside the kernels")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch / process-group / timing path only, on CPU (gloo): prints the contract line")
     ap.add_argument("--shared", type=int, default=0,
                     help="shared experts (every token, weight 1) after the routed ones, e.g. 2 for DeepSeek-MoE")
     ap.add_argument("--decode-tokens", type=int, default=64, help="extra decode point on the same layer (0: off)")
@@ -609,8 +693,17 @@ def main():
     set_format(args.format)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     if args.impl == "reference":
         return run_reference(args)
+    if args.dry_run:
+        return run_dry(args)
+    if "NCCL_DEBUG" not in os.environ and args.gpus > 1:
+        # communicator setup lines (rank / nranks) on stderr; stdout keeps the JSON line
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     return run_ours(args)
 
 

@@ -115,8 +115,14 @@ SMY_API smy_status samoyeds_compress(const smy_wdesc* desc, const void* w_bf16, 
 /* samoyeds_decompress: the inverse of the encoding -- the dense
  * pattern-conforming bf16 weight [rows x ldw] (dev) from the canonical values,
  * codes and indices (which must be present); positions not stored are zero.
- * compress(decompress(w)) with SMY_ASSUME_PRUNED reproduces w bit for bit.  */
-SMY_API smy_status samoyeds_decompress(const smy_weight* w, void* w_bf16, int64_t ldw, void* stream);
+ * compress(decompress(w)) with SMY_ASSUME_PRUNED reproduces w bit for bit.
+ * d_status (dev int32, nullable; the caller zeroes it first): the decoding
+ * invariants are checked on the device -- per (row group, K-block) the N
+ * sub-row indices < M and strictly increasing, per kept 4-group the two codes
+ * strictly increasing -- and a violation writes SMY_E_CORRUPT (values of an
+ * out-of-range sub-row index are dropped, never written outside the block). */
+SMY_API smy_status samoyeds_decompress(const smy_weight* w, void* w_bf16, int64_t ldw, int32_t* d_status,
+                                       void* stream);
 
 /* samoyeds_interleave_gate_up: the interleaved gate/up weight of one expert
  * (reading R20; the paper fuses the activation with "its precedent
@@ -145,9 +151,15 @@ SMY_API smy_status samoyeds_interleave_gate_up(const smy_weight* gate, const smy
  *                            out[t * ldo + o] = bf16(silu(C_gate[t,o]) * C_up[t,o])
  *                            for o < f (BF16; format (1,2,V), V % 32 == 0)
  *   SMY_EPI_SCATTER_ADD      out[sel[t] * ldo + o] += scale[t] * C[t, o]  (f32;
- *                            scale NULL = 1; atomic, order not deterministic)
- * x: dev bf16 [x_rows x ldx], token-major; sel: dev int32 [n_sel], each in
- * [0, x_rows) (not validated on device); n_sel may be 0.  fp32 accumulation. */
+ *                            scale NULL = 1; atomic, order not deterministic;
+ *                            16-byte reductions: ldo % 4 == 0, out 16-byte
+ *                            aligned and rows % 4 == 0, else SMY_E_SHAPE)
+ * x: dev bf16 [x_rows x ldx], token-major; sel: dev int32 [n_sel], strictly
+ * increasing, each in [0, x_rows) (the SEL of P:303); n_sel may be 0.  fp32
+ * accumulation.  SEL is not checked on the hot path: samoyeds_validate_sel
+ * checks it on the device (async, SMY_E_SELECTION into *d_status), and with the
+ * environment variable SMY_DEBUG having bit 65536 set, samoyeds_ssmm runs that
+ * check itself, synchronises its stream and returns SMY_E_SELECTION.        */
 typedef enum {
   SMY_EPI_COMPACT = 0,
   SMY_EPI_SILU_MUL_COMPACT = 1,
@@ -159,13 +171,17 @@ typedef enum {
 SMY_API smy_status samoyeds_ssmm(const smy_weight* w, const smy_weight* w2, const void* x_bf16, int64_t ldx,
                          int64_t x_rows, const int32_t* sel, int32_t n_sel, const float* scale, int epi,
                          void* out, int64_t ldo, int out_dtype, void* stream);
+SMY_API smy_status samoyeds_validate_sel(const int32_t* sel, int32_t n_sel, int64_t x_rows, int32_t* d_status,
+                                         void* stream);
 
 /* --------------------------------------------------- routing / compaction
  * Top-k of fp32 router logits [T x E] per token (ties -> lower expert id) and
  * gate weights (readings R9, R10), then the per-expert selection
  * arrays: counts[E], offsets[E+1] (exclusive scan),
  * sel[T*k] token ids ascending within each expert, gw[T*k] aligned with sel.
- * ids/w (dev [T x k]) are written too.  Bit-exact deterministic.          */
+ * ids/w (dev [T x k]) are written too.  Bit-exact deterministic.  A NaN
+ * logit ranks as -inf (selected only after every finite logit).  gating must
+ * be SMY_GATE_RENORM_TOPK or SMY_GATE_SOFTMAX_ALL (else SMY_E_CONFIG).     */
 #define SMY_GATE_RENORM_TOPK 0
 #define SMY_GATE_SOFTMAX_ALL 1
 SMY_API smy_status smy_route_workspace_bytes(int64_t T, int32_t E, size_t* bytes);
@@ -184,14 +200,20 @@ SMY_API smy_status samoyeds_route(const float* logits, int64_t T, int32_t E, int
  * num_experts + num_shared <= 128); the shared experts run as extra groups of the
  * same two grouped SSMM launches (the routing appends ids E.. with weight 1 to
  * every token).  x dev bf16 [T x hidden]; logits dev fp32
- * [T x E]; out dev fp32 [T x hidden] (overwritten).  The gate/up -> down
+ * [T x E]; out dev [T x hidden] (overwritten), fp32 or bf16 (cfg->out_dtype).  The gate/up -> down
  * intermediate is bf16 (reading R12).                                     */
 #define SMY_GU_SEPARATE 0
 #define SMY_GU_INTERLEAVED 1
 typedef struct {
   int32_t num_experts, top_k, hidden, ffn, num_shared, gating;
   smy_format fmt;
-  int32_t gate_up; /* SMY_GU_SEPARATE | SMY_GU_INTERLEAVED */
+  int32_t gate_up;   /* SMY_GU_SEPARATE | SMY_GU_INTERLEAVED */
+  int32_t out_dtype; /* SMY_F32 (default): out is fp32 [T x hidden];
+                        SMY_BF16: out is bf16 [T x hidden] -- the layer
+                        accumulates in an fp32 buffer at the end of its
+                        workspace (smy_moe_workspace_bytes counts it) and
+                        rounds once (RNE) after the last expert; single-GPU
+                        layer only (comm == NULL, else SMY_E_CONFIG)       */
 } smy_moe_config;
 typedef struct smy_ep_comm smy_ep_comm; /* opaque, library-owned (EP) */
 SMY_API smy_status smy_moe_workspace_bytes(const smy_moe_config* cfg, int64_t max_tokens, size_t* bytes);
@@ -202,9 +224,14 @@ SMY_API smy_status smy_moe_workspace_bytes(const smy_moe_config* cfg, int64_t ma
  * E, sends each token once to every rank owning one of its experts (NCCL
  * send/recv of rows + tags), runs this rank's experts on what it received,
  * returns the fp32 partial rows and sums them into out.  It reads the [W]
- * receive counts on the host once (one stream synchronisation). */
+ * receive counts on the host once (one stream synchronisation).  Every rank
+ * must size its workspace for the same max_tokens and call with T <= it: the
+ * receive buffers hold max_tokens rows per peer.  A rank whose T exceeds its
+ * workspace announces it in the counts exchange (count -1), and then EVERY
+ * rank returns SMY_E_WORKSPACE after that exchange (no rank blocks in NCCL).
+ * out must be 16-byte aligned (SMY_E_SHAPE). */
 SMY_API smy_status samoyeds_moe_layer(const smy_moe_config* cfg, const smy_weight* experts, const smy_weight* shared,
-                              const void* x_bf16, const float* logits, int64_t T, float* out, void* workspace,
+                              const void* x_bf16, const float* logits, int64_t T, void* out, void* workspace,
                               size_t ws_bytes, smy_ep_comm* comm, void* stream);
 
 /* The library-owned NCCL communicator of expert parallelism (libnccl.so.2 is

@@ -13,7 +13,7 @@ Paper:
   * shared experts: "all tokens ... processed by all these shared experts in
     addition to their assigned routed experts"               (§6.2)
 Readings: R9 gate normalisation (RENORM_TOPK default, SOFTMAX_ALL preset),
-R10 top-k ties -> lower expert id, R11 SiLU gated MLP, R12 bf16 intermediate,
+R10 top-k ties -> lower expert id, R10b a NaN logit ranks as -inf, R11 SiLU gated MLP, R12 bf16 intermediate,
 R15 shared experts weight 1.
 """
 from __future__ import annotations
@@ -33,6 +33,7 @@ def route(logits: np.ndarray, top_k: int, mode: int = RENORM_TOPK):
     logits: fp32 [T x E].  Returns ids int32 [T x k] (descending logit, then
     ascending id) and weights fp64 [T x k]."""
     lg = np.asarray(logits, dtype=np.float32).astype(np.float64)
+    lg = np.where(np.isnan(lg), -np.inf, lg)     # reading R10b: a NaN logit ranks as -inf
     T, E = lg.shape
     if not 1 <= top_k <= E:
         raise ValueError("need 1 <= top_k <= E")

@@ -13,7 +13,8 @@ matmul as one step).  Fused epilogues (§4.3 "Operator fusion"):
                      activation fused (R11: SiLU gated MLP; R12: the
                      intermediate is stored as bf16, emulated with RNE)
   * SILU_MUL_INTERLEAVED  the same on one weight holding gate and up rows
-                     interleaved in blocks of 128 (fmt.interleave_rows, R20)
+                     interleaved in blocks of 16 compressed rows
+                     (fmt.interleave_rows / gu_block, R20)
   * SCATTER_ADD      out[sel[t]] += scale[t] * C[t] -- "the weighted
                      accumulation ... is fused with matrix multiplication"
 

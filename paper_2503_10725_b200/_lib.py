@@ -33,7 +33,8 @@ class smy_weight(C.Structure):
 
 class smy_moe_config(C.Structure):
     _fields_ = [("num_experts", C.c_int32), ("top_k", C.c_int32), ("hidden", C.c_int32), ("ffn", C.c_int32),
-                ("num_shared", C.c_int32), ("gating", C.c_int32), ("fmt", smy_format), ("gate_up", C.c_int32)]
+                ("num_shared", C.c_int32), ("gating", C.c_int32), ("fmt", smy_format), ("gate_up", C.c_int32),
+                ("out_dtype", C.c_int32)]
 
 
 class smy_moe_view(C.Structure):
@@ -49,7 +50,8 @@ SIGNATURES = {
     "smy_weight_layout": (C.c_int, [C.POINTER(smy_wdesc), C.POINTER(smy_wlayout)]),
     "samoyeds_compress": (C.c_int, [C.POINTER(smy_wdesc), C.c_void_p, C.c_int64, C.c_int, C.POINTER(smy_weight),
                                     C.c_void_p, C.c_void_p]),
-    "samoyeds_decompress": (C.c_int, [C.POINTER(smy_weight), C.c_void_p, C.c_int64, C.c_void_p]),
+    "samoyeds_decompress": (C.c_int, [C.POINTER(smy_weight), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "samoyeds_validate_sel": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p]),
     "samoyeds_interleave_gate_up": (C.c_int, [C.POINTER(smy_weight), C.POINTER(smy_weight), C.POINTER(smy_weight),
                                               C.c_void_p]),
     "samoyeds_ssmm": (C.c_int, [C.POINTER(smy_weight), C.POINTER(smy_weight), C.c_void_p, C.c_int64, C.c_int64,

@@ -101,15 +101,28 @@ def compress(w: torch.Tensor, fmt: Format, prune: bool = True, stream=None):
     return sw, status
 
 
-def decompress(w: SparseWeight, stream=None) -> torch.Tensor:
-    """samoyeds_decompress: the dense bf16 [rows x cols] (int16 bit patterns) weight."""
+def decompress(w: SparseWeight, stream=None, status: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """samoyeds_decompress: the dense bf16 [rows x cols] (int16 bit patterns) weight.
+    status: optional zeroed int32[1] CUDA tensor; receives SMY_E_CORRUPT (6) if the
+    canonical arrays violate the decoding invariants."""
     lib = _lib.load()
     if w.values is None:
         raise ValueError("decompress needs the canonical arrays (drop_canonical() was called)")
     out = torch.empty(w.rows, w.cols, dtype=torch.int16, device=w.image.device)
     cw = w.c()
-    check(lib.samoyeds_decompress(C.byref(cw), _ptr(out), out.stride(0), _stream(stream)), "samoyeds_decompress")
+    check(lib.samoyeds_decompress(C.byref(cw), _ptr(out), out.stride(0), _ptr(status) if status is not None else None,
+                                  _stream(stream)), "samoyeds_decompress")
     return out
+
+
+def validate_sel(sel: torch.Tensor, x_rows: int, stream=None) -> torch.Tensor:
+    """samoyeds_validate_sel: int32[1] status tensor (0, or SMY_E_SELECTION = 5 if
+    sel is not strictly increasing within [0, x_rows)); asynchronous."""
+    lib = _lib.load()
+    status = torch.zeros(1, dtype=torch.int32, device=sel.device)
+    check(lib.samoyeds_validate_sel(_ptr(sel), sel.numel(), x_rows, _ptr(status), _stream(stream)),
+          "samoyeds_validate_sel")
+    return status
 
 
 def transcode_24(w: SparseWeight, stream=None) -> SparseWeight:
@@ -196,6 +209,9 @@ class MoEConfig:
     # "auto": formats without fast kernels (N>1 with N<M, V=16) are re-encoded as
     # plain 2:4 (2,2,32) when a layer is built (transcode_24); "off": keep them
     transcode: str = "auto"
+    # layer output dtype: "f32" (default) or "bf16" (fp32 accumulation in the
+    # workspace, one RNE rounding at the end; single-GPU layer)
+    out_dtype: str = "f32"
 
     def fast_format(self) -> bool:
         f = self.fmt
@@ -211,12 +227,13 @@ class MoEConfig:
         """The configuration the layer's kernels run on (after transcoding)."""
         if self.transcode == "auto" and not self.fast_format():
             return MoEConfig(self.num_experts, self.top_k, self.hidden, self.ffn, self.num_shared, self.gating,
-                             Format(2, 2, 32), self.gate_up, "off")
+                             Format(2, 2, 32), self.gate_up, "off", self.out_dtype)
         return self
 
     def c(self) -> smy_moe_config:
         return smy_moe_config(self.num_experts, self.top_k, self.hidden, self.ffn, self.num_shared,
-                              GATING[self.gating], self.fmt.c(), GATE_UP[self.resolved_gate_up()])
+                              GATING[self.gating], self.fmt.c(), GATE_UP[self.resolved_gate_up()],
+                              {"f32": 0, "bf16": 1}[self.out_dtype])
 
 
 def _weight_array(triples: Sequence[Sequence[Optional[SparseWeight]]]):
@@ -303,7 +320,8 @@ class MoELayer:
         if T > self.max_tokens:
             raise ValueError("T exceeds the workspace's max_tokens")
         if out is None:
-            out = torch.empty(T, self.cfg.hidden, dtype=torch.float32, device=x.device)
+            out = torch.empty(T, self.cfg.hidden, dtype=torch.bfloat16 if self.cfg.out_dtype == "bf16" else torch.float32,
+                              device=x.device)
         xb = x.view(torch.int16) if x.dtype == torch.bfloat16 else x
         check(lib.samoyeds_moe_layer(C.byref(self._cfg), self._arr, self._sarr, _ptr(xb), _ptr(logits), T,
                                      _ptr(out), _ptr(self.workspace), self.workspace.numel(),

@@ -109,7 +109,7 @@ smy_status synth_launch(uint64_t seed, int dist, float scale, int lo, int hi, in
                         int out_bf16, cudaStream_t s);
 smy_status moe_workspace_bytes(const smy_moe_config* c, int64_t T, size_t* bytes);
 smy_status moe_layer(const smy_moe_config* c, const smy_weight* experts, const smy_weight* shared, const void* x,
-                     const float* logits, int64_t T, float* out, void* workspace, size_t ws_bytes, cudaStream_t s);
+                     const float* logits, int64_t T, void* out, void* workspace, size_t ws_bytes, cudaStream_t s);
 smy_status moe_view(const smy_moe_config* c, int64_t T, void* workspace, size_t ws_bytes, smy_moe_view* v);
 
 }  // namespace smy
@@ -192,14 +192,22 @@ smy_status samoyeds_compress(const smy_wdesc* desc, const void* w_bf16, int64_t 
                          static_cast<cudaStream_t>(stream));
 }
 
-smy_status samoyeds_decompress(const smy_weight* w, void* w_bf16, int64_t ldw, void* stream) {
+smy_status samoyeds_decompress(const smy_weight* w, void* w_bf16, int64_t ldw, int32_t* d_status, void* stream) {
   if (!w || !w_bf16 || !w->values || !w->codes || !w->indices) return SMY_E_NULL;
   Geometry g;
   smy_status st = geometry(&w->d, &g);
   if (st != SMY_OK) return st;
   if (ldw < w->d.cols) return SMY_E_SHAPE;
   if ((st = check_arch()) != SMY_OK) return st;
-  return decompress_launch(w, static_cast<uint16_t*>(w_bf16), ldw, static_cast<cudaStream_t>(stream));
+  return decompress_launch(w, static_cast<uint16_t*>(w_bf16), ldw, d_status, static_cast<cudaStream_t>(stream));
+}
+
+smy_status samoyeds_validate_sel(const int32_t* sel, int32_t n_sel, int64_t x_rows, int32_t* d_status, void* stream) {
+  if ((n_sel > 0 && !sel) || !d_status) return SMY_E_NULL;
+  if (n_sel < 0 || x_rows < 0) return SMY_E_SHAPE;
+  smy_status st;
+  if ((st = check_arch()) != SMY_OK) return st;
+  return sel_check_launch(sel, n_sel, x_rows, d_status, static_cast<cudaStream_t>(stream));
 }
 
 smy_status samoyeds_interleave_gate_up(const smy_weight* gate, const smy_weight* up, smy_weight* gu, void* stream) {
@@ -208,6 +216,11 @@ smy_status samoyeds_interleave_gate_up(const smy_weight* gate, const smy_weight*
       !gu->codes || !gu->indices || !gu->image)
     return SMY_E_NULL;
   if (memcmp(&gate->d, &up->d, sizeof(smy_wdesc)) != 0 || gate->d.rows % 32) return SMY_E_SHAPE;
+  // the kernel moves blocks of 16 compressed rows (reading R20): R = rows*N/M % 16 == 0
+  if ((gate->d.rows * gate->d.fmt.n / gate->d.fmt.m) % 16) {
+    set_last_error("interleave_gate_up needs rows * N / M % 16 == 0 (blocks of 16 compressed rows)");
+    return SMY_E_SHAPE;
+  }
   smy_wdesc d = gate->d;
   d.rows *= 2;
   Geometry g;
@@ -250,8 +263,31 @@ smy_status samoyeds_ssmm(const smy_weight* w, const smy_weight* w2, const void* 
   if (out_dtype != SMY_F32 && out_dtype != SMY_BF16) return SMY_E_CONFIG;
   const int64_t out_cols = epi == SMY_EPI_SILU_MUL_INTERLEAVED ? w->d.rows / 2 : w->d.rows;
   if (ldo < out_cols || (ldo % 2)) return SMY_E_SHAPE;
+  // the scatter epilogue reduces 16 B (4 fp32 outputs) per lane pair
+  const bool v4_ok = ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && w->d.rows % 4 == 0;
+  if (epi == SMY_EPI_SCATTER_ADD && !v4_ok) {
+    set_last_error("SCATTER_ADD needs ldo % 4 == 0, a 16-byte aligned out and rows % 4 == 0");
+    return SMY_E_SHAPE;
+  }
   if ((st = check_arch()) != SMY_OK) return st;
   if (n_sel == 0) return SMY_OK;
+  if (debug_flags() & kDebugValidate) {  // debug builds of a caller: check SEL, synchronously
+    int32_t* d_st = nullptr;
+    int32_t h_st = SMY_OK;
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    if (cudaMallocAsync(reinterpret_cast<void**>(&d_st), 4, cs) != cudaSuccess) return cuda_status(cudaGetLastError());
+    cudaMemsetAsync(d_st, 0, 4, cs);
+    st = sel_check_launch(sel, n_sel, x_rows, d_st, cs);
+    cudaMemcpyAsync(&h_st, d_st, 4, cudaMemcpyDeviceToHost, cs);
+    cudaFreeAsync(d_st, cs);
+    cudaError_t ce = cudaStreamSynchronize(cs);
+    if (st != SMY_OK) return st;
+    if (ce != cudaSuccess) return cuda_status(ce);
+    if (h_st != SMY_OK) {
+      set_last_error("sel: entries must be strictly increasing and in [0, x_rows)");
+      return SMY_E_SELECTION;
+    }
+  }
   const int nw = epi == SMY_EPI_SILU_MUL_COMPACT ? 2 : 1;
   const int nt = ssmm_pick_nt(nw, g.ms, g.rep, n_sel);
   SsmmArgs a;
@@ -289,7 +325,7 @@ smy_status samoyeds_ssmm(const smy_weight* w, const smy_weight* w2, const void* 
   // SMs (split-K / stream-K tail) and the partial sums add.
   {
     const int64_t tiles = (int64_t)g.m_tiles * ((n_sel + nt - 1) / nt);
-    if (a.epi == kEpiCompact && !a.out_bf16 && tiles < 74 && g.k_stages >= 16) {
+    if (a.epi == kEpiCompact && !a.out_bf16 && tiles < 74 && g.k_stages >= 16 && v4_ok) {
       cudaError_t ce = cudaMemset2DAsync(out, (size_t)ldo * 4, 0, (size_t)w->d.rows * 4, (size_t)n_sel,
                                          static_cast<cudaStream_t>(stream));
       if (ce != cudaSuccess) return cuda_status(ce);
@@ -345,7 +381,7 @@ smy_status smy_moe_workspace_bytes(const smy_moe_config* cfg, int64_t max_tokens
 }
 
 smy_status samoyeds_moe_layer(const smy_moe_config* cfg, const smy_weight* experts, const smy_weight* shared,
-                              const void* x_bf16, const float* logits, int64_t T, float* out, void* workspace,
+                              const void* x_bf16, const float* logits, int64_t T, void* out, void* workspace,
                               size_t ws_bytes, smy_ep_comm* comm, void* stream) {
   if (!cfg || !experts || !out || !workspace) return SMY_E_NULL;
   if (T > 0 && (!x_bf16 || !logits)) return SMY_E_NULL;
@@ -354,7 +390,11 @@ smy_status samoyeds_moe_layer(const smy_moe_config* cfg, const smy_weight* exper
     return SMY_E_CONFIG;
   // shared experts run as extra groups with extra routing entries per token
   if (cfg->num_experts + cfg->num_shared > kMaxGroups || cfg->top_k + cfg->num_shared > 16) return SMY_E_CONFIG;
+  if (cfg->gating != SMY_GATE_RENORM_TOPK && cfg->gating != SMY_GATE_SOFTMAX_ALL) return SMY_E_CONFIG;
+  if (cfg->out_dtype != SMY_F32 && cfg->out_dtype != SMY_BF16) return SMY_E_CONFIG;
+  if (cfg->out_dtype == SMY_BF16 && comm != nullptr) return SMY_E_CONFIG;
   if (cfg->hidden % 128 || cfg->ffn % 128) return SMY_E_SHAPE;
+  if (reinterpret_cast<uintptr_t>(out) & 15) return SMY_E_SHAPE;  // 16-B scatter reductions
   smy_status st;
   if (comm != nullptr) {  // expert parallelism: experts = this rank's E / world (NCCL transport)
     const int W = ep_comm_world(comm);
@@ -363,7 +403,7 @@ smy_status samoyeds_moe_layer(const smy_moe_config* cfg, const smy_weight* exper
     lc.num_experts = cfg->num_experts / W;
     if ((st = check_experts(&lc, experts, lc.num_experts)) != SMY_OK) return st;
     if ((st = check_arch()) != SMY_OK) return st;
-    return ep_layer(cfg, experts, x_bf16, logits, T, out, workspace, ws_bytes, comm,
+    return ep_layer(cfg, experts, x_bf16, logits, T, static_cast<float*>(out), workspace, ws_bytes, comm,
                     static_cast<cudaStream_t>(stream));
   }
   if ((st = check_experts(cfg, experts, cfg->num_experts)) != SMY_OK) return st;
@@ -416,8 +456,10 @@ smy_status samoyeds_moe_experts(const smy_moe_config* cfg, const smy_weight* exp
                                 size_t ws_bytes, void* stream) {
   if (!cfg || !experts || !out || !workspace) return SMY_E_NULL;
   if (rows > 0 && (!x_bf16 || !keys || !vals)) return SMY_E_NULL;
-  if (cfg->num_experts < 1 || cfg->top_k < 1 || cfg->top_k > 8 || cfg->num_experts > kMaxGroups) return SMY_E_CONFIG;
-  if (cfg->hidden % 128 || cfg->ffn % 128 || rows < 0) return SMY_E_SHAPE;
+  if (cfg->num_experts < 1 || cfg->top_k < 1 || cfg->top_k > 8 || cfg->num_experts > kMaxGroups ||
+      cfg->num_shared != 0 || cfg->out_dtype != SMY_F32)
+    return SMY_E_CONFIG;
+  if (cfg->hidden % 128 || cfg->ffn % 128 || rows < 0 || (reinterpret_cast<uintptr_t>(out) & 15)) return SMY_E_SHAPE;
   smy_status st;
   if ((st = check_experts(cfg, experts, cfg->num_experts)) != SMY_OK) return st;
   if ((st = check_arch()) != SMY_OK) return st;
@@ -463,7 +505,7 @@ smy_status samoyeds_moe_experts_peer(const smy_moe_config* cfg, const smy_weight
   for (int p = 0; p < world; ++p)
     if (!x_peers[p] || !out_peers[p]) return SMY_E_NULL;
   if (cfg->num_experts < 1 || cfg->top_k < 1 || cfg->top_k > 8 || cfg->num_experts > kMaxGroups ||
-      cfg->num_shared != 0)
+      cfg->num_shared != 0 || cfg->out_dtype != SMY_F32)
     return SMY_E_CONFIG;
   if (cfg->hidden % 128 || cfg->ffn % 128 || rows < 0 || ldx < cfg->hidden || ldx % 8 || ldo < cfg->hidden ||
       ldo % 4)

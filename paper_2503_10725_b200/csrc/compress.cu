@@ -192,18 +192,75 @@ __global__ void decompress_kernel(const uint16_t* __restrict__ values, const uin
     const int64_t r = i / half, c = i % half;
     const int64_t j = (2 * c) / V, q = (c % (V / 2)) / 2;
     const int code = (codes[r * (cols / 8) + c / 4] >> (2 * (c % 4))) & 3;
-    const int64_t row = (r / N) * M + indices[r * (cols / V) + j];
+    const int sub = indices[r * (cols / V) + j];
+    if (sub >= M) continue;  // corrupt index (reported by decode_check_kernel): no write outside the block
+    const int64_t row = (r / N) * M + sub;
     w[row * ldw + j * V + 4 * q + code] = values[i];
   }
 }
 
-smy_status decompress_launch(const smy_weight* src, uint16_t* w, int64_t ldw, cudaStream_t s) {
+// The decoding invariants of the canonical arrays (reading R5/R6, S:43-44,
+// S:80-88): per (row group g, K-block j) the N sub-row indices are < M and
+// strictly increasing; per kept 4-group the two 2-bit codes are strictly
+// increasing.  One thread per (g, j); any violation -> *status = SMY_E_CORRUPT.
+__global__ void decode_check_kernel(const uint8_t* __restrict__ codes, const uint8_t* __restrict__ indices, int64_t G,
+                                    int64_t cols, int N, int M, int V, int32_t* __restrict__ status) {
+  const int64_t J = cols / V;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < G * J; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = i / J, j = i % J;
+    bool bad = false;
+    int prev = -1;
+    for (int n = 0; n < N; ++n) {
+      const int64_t r = g * N + n;
+      const int sub = indices[r * J + j];
+      bad |= sub >= M || sub <= prev;
+      prev = sub;
+      for (int q = 0; q < V / 4; ++q) {
+        const int64_t c = j * (V / 2) + 2 * q;  // first of the two stored values of 4-group q
+        const int c0 = (codes[r * (cols / 8) + c / 4] >> (2 * (c % 4))) & 3;
+        const int c1 = (codes[r * (cols / 8) + (c + 1) / 4] >> (2 * ((c + 1) % 4))) & 3;
+        bad |= c0 >= c1;
+      }
+    }
+    if (bad) *status = SMY_E_CORRUPT;
+  }
+}
+
+// SEL contract of samoyeds_ssmm: entries in [0, x_rows), strictly increasing.
+__global__ void sel_check_kernel(const int32_t* __restrict__ sel, int32_t n, int64_t x_rows,
+                                 int32_t* __restrict__ status) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t t = sel[i];
+    if (t < 0 || t >= x_rows || (i > 0 && sel[i - 1] >= t)) *status = SMY_E_SELECTION;
+  }
+}
+
+smy_status sel_check_launch(const int32_t* sel, int32_t n, int64_t x_rows, int32_t* d_status, cudaStream_t s) {
+  if (n <= 0) return SMY_OK;
+  int blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  sel_check_kernel<<<blocks, 256, 0, s>>>(sel, n, x_rows, d_status);
+  count_launch();
+  return cuda_status(cudaGetLastError());
+}
+
+smy_status decompress_launch(const smy_weight* src, uint16_t* w, int64_t ldw, int32_t* d_status, cudaStream_t s) {
   const smy_wdesc& d = src->d;
   cudaError_t e = cudaMemset2DAsync(w, (size_t)ldw * 2, 0, (size_t)d.cols * 2, (size_t)d.rows, s);
   if (e != cudaSuccess) return cuda_status(e);
   const int64_t R = d.rows * d.fmt.n / d.fmt.m;
   const int64_t n = R * (d.cols / 2);
   if (n == 0) return SMY_OK;
+  if (d_status != nullptr) {
+    const int64_t gj = (d.rows / d.fmt.m) * (d.cols / d.fmt.v);
+    int cb = (int)((gj + 127) / 128);
+    if (cb > 148 * 16) cb = 148 * 16;
+    decode_check_kernel<<<cb, 128, 0, s>>>(static_cast<const uint8_t*>(src->codes),
+                                           static_cast<const uint8_t*>(src->indices), d.rows / d.fmt.m, d.cols,
+                                           d.fmt.n, d.fmt.m, d.fmt.v, d_status);
+    count_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_status(e);
+  }
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   decompress_kernel<<<blocks, 256, 0, s>>>(static_cast<const uint16_t*>(src->values),

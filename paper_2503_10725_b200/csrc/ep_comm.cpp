@@ -180,6 +180,20 @@ smy_status ep_workspace_bytes(const smy_moe_config* c, int64_t T, int world, siz
   return SMY_OK;
 }
 
+// the largest max_tokens whose EP workspace fits in ws_bytes (the byte count is
+// monotone in T): receive buffers are sized by it, not by the call's T, because a
+// peer may send up to ITS T rows
+static int64_t ep_capacity(const smy_moe_config* c, int world, size_t ws_bytes) {
+  int64_t lo = 0, hi = (int64_t)1 << 24;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) / 2;
+    size_t b = 0;
+    if (ep_workspace_bytes(c, mid, world, &b) == SMY_OK && b <= ws_bytes) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
 smy_status ep_layer(const smy_moe_config* c, const smy_weight* experts, const void* x, const float* logits, int64_t T,
                     float* out, void* workspace, size_t ws_bytes, smy_ep_comm* comm, cudaStream_t s) {
   Nccl* n = nccl();
@@ -189,21 +203,30 @@ smy_status ep_layer(const smy_moe_config* c, const smy_weight* experts, const vo
   if (E % W) return SMY_E_CONFIG;
   smy_moe_config lc = *c;
   lc.num_experts = E / W;
+  // every rank sizes its workspace for the same max_tokens (include/samoyeds.h)
+  const int64_t cap = ep_capacity(c, W, ws_bytes);
   size_t core = 0;
-  smy_status st = moe_workspace_bytes(&lc, T * W, &core);
+  smy_status st = moe_workspace_bytes(&lc, cap * W, &core);
   if (st != SMY_OK) return st;
-  EpWs w = carve_ep(c, T, W, static_cast<uint8_t*>(workspace), core);
-  if (w.total > ws_bytes) return SMY_E_WORKSPACE;
+  EpWs w = carve_ep(c, cap, W, static_cast<uint8_t*>(workspace), core);
+  if (w.total > ws_bytes || w.total == 0) return SMY_E_WORKSPACE;
 
-  // 1. route this rank's tokens over all E experts; plan one copy per destination rank
-  st = route_launch(logits, T, E, k, c->gating, w.ids, w.w, w.r_counts, w.r_offsets, w.r_sel, w.r_gw, w.plan_ws,
-                    w.plan_ws_bytes, nullptr, nullptr, 0, nullptr, s);
-  if (st != SMY_OK) return st;
-  st = ep_plan_launch(w.ids, w.w, T, k, E, W, w.cnt_send, w.off_send, w.sel, w.tag_ids, w.tag_w, w.plan_ws,
-                      w.plan_ws_bytes, s);
-  if (st != SMY_OK) return st;
-  st = ep_pack_launch(static_cast<const uint16_t*>(x), d, d, w.off_send, W, w.sel, T * k, w.x_send, s);
-  if (st != SMY_OK) return st;
+  // 1. route this rank's tokens over all E experts; plan one copy per destination
+  //    rank.  A local failure is announced to every peer in the counts exchange
+  //    (count -1) so that all ranks leave after it and none blocks in NCCL.
+  smy_status local = T > cap ? SMY_E_WORKSPACE : SMY_OK;
+  if (local == SMY_OK)
+    local = route_launch(logits, T, E, k, c->gating, w.ids, w.w, w.r_counts, w.r_offsets, w.r_sel, w.r_gw,
+                         w.plan_ws, w.plan_ws_bytes, nullptr, nullptr, 0, nullptr, s);
+  if (local == SMY_OK)
+    local = ep_plan_launch(w.ids, w.w, T, k, E, W, w.cnt_send, w.off_send, w.sel, w.tag_ids, w.tag_w, w.plan_ws,
+                           w.plan_ws_bytes, s);
+  if (local == SMY_OK)
+    local = ep_pack_launch(static_cast<const uint16_t*>(x), d, d, w.off_send, W, w.sel, T * k, w.x_send, s);
+  if (local != SMY_OK) {
+    cudaGetLastError();
+    if (cudaMemsetAsync(w.cnt_send, 0xFF, W * 4, s) != cudaSuccess) return cuda_status(cudaGetLastError());
+  }
 
   // 2. counts: one int per peer each way, then the host needs them for the split sizes
   n->GroupStart();
@@ -217,12 +240,22 @@ smy_status ep_layer(const smy_moe_config* c, const smy_weight* experts, const vo
   cudaMemcpyAsync(cr.data(), w.cnt_recv, W * 4, cudaMemcpyDeviceToHost, s);
   cudaError_t ce = cudaStreamSynchronize(s);
   if (ce != cudaSuccess) return cuda_status(ce);
+  if (local != SMY_OK) return local;
+  for (int q = 0; q < W; ++q)
+    if (cr[q] < 0) {
+      set_last_error("expert parallelism: a peer rank failed before the dispatch (T > its workspace, or a launch)");
+      return SMY_E_WORKSPACE;
+    }
   std::vector<int64_t> os(W + 1, 0), orr(W + 1, 0);
   for (int q = 0; q < W; ++q) {
     os[q + 1] = os[q] + cs[q];
     orr[q + 1] = orr[q] + cr[q];
   }
   const int64_t R = orr[W];
+  if (R > cap * W) {  // only with mismatched max_tokens across ranks (a caller contract violation)
+    set_last_error("expert parallelism: received rows exceed the workspace (ranks sized for different max_tokens)");
+    return SMY_E_WORKSPACE;
+  }
 
   // 3. dispatch: token rows + tags (local expert ids, gate weights)
   n->GroupStart();
@@ -240,10 +273,11 @@ smy_status ep_layer(const smy_moe_config* c, const smy_weight* experts, const vo
   }
   if ((st = nccl_status(n->GroupEnd())) != SMY_OK) return st;
 
-  // 4. this rank's experts over the received rows -> fp32 partial rows
-  st = moe_core(&lc, experts, nullptr, w.x_recv, nullptr, w.keys_recv, w.vals_recv, R, w.part, w.core_ws,
-                w.core_ws_bytes, s);
-  if (st != SMY_OK) return st;
+  // 4. this rank's experts over the received rows -> fp32 partial rows (a failure
+  //    here still posts the combine below: the peers are waiting for it)
+  const smy_status core_st = moe_core(&lc, experts, nullptr, w.x_recv, nullptr, w.keys_recv, w.vals_recv, R, w.part,
+                                      w.core_ws, w.core_ws_bytes, s);
+  if (core_st != SMY_OK) cudaGetLastError();
 
   // 5. combine: partial rows back to their token's rank, summed into out
   n->GroupStart();
@@ -252,6 +286,7 @@ smy_status ep_layer(const smy_moe_config* c, const smy_weight* experts, const vo
     if (cs[q]) n->Recv(w.back + os[q] * d, (size_t)cs[q] * d, ncclFloat32, q, comm->comm, s);
   }
   if ((st = nccl_status(n->GroupEnd())) != SMY_OK) return st;
+  if (core_st != SMY_OK) return core_st;
   ce = cudaMemsetAsync(out, 0, (size_t)T * d * 4, s);
   if (ce != cudaSuccess) return cuda_status(ce);
   return ep_combine_launch(w.back, d, w.off_send, W, w.sel, T * k, out, s);

@@ -17,6 +17,16 @@ constexpr int kEBytes = 2048;     // E TMEM image per stage
 constexpr int kMaxGroups = 128;   // experts per grouped launch
 constexpr int kMaxPeers = 8;      // ranks of one NVLink/NVSwitch node (expert parallelism)
 
+// widest token tile of the (1,2,V) single-weight kernels (interleaved gate/up, down);
+// a build knob for A/B experiments (probes/), 224 by default
+#ifndef SMY_NT_WIDE
+#define SMY_NT_WIDE 224
+#endif
+// token-ring depth of the SEL-gather pair launches (SPLIT rings)
+#ifndef SMY_TOKEN_SLOTS
+#define SMY_TOKEN_SLOTS 5
+#endif
+
 struct Geometry {
   int64_t R;        // compressed rows = rows * N / M
   int m_tiles, k_stages, planes, rep, block;
@@ -112,7 +122,9 @@ smy_status compact_launch(const int32_t* keys, const float* vals, int64_t T, int
                           const int* tile_mt, int n_tile_cfgs, int32_t* tile_prefix, cudaStream_t s);
 
 // --------------------------------------------------------------- compress
-smy_status decompress_launch(const smy_weight* src, uint16_t* w, int64_t ldw, cudaStream_t s);
+smy_status decompress_launch(const smy_weight* src, uint16_t* w, int64_t ldw, int32_t* d_status, cudaStream_t s);
+smy_status sel_check_launch(const int32_t* sel, int32_t n, int64_t x_rows, int32_t* d_status, cudaStream_t s);
+constexpr int kDebugValidate = 65536;  // SMY_DEBUG bit: validate SEL in samoyeds_ssmm (synchronising)
 // interleaved gate/up weight (reading R20): canonical rows moved, image re-packed
 smy_status interleave_launch(const smy_weight* gate, const smy_weight* up, const smy_wdesc& d, const Geometry& g,
                              smy_weight* gu, cudaStream_t s);

@@ -92,8 +92,20 @@ smy_status moe_workspace_bytes(const smy_moe_config* c, int64_t T, size_t* bytes
   smy_status st = geometry(&d, &g);
   if (st != SMY_OK) return st;
   *bytes = carve(c, T, !interleaved(c) && !gate_up_fused(g), nullptr).total;
+  // bf16 layer output: the fp32 accumulation buffer after the layer's own regions
+  if (c->out_dtype == SMY_BF16) *bytes += align_up((size_t)T * c->hidden * 4, 256);
   return SMY_OK;
 }
+
+namespace {
+__global__ void f32_to_bf16_kernel(const float4* __restrict__ in, int64_t n4, uint2* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = in[i];
+    const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    out[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+  }
+}
+}  // namespace
 
 // grouped SSMM over `groups` weights; tile prefix already on the device
 static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* w1, int groups, const Geometry& g,
@@ -332,8 +344,28 @@ smy_status moe_view(const smy_moe_config* c, int64_t T, void* workspace, size_t 
 }
 
 smy_status moe_layer(const smy_moe_config* c, const smy_weight* experts, const smy_weight* shared, const void* x,
-                     const float* logits, int64_t T, float* out, void* workspace, size_t ws_bytes, cudaStream_t s) {
-  return moe_core(c, experts, shared, x, logits, nullptr, nullptr, T, out, workspace, ws_bytes, s);
+                     const float* logits, int64_t T, void* out, void* workspace, size_t ws_bytes, cudaStream_t s) {
+  if (c->out_dtype != SMY_BF16)
+    return moe_core(c, experts, shared, x, logits, nullptr, nullptr, T, static_cast<float*>(out), workspace, ws_bytes,
+                    s);
+  // bf16 output: accumulate in fp32 at the end of the workspace, round once
+  smy_moe_config cf = *c;
+  cf.out_dtype = SMY_F32;
+  size_t core = 0;
+  smy_status st = moe_workspace_bytes(&cf, T, &core);
+  if (st != SMY_OK) return st;
+  core = align_up(core, 256);
+  const size_t acc_bytes = (size_t)T * c->hidden * 4;
+  if (core + acc_bytes > ws_bytes) return SMY_E_WORKSPACE;
+  float* acc = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + core);
+  st = moe_core(&cf, experts, shared, x, logits, nullptr, nullptr, T, acc, workspace, core, s);
+  if (st != SMY_OK || T == 0) return st;
+  const int64_t n4 = T * c->hidden / 4;
+  int blocks = (int)((n4 + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  f32_to_bf16_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(acc), n4, static_cast<uint2*>(out));
+  count_launch();
+  return cuda_status(cudaGetLastError());
 }
 
 }  // namespace smy

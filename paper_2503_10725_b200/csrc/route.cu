@@ -29,6 +29,7 @@ __device__ __forceinline__ void topk_warp(const float* __restrict__ lg, int E, i
   for (int j = 0; j < V; ++j) {
     const int e = lane + 32 * j;
     v[j] = e < E ? lg[e] : -INFINITY;
+    if (isnan(v[j])) v[j] = -INFINITY;  // a NaN logit ranks as -inf (include/samoyeds.h, samoyeds_route)
     rank[j] = 0;
   }
 #pragma unroll
@@ -93,7 +94,7 @@ __device__ __forceinline__ void build_masks(const int32_t* __restrict__ ids, int
   if (t < T)
     for (int i = 0; i < k; ++i) {
       const int key = ids[t * k + i];
-      if (key >= 0) atomicOr(&mask[w][key], 1u << l);  // negative keys: no entry
+      if (key >= 0 && key < E) atomicOr(&mask[w][key], 1u << l);  // keys outside [0, E): no entry
     }
   __syncthreads();
 }
@@ -214,7 +215,7 @@ __global__ void route_small_kernel(const float* __restrict__ logits, int64_t T, 
   const uint32_t lt = (1u << lane) - 1u;
   for (int i = 0; i < k; ++i) {
     const int e = ids[(int64_t)t * k + i];
-    if (e < 0) continue;
+    if (e < 0 || e >= E) continue;
     const int pos = wbase[wp][e] + __popc(mask[wp][e] & lt);
     sel[pos] = t;
     gw[pos] = w[(int64_t)t * k + i];
@@ -267,7 +268,7 @@ __global__ void route_scatter_kernel(const int32_t* __restrict__ ids, const floa
   const uint32_t lt = (1u << l) - 1u;
   for (int i = 0; i < k; ++i) {
     const int e = ids[t * k + i];
-    if (e < 0) continue;
+    if (e < 0 || e >= E) continue;
     const int pos = wbase[ww][e] + __popc(mask[ww][e] & lt);
     sel[pos] = (int32_t)t;
     gw[pos] = w[t * k + i];

@@ -7,7 +7,7 @@ extern template smy_status launch_t<16,1,2,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<32,1,2,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<64,1,2,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<128,1,2,1>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_t<224,1,2,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<SMY_NT_WIDE,1,2,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<16,2,2,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<32,2,2,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<64,2,2,1>(const SsmmArgs&, cudaStream_t);
@@ -33,8 +33,8 @@ extern template smy_status launch_t<16,2,8,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<64, 2, 2, 0>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<112, 2, 2, 0>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<128, 1, 2, 0>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<224, 1, 2, 0>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<224, 1, 2, 1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<SMY_NT_WIDE, 1, 2, 0>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<SMY_NT_WIDE, 1, 2, 1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<128, 1, 1, 0>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<256, 1, 1, 0>(const SsmmArgs&, cudaStream_t);
 
@@ -45,7 +45,7 @@ const Entry kTable[] = {
     {32, 1, 2, 1, &launch_t<32,1,2,1>},
     {64, 1, 2, 1, &launch_t<64,1,2,1>},
     {128, 1, 2, 1, &launch_t<128,1,2,1>},
-    {224, 1, 2, 1, &launch_t<224,1,2,1>},
+    {SMY_NT_WIDE, 1, 2, 1, &launch_t<SMY_NT_WIDE,1,2,1>},
     {16, 2, 2, 1, &launch_t<16,2,2,1>},
     {32, 2, 2, 1, &launch_t<32,2,2,1>},
     {64, 2, 2, 1, &launch_t<64,2,2,1>},
@@ -85,7 +85,7 @@ int ssmm_pair_cluster(int nt, int nw, int ms, int rep, int m_tiles, int64_t toke
   if (debug_flags() & 16) return 0;  // SMY_DEBUG=16: force the single-CTA kernel
   // an odd m-tile count gives the last pair a phantom peer tile (loads repeated, stores masked)
   if (rep != 1 || m_tiles < 2 || tokens_per_group < 64) return 0;
-  if (ms == 2 && !(nw == 2 ? (nt == 64 || nt == 112) : (nt == 128 || nt == 224))) return 0;
+  if (ms == 2 && !(nw == 2 ? (nt == 64 || nt == 112) : (nt == 128 || nt == SMY_NT_WIDE))) return 0;
   if (ms == 1 && !(nw == 1 && (nt == 128 || nt == 256))) return 0;  // N == M: plain 2:4
   if (ms != 1 && ms != 2) return 0;
   // (4-CTA clusters sharing weight stages by multicast measured 2x slower on
@@ -153,8 +153,8 @@ smy_status ssmm_launch_pair(const SsmmArgs& a0, int nt, int nw, int ms, int cl, 
   if (ms == 2 && nw == 2 && nt == 112) return launch_pair_t<112, 2, 2, 0>(a, s);
   if (ms == 2 && nw == 1 && nt == 128) return launch_pair_t<128, 1, 2, 0>(a, s);
   // SEL-gathered token rows (gate/up): separate, deeper token ring
-  if (ms == 2 && nw == 1 && nt == 224) return a.sel_in && !(a.debug & 16384) ? launch_pair_t<224, 1, 2, 1>(a, s)
-                                                                              : launch_pair_t<224, 1, 2, 0>(a, s);
+  if (ms == 2 && nw == 1 && nt == SMY_NT_WIDE) return a.sel_in && !(a.debug & 16384) ? launch_pair_t<SMY_NT_WIDE, 1, 2, 1>(a, s)
+                                                                              : launch_pair_t<SMY_NT_WIDE, 1, 2, 0>(a, s);
   if (ms == 1 && nw == 1 && nt == 128) return launch_pair_t<128, 1, 1, 0>(a, s);
   if (ms == 1 && nw == 1 && nt == 256) return launch_pair_t<256, 1, 1, 0>(a, s);
   set_last_error("ssmm: unsupported pair (nt, nw)");

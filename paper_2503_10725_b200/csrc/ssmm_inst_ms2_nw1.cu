@@ -6,5 +6,5 @@ template smy_status launch_t<16,1,2,1>(const SsmmArgs&, cudaStream_t);
 template smy_status launch_t<32,1,2,1>(const SsmmArgs&, cudaStream_t);
 template smy_status launch_t<64,1,2,1>(const SsmmArgs&, cudaStream_t);
 template smy_status launch_t<128,1,2,1>(const SsmmArgs&, cudaStream_t);
-template smy_status launch_t<224,1,2,1>(const SsmmArgs&, cudaStream_t);
+template smy_status launch_t<SMY_NT_WIDE,1,2,1>(const SsmmArgs&, cudaStream_t);
 }  // namespace smy

@@ -191,7 +191,7 @@ struct PairCfg {
   // split rings: 5 token slots (measured: their depth matters more than the weights'),
   // the rest of shared memory to weight slots
   static constexpr int kBFit = (kSmemCap - 3 * kWStage) / kBStage;
-  static constexpr int kBStages = SPLIT ? (5 < kBFit ? 5 : kBFit) : kStages;
+  static constexpr int kBStages = SPLIT ? (SMY_TOKEN_SLOTS < kBFit ? SMY_TOKEN_SLOTS : kBFit) : kStages;
   static constexpr int kWStagesRaw = SPLIT ? (kSmemCap - kBStages * kBStage) / kWStage : kStages;
   static constexpr int kWStages = kWStagesRaw > 8 ? 8 : kWStagesRaw;
   static constexpr int kSmemBytes = kWStages * kWStage + kBStages * kBStage + 1024 + kAux;
@@ -225,6 +225,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   const bool gather = a.sel_in != nullptr;
   const int warp = warp_id(), lane = lane_id();
   uint8_t* zbuf = aux + 1024;  // 1 KB of zeros: the operand of the accumulator-clearing MMA
+  // TMEM allocation first, ordered before every other shared-memory write of the
+  // prologue (compute-sanitizer racecheck flagged the allocator's slot write
+  // against the prologue's stores when they were unordered)
+  if (warp_id() == 5) tmem_alloc2(tmem_slot, C::kTmemCols);
+  __syncthreads();
   if (threadIdx.x < 256) {
     reinterpret_cast<uint32_t*>(zbuf)[threadIdx.x] = 0u;
     fence_proxy_async_smem();
@@ -255,7 +260,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     }
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc2(tmem_slot, C::kTmemCols);
   tc_fence_before();
   __syncthreads();
   cluster_sync_all();  // both CTAs' barriers exist before any remote arrive

@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(320, 1) bench(const __grid_constant__ CUtensor
   uint32_t crank = 0;
   if (mode == 4) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) { mbar_init(&full[s], mode == 2 ? 4 : mode == 5 ? 8 : mode == 6 ? 4 : 1); mbar_init(&empty[s], mode == 4 ? 4 : 1); }
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], (mode == 2 || mode == 8) ? (mode == 8 ? 5 : 4) : mode == 5 ? 8 : mode == 6 ? 4 : 1); mbar_init(&empty[s], mode == 4 ? 4 : 1); }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   __syncthreads();
@@ -86,8 +86,28 @@ __global__ void __launch_bounds__(320, 1) bench(const __grid_constant__ CUtensor
       __syncwarp();
       if (lane == 0) arrive(&full[st]);
     }
-  } else if (mode == 2 && warp < 4) {
-    const int tid = threadIdx.x;
+  } else if (mode == 8 && warp == 4) {
+    // hybrid: rows [0, kG) of every stage by tile::gather4 from one thread
+    constexpr int kG = 16;
+    for (int it = 0; it < iters; ++it) {
+      const int st = it % S;
+      wait(&empty[st], ((it / S) & 1) ^ 1);
+      uint8_t* b = sm + st * STAGE;
+      const int col0 = (it * 128) % (ldx - 128);
+      if (lane == 0) {
+        arrive_tx(&full[st], kG * 256);
+        for (int g = 0; g < kG / 4; ++g)
+          for (int atom = 0; atom < 2; ++atom) {
+            const int* r = sel + base + 4 * g;
+            asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                         " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(su(b + atom * NT * 128 + g * 512)), "l"(&gmap),
+                         "r"(col0 + atom * 64), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(su(&full[st]))
+                         : "memory");
+          }
+      }
+    }
+  } else if ((mode == 2 || mode == 8) && warp < 4) {
+    const int tid = threadIdx.x + (mode == 8 ? 16 * 16 : 0);  // mode 8: rows from kG = 16 on
     for (int it = 0; it < iters; ++it) {
       const int st = it % S;
       wait(&empty[st], ((it / S) & 1) ^ 1);
@@ -104,7 +124,7 @@ __global__ void __launch_bounds__(320, 1) bench(const __grid_constant__ CUtensor
       __syncwarp();
       if (lane == 0) arrive(&full[st]);
     }
-  } else if (warp == 4 && mode != 2 && mode < 5) {
+  } else if (warp == 4 && mode != 2 && mode != 8 && (mode < 5 || mode == 7)) {
     for (int it = 0; it < iters; ++it) {
       const int st = it % S;
       wait(&empty[st], ((it / S) & 1) ^ 1);
@@ -127,7 +147,16 @@ __global__ void __launch_bounds__(320, 1) bench(const __grid_constant__ CUtensor
       } else {
         if (lane == 0) arrive_tx(&full[st], STAGE);
         __syncwarp();
-        if (mode == 0) {
+        if (mode == 7 && lane == 0) {  // one thread issues every gather4 of the stage
+          for (int g = 0; g < NT / 4; ++g)
+            for (int atom = 0; atom < 2; ++atom) {
+              const int* r = sel + base + 4 * g;
+              asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                           " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(su(b + atom * NT * 128 + g * 512)), "l"(&gmap),
+                           "r"(col0 + atom * 64), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(su(&full[st]))
+                           : "memory");
+            }
+        } else if (mode == 0) {
           for (int g = lane; g < NT / 4; g += 32)
             for (int atom = 0; atom < 2; ++atom) {
               const int* r = sel + base + 4 * g;
@@ -184,8 +213,8 @@ int main() {
   const int smem = S * STAGE + 2048;
   CK(cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int iters = 2000;
-  const char* names[] = {"gather4", "tma-row", "cp.async", "tma-tile(contig)", "gather4-mcast4", "cp.async-8w", "cp.async-2x4w-alt"};
-  for (int mode = 2; mode < 7; ++mode) { if (mode == 4) continue;
+  const char* names[] = {"gather4", "tma-row", "cp.async", "tma-tile(contig)", "gather4-mcast4", "cp.async-8w", "cp.async-2x4w-alt", "gather4-1thread", "hybrid g4x16+cp.async"};
+  for (int mode = 0; mode < 9; ++mode) { if (mode == 4 || mode == 1 || mode == 5 || mode == 6) continue;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(148); cfg.blockDim = dim3(320); cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];

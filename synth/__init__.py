@@ -5,7 +5,8 @@ the CUDA product path (``paper_2503_10725_b200``).  It holds none of the
 Samoyeds method's arithmetic: it only turns (seed, flat index) into input
 values.  The CUDA library carries a twin of the same generator
 (``csrc/synth.cu``, exported as ``smy_synth_fill``) so that multi-GB weights can
-be generated on the device; ``tests/test_synth.py`` pins the two bit-exactly.
+be generated on the device; ``tests/test_gpu_parity.py::test_synth_twin_bit_exact``
+pins the two bit-exactly.
 
 Generator: a splitmix64-style finaliser over ``key(seed) + (i + 1) * PHI``.
 Every distribution below is computed with exactly representable integer steps

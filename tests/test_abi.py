@@ -88,3 +88,50 @@ def test_moe_workspace_query(lib):
     b = C.c_size_t()
     check(lib.smy_moe_workspace_bytes(C.byref(cfg), 4096, C.byref(b)), "ws")
     assert b.value >= 4096 * 2 * 14336 * 2                         # the bf16 intermediate
+
+
+def _fake_weight(rows, cols, fmt, addr):
+    """an smy_weight whose (never dereferenced) device pointers are `addr`"""
+    from paper_2503_10725_b200._lib import smy_format, smy_wdesc, smy_weight
+    p = C.c_void_p(addr)
+    return smy_weight(smy_wdesc(rows, cols, smy_format(*fmt)), p, p, p, p)
+
+
+def test_ssmm_scatter_alignment_rejected_without_gpu(lib):
+    """SCATTER_ADD reduces 16 B per lane pair: ldo % 4, a 16-B aligned out and
+    rows % 4 are checked on the host, before the arch check."""
+    w = _fake_weight(256, 256, (1, 2, 32), 0x10000)
+    p = C.c_void_p(0x20000)
+    # ldo = 258 (even, >= rows, not % 4)
+    assert lib.samoyeds_ssmm(C.byref(w), None, p, 256, 64, p, 16, None, 2, p, 258, 0, None) == 2
+    # out 8-B aligned only
+    assert lib.samoyeds_ssmm(C.byref(w), None, p, 256, 64, p, 16, None, 2, C.c_void_p(0x20008), 256, 0, None) == 2
+    # rows = 258 (% M == 0, not % 4)
+    w2 = _fake_weight(258, 256, (1, 2, 32), 0x10000)
+    assert lib.samoyeds_ssmm(C.byref(w2), None, p, 256, 64, p, 16, None, 2, p, 260, 0, None) == 2
+
+
+def test_interleave_rejects_formats_without_16_row_blocks(lib):
+    """samoyeds_interleave_gate_up moves blocks of 16 compressed rows: weights with
+    R = rows * N / M not a multiple of 16 are rejected (the oracle's
+    interleave_gate_up requires rows % (16 M / N))."""
+    for fmt, rows, want in (((1, 4, 32), 32, 2), ((1, 8, 32), 64, 2), ((1, 2, 32), 48, 2)):
+        g = _fake_weight(rows, 256, fmt, 0x10000)
+        u = _fake_weight(rows, 256, fmt, 0x20000)
+        gu = _fake_weight(2 * rows, 256, fmt, 0x30000)
+        assert lib.samoyeds_interleave_gate_up(C.byref(g), C.byref(u), C.byref(gu), None) == want, fmt
+
+
+def test_moe_layer_rejects_unknown_gating_and_misaligned_out(lib):
+    from paper_2503_10725_b200 import MoEConfig, Format
+    from paper_2503_10725_b200._lib import smy_weight
+    ws = (smy_weight * 24)()
+    p = C.c_void_p(0x10000)
+    cfg = MoEConfig(8, 2, 256, 256, fmt=Format(1, 2, 32)).c()
+    cfg.gating = 7
+    assert lib.samoyeds_moe_layer(C.byref(cfg), ws, None, p, p, 16, p, p, 16, None, None) == 3
+    cfg.gating = 0
+    assert lib.samoyeds_moe_layer(C.byref(cfg), ws, None, p, p, 16, C.c_void_p(0x10004), p, 16, None, None) == 2
+    # samoyeds_moe_experts has no shared experts
+    cfg.num_shared = 1
+    assert lib.samoyeds_moe_experts(C.byref(cfg), ws, p, 16, p, p, p, p, 16, None) == 3

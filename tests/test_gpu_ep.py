@@ -234,6 +234,21 @@ def test_ep_c_abi_nccl_world1(smy):
         ref, S = moe.moe_layer(encs, x, lg, k)
         assert OS.rel_fro(got - ref, ref) <= 1e-3
         assert (np.abs(got - ref) <= 1e-2 * S + 1e-30).all()
+        # T above the workspace's max_tokens: announced in the counts exchange (count
+        # -1) and returned as SMY_E_WORKSPACE after it, on every rank
+        import ctypes as C
+        from paper_2503_10725_b200 import _lib
+        T2 = T + 57
+        x2 = dev16(synth.activations_bf16(synth.SEED_X, T2, d))
+        lg2 = torch.from_numpy(synth.router_logits(synth.SEED_LOGITS, T2, E)).cuda()
+        out2 = torch.empty(T2, d, dtype=torch.float32, device="cuda")
+        st = _lib.load().samoyeds_moe_layer(C.byref(layer._cfg), layer._arr, None, x2.data_ptr(), lg2.data_ptr(), T2,
+                                            out2.data_ptr(), layer.workspace.data_ptr(), layer.workspace.numel(),
+                                            comm.handle, None)
+        assert st == 7, st
+        # the communicator still works afterwards (no rank left inside NCCL)
+        again = layer(dev16(x), torch.from_numpy(lg).cuda()).cpu().numpy().astype(np.float64)
+        assert OS.rel_fro(again - ref, ref) <= 1e-3
     finally:
         if comm is not None:
             comm.close()

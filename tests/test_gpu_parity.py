@@ -417,6 +417,37 @@ def test_moe_layer_prefill_pair_kernels(smy, case):
     check_tol(got, ref, S, "moe layer (pair kernels)")
 
 
+@pytest.mark.parametrize("T", [1, 100, 600])
+def test_moe_layer_bf16_output(smy, T):
+    """cfg.out_dtype = bf16 (reading R13: optional bf16 layer output, compared
+    after emulated rounding): fp32 accumulation, one RNE rounding -- against the
+    oracle's output rounded to bf16: rel Frobenius <= 1e-3 and every element
+    within one bf16 ulp plus the north-star per-element bound."""
+    fmt = F.SparseFormat(1, 2, 32)
+    E, d, f, k = 8, 256, 512, 2
+    encs, sws = [], []
+    for e in range(E):
+        te, ts = [], []
+        for i in range(3):
+            r, c = (f, d) if i < 2 else (d, f)
+            w = synth.weight_bf16(synth.weight_seed(e, i), r, c)
+            te.append(F.encode(F.prune(w, fmt), fmt))
+            ts.append(smy.compress(dev16(w), gpu_format(fmt))[0])
+        encs.append(tuple(te))
+        sws.append(tuple(ts))
+    x = synth.activations_bf16(synth.SEED_X, T, d)
+    lg = synth.router_logits(synth.SEED_LOGITS, T, E)
+    layer = smy.MoELayer(smy.MoEConfig(E, k, d, f, out_dtype="bf16"), sws, max_tokens=T)
+    out = layer(dev16(x), torch.from_numpy(lg).cuda())
+    assert out.dtype == torch.bfloat16 and tuple(out.shape) == (T, d)
+    got = bf16.to_f64(host16(out.view(torch.int16)))
+    ref64, S = moe.moe_layer(encs, x, lg, k)
+    ref = bf16.to_f64(bf16.from_f64(ref64))
+    assert OS.rel_fro(got - ref, ref) <= REL_FRO
+    bad = np.abs(got - ref) > np.maximum(bf16_ulp(ref), bf16_ulp(got)) + ELEM * S + 1e-30
+    assert not bad.any(), np.argwhere(bad)[:3]
+
+
 def test_moe_layer_all_tokens_one_expert(smy):
     fmt = F.SparseFormat(1, 2, 32)
     got, ref, S = _layer_case(smy, fmt, E=4, d=128, f=256, T=200, k=1, skew=50.0)

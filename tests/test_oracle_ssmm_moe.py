@@ -178,6 +178,12 @@ def test_route_gate_weights_closed_form():
     assert np.allclose(w[0], [5 / 15, 4 / 15, 3 / 15], rtol=1e-6, atol=0)
     ids, w = moe.route(lg, 3, moe.RENORM_TOPK)
     assert np.allclose(w[0], [5 / 12, 4 / 12, 3 / 12], rtol=1e-6, atol=0)
+    # a NaN logit ranks as -inf (R10b): selected after every finite logit, weight 0
+    lg = np.array([[np.nan, np.log(2.0), 0.0, np.nan]], dtype=np.float32)
+    ids, w = moe.route(lg, 3, moe.SOFTMAX_ALL)
+    assert ids[0].tolist() == [1, 2, 0] and np.allclose(w[0], [2 / 3, 1 / 3, 0.0], rtol=1e-6, atol=0)
+    ids, w = moe.route(lg, 2, moe.RENORM_TOPK)
+    assert ids[0].tolist() == [1, 2] and np.allclose(w[0], [2 / 3, 1 / 3], rtol=1e-6, atol=0)
     # ties -> lower id (R10), weights equal
     ids, w = moe.route(np.zeros((1, 4), dtype=np.float32), 2, moe.SOFTMAX_ALL)
     assert ids[0].tolist() == [0, 1] and np.allclose(w[0], [0.25, 0.25], rtol=1e-12)
