@@ -479,13 +479,20 @@ def run_ours(args):
     # timed region; as in a serving loop, step s+1's upload and step s-1's
     # download run on copy streams beside step s's compute (double-buffered
     # device tensors, event-ordered), so e2e = max(PCIe, compute) when they overlap.
+    # The single-GPU layer returns bf16 here (cfg.out_dtype = "bf16": fp32 accumulation,
+    # one rounding -- what the next layer of a model consumes), halving the PCIe
+    # download; the expert-parallel layer returns fp32.
     nb = 2
+    e2e_bf16 = not ep and not args.e2e_f32
+    e_layer = (P.MoELayer(P.MoEConfig(E, k, d, f, NS, gating, P.Format(*FMT), "auto", args.transcode, "bf16"),
+                          layer.experts, shared=layer.shared, max_tokens=T, device=device) if e2e_bf16 else layer)
+    out_dt = torch.bfloat16 if e2e_bf16 else torch.float32
     x_h = x.cpu().pin_memory()
     lg_h = lg.cpu().pin_memory()
-    out_h = [torch.empty(T, d, dtype=torch.float32).pin_memory() for _ in range(nb)]
+    out_h = [torch.empty(T, d, dtype=out_dt).pin_memory() for _ in range(nb)]
     xs = [x] + [torch.empty_like(x) for _ in range(nb - 1)]
     lgs = [lg] + [torch.empty_like(lg) for _ in range(nb - 1)]
-    outs = [out] + [torch.empty_like(out) for _ in range(nb - 1)]
+    outs = [torch.empty(T, d, dtype=out_dt, device=device) for _ in range(nb)]
     h2d, d2h = torch.cuda.Stream(device), torch.cuda.Stream(device)
     ev_in = [torch.cuda.Event() for _ in range(nb)]
     ev_done = [torch.cuda.Event() for _ in range(nb)]
@@ -502,7 +509,7 @@ def run_ours(args):
         stream.wait_event(ev_in[i])
         if s_ >= nb:
             stream.wait_event(ev_free[i])         # step s-nb's output has been downloaded
-        layer(xs[i], lgs[i], outs[i])
+        e_layer(xs[i], lgs[i], outs[i])
         ev_done[i].record(stream)
         with torch.cuda.stream(d2h):
             d2h.wait_event(ev_done[i])
@@ -555,8 +562,12 @@ def run_ours(args):
              "peak_source": f"2 x {src} bf16 dense burst ({bf16_burst} TF/s)"} if tensor_bound else
             {"bound": "hbm", "achieved": ach_gbs, "peak": hbm, "unit": "GB/s", "frac": ach_gbs / hbm,
              "traffic": None, "peak_source": f"{src} hbm_gbs"})
-    roof["traffic"] = ncu_traffic(model, T, gate_up_kernel(T * k // E, f))
-    roof.update({"kernel": gate_up_kernel(T * k // E, f) + " interleaved gate/up (fused SiLU*up)",
+    # the kernel the library launched (its own tile / CTA-pair decisions); under EP
+    # the local experts' launch is approximated by the same rule on T*k/E rows each
+    gu_name = (layer.kernel_names(T)[0] if isinstance(layer, P.MoELayer) and layer.comm is None
+               else gate_up_kernel(T * k // E, f))
+    roof["traffic"], roof["traffic_source"] = ncu_traffic(model, T, gu_name, NS)
+    roof.update({"kernel": gu_name + " interleaved gate/up (fused SiLU*up)",
                  "per_launch_ms": ph_ms[2],
                  "algorithmic_flops": flops_gu, "algorithmic_bytes": bytes_gu,
                  "other_view": ({"achieved_gbs": ach_gbs, "hbm_frac": ach_gbs / hbm} if tensor_bound else
@@ -587,7 +598,8 @@ def run_ours(args):
         "down_ssmm_tflops": (flops_gu / 2) / (ph_ms[3] * 1e-3) / 1e12,
         "roofline": roof,
         "e2e": {"value": T * world / (ms_e2e * 1e-3), "unit": "tokens/s",
-                "h2d_bytes_per_step": T * d * 2 + T * E * 4, "d2h_bytes_per_step": T * d * 4,
+                "h2d_bytes_per_step": T * d * 2 + T * E * 4, "d2h_bytes_per_step": T * d * (2 if e2e_bf16 else 4),
+                "out_dtype": "bf16" if e2e_bf16 else "f32",
                 "overlap": "copies of steps s+1 / s-1 on separate streams beside step s (double-buffered)"},
         "decode": dec,
         "gpu_launches": int(launches),
@@ -623,17 +635,21 @@ def gate_up_kernel(tokens_per_expert, f):
     return "ssmm_kernel<%d, 1, 2, 1>" % nt
 
 
-def ncu_traffic(model, T, kernel):
-    """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel from the
-    committed ncu --set full capture (profiles/r1_ncu_summary.json), or None."""
-    p = os.path.join(ROOT, "profiles", "r1_ncu_summary.json")
-    if not os.path.exists(p):
-        return None
-    tag = "%s_T%d: void %s" % (model, T, kernel)
-    for k, v in json.load(open(p))["kernels"].items():
-        if k.startswith(tag):
-            return v["dram_read"] + v["dram_write"]
-    return None
+def ncu_traffic(model, T, kernel, shared=0):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, per
+    launch, from the committed ncu --set full capture of this workload
+    (profiles/r2_ncu_summary.json, written by probes/ncu_summary.py from
+    probes/capture_r2.sh), keyed by the kernel name the library reports
+    (smy_moe_kernel_names); (None, why) when there is no capture."""
+    for rnd in ("r2", "r1"):
+        p = os.path.join(ROOT, "profiles", f"{rnd}_ncu_summary.json")
+        if not os.path.exists(p):
+            continue
+        tag = "%s_T%d%s: void %s" % (model, T, f"_sh{shared}" if shared else "", kernel)
+        for key, v in json.load(open(p))["kernels"].items():
+            if key.startswith(tag):
+                return v["dram_read"] + v["dram_write"], f"profiles/{rnd}_ncu_summary.json [{key}]"
+    return None, f"no ncu capture of {model} T={T} {kernel} in profiles/"
 
 
 class stdout_to_stderr:
@@ -684,6 +700,7 @@ def main():
     ap.add_argument("--ep-transport", default="nccl", choices=["nccl", "torch", "peer"],
                     help="EP token/output transport: the library's NCCL communicator (default), torch "
                          "all_to_all_single, or NVLink peer memory inside the kernels")
+    ap.add_argument("--e2e-f32", action="store_true", help="e2e leg with the fp32 layer output (default bf16)")
     ap.add_argument("--dry-run", action="store_true",
                     help="launch / process-group / timing path only, on CPU (gloo): prints the contract line")
     ap.add_argument("--shared", type=int, default=0,

@@ -320,6 +320,11 @@ typedef struct {
   int64_t inter_rows;
   int32_t groups;
 } smy_moe_view;
+/* smy_moe_kernel_names: the names (as profilers print them, e.g.
+ * "ssmm_pair_kernel<224, 1, 2, 1>") of the gate/up and down SSMM kernels a
+ * single-GPU samoyeds_moe_layer call over T tokens launches -- the same tile and
+ * CTA-pair decisions as the call itself (host only; len >= 48).             */
+SMY_API smy_status smy_moe_kernel_names(const smy_moe_config* cfg, int64_t T, char* gate_up, char* down, int32_t len);
 SMY_API smy_status smy_moe_workspace_view(const smy_moe_config* cfg, int64_t T, void* workspace, size_t ws_bytes,
                                           smy_moe_view* view);
 

@@ -86,6 +86,7 @@ SIGNATURES = {
     "smy_ep_comm_destroy": (C.c_int, [C.c_void_p]),
     "smy_moe_ep_workspace_bytes": (C.c_int, [C.POINTER(smy_moe_config), C.c_int64, C.c_int32,
                                              C.POINTER(C.c_size_t)]),
+    "smy_moe_kernel_names": (C.c_int, [C.POINTER(smy_moe_config), C.c_int64, C.c_char_p, C.c_char_p, C.c_int32]),
     "smy_moe_workspace_view": (C.c_int, [C.POINTER(smy_moe_config), C.c_int64, C.c_void_p, C.c_size_t,
                                          C.POINTER(smy_moe_view)]),
     "smy_moe_set_phase_events": (C.c_int, [C.c_void_p, C.c_int]),

@@ -329,6 +329,13 @@ class MoELayer:
                                      _stream(stream)), "samoyeds_moe_layer")
         return out
 
+    def kernel_names(self, T: int):
+        """smy_moe_kernel_names: (gate/up, down) SSMM kernel names of a call over T tokens."""
+        lib = _lib.load()
+        gu, dn = C.create_string_buffer(96), C.create_string_buffer(96)
+        check(lib.smy_moe_kernel_names(C.byref(self._cfg), T, gu, dn, 96), "smy_moe_kernel_names")
+        return gu.value.decode(), dn.value.decode()
+
     def view(self, T: int):
         """smy_moe_workspace_view: the routing result and the compact bf16 gate/up
         intermediate the last single-GPU call over T tokens left in the

@@ -111,6 +111,7 @@ smy_status moe_workspace_bytes(const smy_moe_config* c, int64_t T, size_t* bytes
 smy_status moe_layer(const smy_moe_config* c, const smy_weight* experts, const smy_weight* shared, const void* x,
                      const float* logits, int64_t T, void* out, void* workspace, size_t ws_bytes, cudaStream_t s);
 smy_status moe_view(const smy_moe_config* c, int64_t T, void* workspace, size_t ws_bytes, smy_moe_view* v);
+smy_status moe_kernel_names(const smy_moe_config* c, int64_t T, char* gu, char* dn, int len);
 
 }  // namespace smy
 
@@ -413,6 +414,13 @@ smy_status samoyeds_moe_layer(const smy_moe_config* cfg, const smy_weight* exper
                    static_cast<cudaStream_t>(stream));
 }
 
+
+smy_status smy_moe_kernel_names(const smy_moe_config* cfg, int64_t T, char* gate_up, char* down, int32_t len) {
+  if (!cfg || !gate_up || !down) return SMY_E_NULL;
+  if (T < 0 || len < 48) return SMY_E_SHAPE;
+  if (cfg->num_experts < 1 || cfg->top_k < 1) return SMY_E_CONFIG;
+  return moe_kernel_names(cfg, T, gate_up, down, len);
+}
 
 smy_status smy_moe_workspace_view(const smy_moe_config* cfg, int64_t T, void* workspace, size_t ws_bytes,
                                   smy_moe_view* view) {

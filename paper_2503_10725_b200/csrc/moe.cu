@@ -13,6 +13,7 @@
 #include <cuda_bf16.h>
 
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 
 #include "internal.h"
@@ -321,6 +322,38 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
     if (st != SMY_OK) return st;
   }
   record_phase(5, s);
+  return SMY_OK;
+}
+
+// The SSMM kernels a single-GPU layer call over T tokens launches (the same
+// tile-width / CTA-pair decisions as moe_core, weight images in one block as
+// prepare_experts lays them out): names as the profiler prints them.
+smy_status moe_kernel_names(const smy_moe_config* c, int64_t T, char* gu, char* dn, int len) {
+  const bool ilv = interleaved(c);
+  smy_wdesc dgu{ilv ? 2 * c->ffn : c->ffn, c->hidden, c->fmt}, ddn{c->hidden, c->ffn, c->fmt};
+  Geometry ggu, gdn;
+  smy_status st;
+  if ((st = geometry(&dgu, &ggu)) != SMY_OK) return st;
+  if ((st = geometry(&ddn, &gdn)) != SMY_OK) return st;
+  const bool fused = ilv || gate_up_fused(ggu);
+  const int nw_gu = ilv ? 1 : fused ? 2 : 1;
+  const int Er = c->num_experts, kr = c->top_k;
+  const int64_t tpg = Er ? (T * kr + Er - 1) / Er : 0;
+  const int64_t tpg_hi = tpg + (int64_t)(3.0 * sqrt((double)tpg) + 0.999);
+  const int nt_gu = ssmm_pick_nt(nw_gu, ggu.ms, ggu.rep, tpg_hi);
+  const int nt_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, tpg_hi);
+  const int cl_gu = fused ? ssmm_pair_cluster(nt_gu, nw_gu, ggu.ms, ggu.rep, ggu.m_tiles, tpg) : 0;
+  const int cl_dn = ssmm_pair_cluster(nt_dn, 1, gdn.ms, gdn.rep, gdn.m_tiles, tpg);
+  // the SEL-gather pair launch of the widest (1,2,V) tile runs split rings (ssmm.cu)
+  const int split_gu = cl_gu && ggu.ms == 2 && nw_gu == 1 && nt_gu == SMY_NT_WIDE && !(debug_flags() & 16384);
+  if (cl_gu)
+    snprintf(gu, len, "ssmm_pair_kernel<%d, %d, %d, %d>", nt_gu, nw_gu, ggu.ms, split_gu);
+  else
+    snprintf(gu, len, "ssmm_kernel<%d, %d, %d, %d>", nt_gu, nw_gu, ggu.ms, ggu.rep);
+  if (cl_dn)
+    snprintf(dn, len, "ssmm_pair_kernel<%d, %d, %d, %d>", nt_dn, 1, gdn.ms, 0);
+  else
+    snprintf(dn, len, "ssmm_kernel<%d, %d, %d, %d>", nt_dn, 1, gdn.ms, gdn.rep);
   return SMY_OK;
 }
 

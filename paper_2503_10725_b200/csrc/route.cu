@@ -14,12 +14,6 @@ constexpr int kRouteWarps = kRouteThreads / 32;
 constexpr int kMaxK = 16;  // top-k plus appended shared experts
 constexpr int kMaxE = 256;
 
-// One warp per token: lane l holds logits l, l+32, ... (coalesced).  Each
-// element's rank = #{elements with a larger logit, or an equal logit and a
-// lower expert id} (ties keep the lower id, R10) is counted against all E
-// values broadcast by shuffles -- independent, pipelined steps instead of k
-// dependent argmax rounds.  Elements of rank < k are the top-k, in order.
-// Writes ids / gate weights of token row `t` directly.
 template <int V>
 __device__ __forceinline__ void topk_warp(const float* __restrict__ lg, int E, int k, int gating, int lane,
                                           int32_t* __restrict__ ids, float* __restrict__ w) {
@@ -170,11 +164,12 @@ __global__ void route_count_kernel(const int32_t* __restrict__ ids, int64_t T, i
 
 // T <= kRouteThreads: the whole routing + compaction in one block / one launch
 // (top-k, masks, counts, offsets, tile prefixes, scatter).
-__global__ void route_small_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int ns, int gating,
-                                   int32_t* __restrict__ ids, float* __restrict__ w, int32_t* __restrict__ counts,
-                                   int32_t* __restrict__ offsets, int nt0, int mt0, int32_t* __restrict__ prefix0,
-                                   int nt1, int mt1, int32_t* __restrict__ prefix1, int32_t* __restrict__ sel,
-                                   float* __restrict__ gw) {
+__device__ __forceinline__ void small_route(const float* __restrict__ logits, int64_t T, int E, int k, int ns,
+                                            int gating, int32_t* __restrict__ ids, float* __restrict__ w,
+                                            int32_t* __restrict__ counts, int32_t* __restrict__ offsets, int nt0,
+                                            int mt0, int32_t* __restrict__ prefix0, int nt1, int mt1,
+                                            int32_t* __restrict__ prefix1, int32_t* __restrict__ sel,
+                                            float* __restrict__ gw) {
   __shared__ uint32_t mask[kRouteWarps][kMaxE];
   __shared__ int32_t wbase[kRouteWarps][kMaxE];
   const int wp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -220,6 +215,14 @@ __global__ void route_small_kernel(const float* __restrict__ logits, int64_t T, 
     sel[pos] = t;
     gw[pos] = w[(int64_t)t * k + i];
   }
+}
+
+__global__ void route_small_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int ns, int gating,
+                                   int32_t* __restrict__ ids, float* __restrict__ w, int32_t* __restrict__ counts,
+                                   int32_t* __restrict__ offsets, int nt0, int mt0, int32_t* __restrict__ prefix0,
+                                   int nt1, int mt1, int32_t* __restrict__ prefix1, int32_t* __restrict__ sel,
+                                   float* __restrict__ gw) {
+  small_route(logits, T, E, k, ns, gating, ids, w, counts, offsets, nt0, mt0, prefix0, nt1, mt1, prefix1, sel, gw);
 }
 
 // Single block: counts, offsets, per-block bases and SSMM tile prefixes.
@@ -311,7 +314,10 @@ smy_status route_launch(const float* logits, int64_t T, int E, int k, int gating
   if (T <= kRouteThreads) {  // one block for the compaction (decode sizes)
     // up to 4 tokens per warp: top-k inside the same launch; more: a grid-wide
     // top-k launch first (one warp per token) so the block only compacts
-    const bool fused_topk = T <= 4 * kRouteWarps;  // (16 per warp measured slower than two launches)
+    // (16 per warp measured slower than two launches; so were, at T = 64, E = 64: one
+    // 1024-thread block doing both, top-k by argmax rounds, and one cooperative launch
+    // with a grid barrier -- probes/route_ab.sh)
+    const bool fused_topk = T <= 4 * kRouteWarps;
     if (logits != nullptr && !fused_topk) {
       route_topk_kernel<<<(unsigned)((T + kRouteWarps - 1) / kRouteWarps), kRouteThreads, 0, s>>>(logits, T, Er, kr,
                                                                                                  gating, ids, w, ns);
