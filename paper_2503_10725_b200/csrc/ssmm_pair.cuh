@@ -160,6 +160,14 @@ constexpr int kPairEpiWarps = 8;                    // warps 0-3 and 10-13
 // be a multiple of 16, so a half is a whole number of 8-row swizzle atoms
 __device__ __forceinline__ int pair_half(int n) { return ((n + 15) >> 4) << 3; }
 constexpr int kPairThreads = 32 * (11 + kPairEpiWarps - 4);  // + producer, 2 MMA issuers, 4 gather
+// SEL-gather launches (SPLIT) add 4 gather warps (15-18): the cp.async gather is what
+// binds the gate/up ring (probes/gather2_bench.cu: 28 KB stages with 19.5 KB of
+// weights beside them, 1344 clk per stage with 4 warps, 1185 with 8)
+#ifndef SMY_PAIR_GATHER_WARPS
+#define SMY_PAIR_GATHER_WARPS 8
+#endif
+constexpr int pair_threads(int split) { return kPairThreads + (split ? 32 * (SMY_PAIR_GATHER_WARPS - 4) : 0); }
+constexpr int pair_gather_threads(int split) { return split ? 32 * SMY_PAIR_GATHER_WARPS : kGatherThreads; }
 
 // MS = accumulator slots per weight: 2 for (1,2,V) (the lane-masked remap), 1 for
 // N == M (plain 2:4, no remap -- the weight-only-sparse baseline formats)
@@ -201,7 +209,7 @@ struct PairCfg {
 };
 
 template <int NT, int NW, int MS, int SPLIT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT), 1)
     ssmm_pair_kernel(const __grid_constant__ SsmmArgs a) {
   using C = PairCfg<NT, NW, MS, SPLIT>;
   constexpr int SW = C::kWStages, SB = C::kBStages;
@@ -243,7 +251,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       for (int s = 0; s < SB; ++s) {
         // gather: own gather threads (+ the peer's relay on the leader); contiguous
         // rows: the leader's expect_tx (both CTAs' TMA bytes)
-        mbar_init(&bfull[s], gather ? kGatherThreads + (leader ? 1 : 0) : 1);
+        mbar_init(&bfull[s], gather ? pair_gather_threads(SPLIT) + (leader ? 1 : 0) : 1);
         mbar_init(&bempty[s], kIssuers);
       }
     } else {
@@ -434,18 +442,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           mbar_arrive_cluster(bfull_lead + sb * 8);
         }
     }
-  } else if (warp >= 6 && warp < 10) {
+  } else if ((warp >= 6 && warp < 10) || warp >= 15) {
     // ============ SEL gather of this CTA's half of the token rows (cp.async) ============
-    // Thread tb owns the 16-B chunk ch = tb % 16 of rows tb/16 + 8i (i < H/8) of
-    // the tile for every k-stage, so the row lookups, source pointers and
-    // swizzled destination offsets are computed once per tile; a stage is then
-    // H/8 (address add + cp.async) per thread.
+    // Thread tb owns the 16-B chunk ch = tb % 16 of rows tb/16 + RS*i (i < H/RS,
+    // RS = gather threads / 16) of the tile for every k-stage, so the row lookups,
+    // source pointers and swizzled destination offsets are computed once per tile;
+    // a stage is then H/RS (address add + cp.async) per thread.
     if (gather) {
-      const int tb = threadIdx.x - 6 * 32;
-      static_assert(kGatherThreads == 128 && H % 8 == 0, "gather mapping");
-      constexpr int NI = H / 8;
+      constexpr int GT = pair_gather_threads(SPLIT), RS = GT / 16;
+      const int tb = warp < 10 ? threadIdx.x - 6 * 32 : threadIdx.x - 15 * 32 + kGatherThreads;
+      static_assert(GT % 128 == 0 && H % RS == 0, "gather mapping");
+      constexpr int NI = H / RS;
       const int r0 = tb >> 4, ch = tb & 15;
-      const uint32_t dst0 = (uint32_t)((ch >> 3) * (H * 128) + r0 * 128 + (((ch & 7) ^ r0) << 4));
+      const uint32_t dst0 = (uint32_t)((ch >> 3) * (H * 128) + r0 * 128 + (((ch & 7) ^ (r0 & 7)) << 4));
       uint32_t it = 0;
       TileInfo ti;
       for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep) {
@@ -454,7 +463,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         const int hh = pair_half(ti.n_local);
 #pragma unroll
         for (int i = 0; i < NI; ++i) {
-          const int tl = r0 + 8 * i;  // row within this CTA's half
+          const int tl = r0 + RS * i;  // row within this CTA's half
           const int t = (int)cta * hh + tl;
           const int rid = (tl < hh && t < ti.n_local) ? a.sel_in[ti.row0 + ti.t0 + t] : -1;
           src[i] = (rid >= 0 ? x_row(a, rid) : a.x) + ch * 8;
@@ -472,7 +481,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 #pragma unroll
             for (int i = 0; i < NI; ++i)
               if ((valid >> i) & 1u)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(bs + 1024u * i), "l"(src[i] + kcol0)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(bs + 128u * RS * i), "l"(src[i] + kcol0)
                              : "memory");
           }
           cp_async_mbar_arrive_noinc(&bfull[st]);
@@ -675,7 +684,7 @@ smy_status launch_pair_t(const SsmmArgs& a, cudaStream_t s) {
   const int pairs = (b.streamk || a.max_tiles >= num_sms / 2) ? num_sms / 2 : a.max_tiles;
   b.workers = pairs;
   b.m_fastest = a.epi == kEpiScatter && !(a.debug & 2048);
-  kern<<<2 * pairs, kPairThreads, C::kSmemBytes, s>>>(b);
+  kern<<<2 * pairs, pair_threads(SPLIT), C::kSmemBytes, s>>>(b);
   count_launch();
   return cuda_status(cudaGetLastError());
 }
