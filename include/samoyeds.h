@@ -338,6 +338,27 @@ SMY_API smy_status smy_moe_workspace_view(const smy_moe_config* cfg, int64_t T, 
 SMY_API smy_status smy_moe_set_phase_events(void** events, int n);
 SMY_API uint64_t smy_launch_count(void);
 /* SMY_DEBUG=128 profiling: copy (and reset) role cycle counters [2][ctas][16] (gate/up, scatter launches). */
+/* Ablation variants of samoyeds_moe_layer -- the breakdown measurement of
+ * SURVEY.md §8(f)-2 ("+W" vs "+WI"; P:374-376 the compressed output
+ * layout), NOT the product path.  After smy_moe_set_variant(v, scratch, bytes)
+ * with v != 0, single-GPU interleaved layer calls (comm == NULL, router logits)
+ * on the calling thread (thread-local) compute the same layer as:
+ *   SMY_VARIANT_PERMUTE      x[SEL] copied to an expert-major buffer (the
+ *                            materialised input permutation), gate/up on it as
+ *                            contiguous rows, down into compact fp32 rows, then a
+ *                            weighted un-permute (out[sel[i]] += gw[i] y[i])
+ *   SMY_VARIANT_DENSE_INTER  the intermediate in a token-position layout
+ *                            [(E+ns) x T x ffn], zero-filled every call, gate/up
+ *                            storing row e*T + sel[i], down gathering it back
+ * Other layer calls return SMY_E_CONFIG while a variant is set.  scratch: device
+ * buffer of >= smy_moe_variant_scratch_bytes(cfg, T, v) bytes (SMY_E_WORKSPACE),
+ * caller-owned, alive while the variant is set.  v = SMY_VARIANT_PRODUCT (0)
+ * restores the product path.  Unknown v: SMY_E_CONFIG.                      */
+#define SMY_VARIANT_PRODUCT 0
+#define SMY_VARIANT_PERMUTE 1
+#define SMY_VARIANT_DENSE_INTER 2
+SMY_API smy_status smy_moe_variant_scratch_bytes(const smy_moe_config* cfg, int64_t T, int32_t variant, size_t* bytes);
+SMY_API smy_status smy_moe_set_variant(int32_t variant, void* scratch, size_t bytes);
 SMY_API int smy_debug_prof(unsigned long long* host, int ctas);
 
 /* ------------------------------------------------------ synthetic inputs

@@ -90,6 +90,9 @@ SIGNATURES = {
     "smy_moe_workspace_view": (C.c_int, [C.POINTER(smy_moe_config), C.c_int64, C.c_void_p, C.c_size_t,
                                          C.POINTER(smy_moe_view)]),
     "smy_moe_set_phase_events": (C.c_int, [C.c_void_p, C.c_int]),
+    "smy_moe_variant_scratch_bytes": (C.c_int, [C.POINTER(smy_moe_config), C.c_int64, C.c_int32,
+                                               C.POINTER(C.c_size_t)]),
+    "smy_moe_set_variant": (C.c_int, [C.c_int32, C.c_void_p, C.c_size_t]),
     "smy_launch_count": (C.c_uint64, []),
     "smy_debug_prof": (C.c_int, [C.c_void_p, C.c_int]),
     "smy_synth_fill": (C.c_int, [C.c_uint64, C.c_int, C.c_float, C.c_int, C.c_int, C.c_int64, C.c_int64,

@@ -5,6 +5,7 @@ libsamoyeds.so kernels.  Names follow the C ABI and the paper's notation.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 from dataclasses import dataclass
 from typing import Optional, Sequence
@@ -328,6 +329,26 @@ class MoELayer:
                                      self.comm.handle if self.comm is not None else None,
                                      _stream(stream)), "samoyeds_moe_layer")
         return out
+
+    VARIANTS = {"product": 0, "permute": 1, "dense_inter": 2}
+
+    @contextlib.contextmanager
+    def variant(self, name: str, T: int):
+        """Ablation only (smy_moe_set_variant): inside the block,
+        this thread's single-GPU layer calls over <= T tokens run the named
+        variant ("permute": materialised input permutation; "dense_inter": token-
+        position intermediate layout) with scratch allocated here."""
+        lib = _lib.load()
+        v = self.VARIANTS[name]
+        b = C.c_size_t()
+        check(lib.smy_moe_variant_scratch_bytes(C.byref(self._cfg), T, v, C.byref(b)), "smy_moe_variant_scratch_bytes")
+        scratch = torch.empty(max(b.value, 1), dtype=torch.uint8, device=self.workspace.device)
+        check(lib.smy_moe_set_variant(v, _ptr(scratch), b.value), "smy_moe_set_variant")
+        try:
+            yield self
+        finally:
+            check(lib.smy_moe_set_variant(0, None, 0), "smy_moe_set_variant")
+            del scratch
 
     def kernel_names(self, T: int):
         """smy_moe_kernel_names: (gate/up, down) SSMM kernel names of a call over T tokens."""

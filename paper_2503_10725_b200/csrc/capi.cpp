@@ -558,6 +558,16 @@ smy_status smy_moe_set_phase_events(void** events, int n) {
 
 uint64_t smy_launch_count(void) { return g_launches.load(); }
 
+smy_status smy_moe_variant_scratch_bytes(const smy_moe_config* cfg, int64_t T, int32_t variant, size_t* bytes) {
+  if (!cfg || !bytes) return SMY_E_NULL;
+  if (T < 0) return SMY_E_SHAPE;
+  return moe_variant_bytes(cfg, T, variant, bytes);
+}
+
+smy_status smy_moe_set_variant(int32_t variant, void* scratch, size_t bytes) {
+  return moe_set_variant(variant, scratch, bytes);
+}
+
 // SMY_DEBUG & 128: accumulated per-role cycle counters of the last pair-kernel launches
 int smy_debug_prof(unsigned long long* host, int ctas) {
   if (!g_prof || ctas > g_prof_ctas) return 0;

@@ -64,6 +64,7 @@ struct SsmmArgs {
   void* out;
   int64_t ldo;
   const int32_t* sel_out;  // scatter destinations (SCATTER only)
+  const int32_t* rows_out;  // SILU_MUL_ILV output row of compact row r (ablation variant only; NULL: r)
   const float* scale;      // scatter scale, NULL = 1
   int max_tiles;           // tile count (single group) / upper bound (grouped)
   int weights_stream;      // 1: weights read once per call (decode) -> L2 evict_first
@@ -168,5 +169,7 @@ smy_status ep_layer(const smy_moe_config* c, const smy_weight* experts, const vo
 smy_status ep_row_ids_launch(const int32_t* sel, const int32_t* offsets, int world, int rank, int64_t max_rows,
                              int32_t* row_ids, cudaStream_t s);
 void record_phase(int i, cudaStream_t s);  // no-op unless bench hooks are set
+smy_status moe_variant_bytes(const smy_moe_config* c, int64_t T, int v, size_t* bytes);
+smy_status moe_set_variant(int v, void* scratch, size_t bytes);
 
 }  // namespace smy

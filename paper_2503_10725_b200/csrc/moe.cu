@@ -115,9 +115,10 @@ static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* 
                           int epi, void* out, int64_t ldo, int out_bf16, const int32_t* sel_out,
                           const float* scale, int64_t k_cols, int stream_w, int k_splits, int cl,
                           cudaStream_t s, const PeerRows* peers = nullptr, float* zero_ptr = nullptr,
-                          int64_t zero_elems = 0) {
+                          int64_t zero_elems = 0, const int32_t* rows_out = nullptr) {
   SsmmArgs a;
   memset(&a, 0, sizeof(a));
+  a.rows_out = rows_out;
   a.zero_ptr = zero_ptr;
   a.zero_elems = zero_elems;
   if (peers != nullptr) {
@@ -161,6 +162,73 @@ static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* 
   return cl ? ssmm_launch_pair(a, nt, nw, g.ms, cl, s) : ssmm_launch(a, nt, nw, g.ms, g.rep, s);
 }
 
+// ---- ablation variants (the paper's breakdown, and
+// the compressed-output-layout figure).  NOT the product path: the layer
+// runs them only between smy_moe_set_variant(v != 0) and smy_moe_set_variant(0), on
+// the calling thread, with caller-provided scratch.
+//   SMY_VARIANT_PERMUTE ("+W"): the input permutation materialised -- xp = x[SEL]
+//     (expert-major copy), gate/up on xp as contiguous rows (2D TMA, no gather),
+//     down into compact fp32 rows y, then the un-permute out[sel[i]] += gw[i] y[i]
+//   SMY_VARIANT_DENSE_INTER (no compressed output layout): the intermediate is an
+//     [E x T x f] token-position layout, zero-filled every call (the zero rows are
+//     the redundant transfers P:374 removes); gate/up stores row e*T + sel[i], the
+//     down launch gathers those rows back through SEL
+namespace {
+struct Variant {
+  int v = 0;
+  uint8_t* scratch = nullptr;
+  size_t bytes = 0;
+};
+thread_local Variant t_variant;
+
+__global__ void permute_rows_kernel(const uint16_t* __restrict__ x, int64_t d, const int32_t* __restrict__ sel,
+                                    const int32_t* __restrict__ offsets, int E, uint16_t* __restrict__ xp) {
+  const int64_t n = offsets[E], v8 = d / 8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * v8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / v8, c = i % v8;
+    reinterpret_cast<uint4*>(xp + r * d)[c] = reinterpret_cast<const uint4*>(x + (int64_t)sel[r] * d)[c];
+  }
+}
+__global__ void unpermute_rows_kernel(const float* __restrict__ y, int64_t d, const int32_t* __restrict__ sel,
+                                      const float* __restrict__ gw, const int32_t* __restrict__ offsets, int E,
+                                      float* __restrict__ out) {
+  const int64_t n = offsets[E], v4 = d / 4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * v4; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / v4, c = i % v4;
+    const float4 a = reinterpret_cast<const float4*>(y + r * d)[c];
+    const float g = gw[r];
+    atomicAdd(reinterpret_cast<float4*>(out + (int64_t)sel[r] * d) + c, make_float4(g * a.x, g * a.y, g * a.z, g * a.w));
+  }
+}
+__global__ void dense_rows_kernel(const int32_t* __restrict__ sel, const int32_t* __restrict__ offsets, int E,
+                                  int64_t T, int32_t* __restrict__ rows) {
+  for (int e = blockIdx.x; e < E; e += gridDim.x)
+    for (int i = offsets[e] + threadIdx.x; i < offsets[e + 1]; i += blockDim.x) rows[i] = (int32_t)(e * T + sel[i]);
+}
+size_t variant_bytes(const smy_moe_config* c, int64_t T, int v) {
+  const int ns = c->num_shared > 0 ? c->num_shared : 0;
+  const int64_t Tk = T * (c->top_k + ns);
+  if (v == SMY_VARIANT_PERMUTE) return align_up((size_t)Tk * c->hidden * 2, 256) + align_up((size_t)Tk * c->hidden * 4, 256);
+  if (v == SMY_VARIANT_DENSE_INTER)
+    return align_up((size_t)(c->num_experts + ns) * T * c->ffn * 2, 256) + align_up((size_t)Tk * 4, 256);
+  return 0;
+}
+}  // namespace
+
+smy_status moe_variant_bytes(const smy_moe_config* c, int64_t T, int v, size_t* bytes) {
+  if (v < 0 || v > SMY_VARIANT_DENSE_INTER) return SMY_E_CONFIG;
+  *bytes = variant_bytes(c, T, v);
+  return SMY_OK;
+}
+smy_status moe_set_variant(int v, void* scratch, size_t bytes) {
+  if (v < 0 || v > SMY_VARIANT_DENSE_INTER) return SMY_E_CONFIG;
+  if (v != 0 && scratch == nullptr) return SMY_E_NULL;
+  t_variant.v = v;
+  t_variant.scratch = static_cast<uint8_t*>(scratch);
+  t_variant.bytes = bytes;
+  return SMY_OK;
+}
+
 // The expert computation over T rows of x.  Routing either comes from router
 // logits (top-k on device) or is given as keys[T x k] (expert ids, -1 = none)
 // with weights vals[T x k] -- the expert-parallel receive side.
@@ -196,8 +264,16 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   const int nt_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, tpg_hi);
   // expected down tiles -> K split (the scatter-add epilogue makes partial sums free)
   const int64_t act = E < T * k ? E : T * k;
-  const int ks_dn = ssmm_pick_ksplit((int64_t)gdn.m_tiles * act * ((tpg + nt_dn - 1) / (nt_dn > 0 ? nt_dn : 1)),
-                                     gdn.k_stages);
+  const Variant var = t_variant;
+  if (var.v != 0) {  // ablation variants: the single-GPU interleaved layer with router logits
+    if (!ilv || keys != nullptr || peers != nullptr) return SMY_E_CONFIG;
+    if (variant_bytes(c, T, var.v) > var.bytes) return SMY_E_WORKSPACE;
+  }
+  // the permute variant's down writes compact fp32 rows: no K split
+  const int ks_dn = var.v == SMY_VARIANT_PERMUTE
+                        ? 1
+                        : ssmm_pick_ksplit((int64_t)gdn.m_tiles * act * ((tpg + nt_dn - 1) / (nt_dn > 0 ? nt_dn : 1)),
+                                           gdn.k_stages);
   const smy_weight* wg[kMaxGroups];
   const smy_weight* wu[kMaxGroups];
   const smy_weight* wd[kMaxGroups];
@@ -245,7 +321,28 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   const uint16_t* xb = static_cast<const uint16_t*>(x);
 
   // gate/up: H = Wg x[SEL], U = Wu x[SEL], inter = bf16(silu(H) * U)
-  if (ilv) {
+  uint16_t* xp = nullptr;       // SMY_VARIANT_PERMUTE: x[SEL], then y (fp32) after it
+  float* yp = nullptr;
+  uint16_t* inter_dense = nullptr;  // SMY_VARIANT_DENSE_INTER: [E x T x f], then the row map
+  int32_t* rows_dense = nullptr;
+  const int vblocks = 148 * 8;
+  if (var.v == SMY_VARIANT_PERMUTE) {
+    xp = reinterpret_cast<uint16_t*>(var.scratch);
+    yp = reinterpret_cast<float*>(var.scratch + align_up((size_t)Tk * d * 2, 256));
+    permute_rows_kernel<<<vblocks, 256, 0, s>>>(xb, d, w.sel, w.offsets, E, xp);
+    count_launch();
+    st = grouped(wg, nullptr, E, ggu, f, nt_gu, 1, xp, d, Tk, nullptr, w.offsets, prefix_gu, max_gu, kEpiSiluMulIlv,
+                 w.inter, f, 1, nullptr, nullptr, d, tpg <= nt_gu, 1, cl_gu, s, nullptr, zero_out, T * d);
+  } else if (var.v == SMY_VARIANT_DENSE_INTER) {
+    inter_dense = reinterpret_cast<uint16_t*>(var.scratch);
+    rows_dense = reinterpret_cast<int32_t*>(var.scratch + align_up((size_t)E * T * f * 2, 256));
+    cudaMemsetAsync(inter_dense, 0, (size_t)E * T * f * 2, s);
+    dense_rows_kernel<<<E, 256, 0, s>>>(w.sel, w.offsets, E, T, rows_dense);
+    count_launch();
+    st = grouped(wg, nullptr, E, ggu, f, nt_gu, 1, xb, d, T, w.sel, w.offsets, prefix_gu, max_gu, kEpiSiluMulIlv,
+                 inter_dense, f, 1, nullptr, nullptr, d, tpg <= nt_gu, 1, cl_gu, s, nullptr, zero_out, T * d,
+                 rows_dense);
+  } else if (ilv) {
     st = grouped(wg, nullptr, E, ggu, f, nt_gu, 1, xb, peers ? peers->ldx : d, T, w.sel, w.offsets, prefix_gu,
                  max_gu, kEpiSiluMulIlv, w.inter, f, 1, nullptr, nullptr, d, tpg <= nt_gu, 1, cl_gu, s, peers,
                  zero_out, T * d);
@@ -264,8 +361,21 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   if (st != SMY_OK) return st;
   record_phase(3, s);
   // down: out[sel[t]] += gw[t] * Wd inter[t]
-  st = grouped(wd, nullptr, E, gdn, d, nt_dn, 1, w.inter, f, Tk, nullptr, w.offsets, prefix_dn, max_dn, kEpiScatter,
-               out, peers ? peers->ldo : d, 0, w.sel, w.gw, f, tpg <= nt_dn, ks_dn, cl_dn, s, peers);
+  if (var.v == SMY_VARIANT_PERMUTE) {
+    st = grouped(wd, nullptr, E, gdn, d, nt_dn, 1, w.inter, f, Tk, nullptr, w.offsets, prefix_dn, max_dn, kEpiCompact,
+                 yp, d, 0, nullptr, nullptr, f, tpg <= nt_dn, 1, cl_dn, s);
+    if (st == SMY_OK) {
+      unpermute_rows_kernel<<<vblocks, 256, 0, s>>>(yp, d, w.sel, w.gw, w.offsets, E, out);
+      count_launch();
+      st = cuda_status(cudaGetLastError());
+    }
+  } else if (var.v == SMY_VARIANT_DENSE_INTER) {
+    st = grouped(wd, nullptr, E, gdn, d, nt_dn, 1, inter_dense, f, (int64_t)E * T, rows_dense, w.offsets, prefix_dn,
+                 max_dn, kEpiScatter, out, d, 0, w.sel, w.gw, f, tpg <= nt_dn, ks_dn, cl_dn, s);
+  } else {
+    st = grouped(wd, nullptr, E, gdn, d, nt_dn, 1, w.inter, f, Tk, nullptr, w.offsets, prefix_dn, max_dn, kEpiScatter,
+                 out, peers ? peers->ldo : d, 0, w.sel, w.gw, f, tpg <= nt_dn, ks_dn, cl_dn, s, peers);
+  }
   if (st != SMY_OK) return st;
   record_phase(4, s);
 

@@ -215,7 +215,7 @@ __device__ __forceinline__ void scatter_chunk_v4(const float (&v0)[16], const fl
 // lane g of slot 1 -- so all 32 lanes compute one bf16(silu(g) * u) and the warp
 // stores 32 consecutive outputs (64 B).  No shared memory, no barrier.
 __device__ __forceinline__ void ilv_chunk(const float (&v)[2][16], bool valid, int jmax, uint16_t* out, int64_t ldo,
-                                          int64_t row_base, int cg, int lane) {
+                                          int64_t row_base, int cg, int lane, const int32_t* rows_out = nullptr) {
   const bool is_up = lane >= 16;
   // token pair (c, c+1): the gate lane finishes both slots of token c, the up lane
   // both slots of token c+1 -- two shuffles swap what each lacks, and each lane
@@ -231,8 +231,16 @@ __device__ __forceinline__ void ilv_chunk(const float (&v)[2][16], bool valid, i
     const __nv_bfloat162 h = __floats2bfloat162_rn(silu_mul(g0, u0), silu_mul(g1, u1));
     packed[j] = *reinterpret_cast<const uint32_t*>(&h);
   }
-  uint32_t* o = reinterpret_cast<uint32_t*>(out + (row_base + (is_up ? 1 : 0)) * ldo + 2 * cg);
   const int n = valid ? jmax : 0;
+  if (rows_out != nullptr) {  // ablation only (SMY_VARIANT_DENSE_INTER): row r goes to rows_out[r]
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int t = 2 * j + (is_up ? 1 : 0);
+      if (t < n) *reinterpret_cast<uint32_t*>(out + (int64_t)rows_out[row_base + t] * ldo + 2 * cg) = packed[j];
+    }
+    return;
+  }
+  uint32_t* o = reinterpret_cast<uint32_t*>(out + (row_base + (is_up ? 1 : 0)) * ldo + 2 * cg);
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     if (2 * j + (is_up ? 1 : 0) < n) *o = packed[j];
@@ -552,7 +560,7 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
           tmem_ld16(tmem + lane_base + ab * C::kAccCols + NT + c0, v[1 % MS]);
           tmem_ld_wait();
           ilv_chunk(v, cg < a.R / 2 && !(a.debug & 8), min(16, ti.n_local - c0), static_cast<uint16_t*>(a.out), a.ldo,
-                    ti.row0 + ti.t0 + c0, cg, lane);
+                    ti.row0 + ti.t0 + c0, cg, lane, a.rows_out);
         }
         tc_fence_before();
         zero_acc(ab);

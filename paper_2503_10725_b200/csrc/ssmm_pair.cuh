@@ -537,7 +537,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
             if (prof) pc[8] += clk() - tl0;
             if (!(a.debug & 32))
               ilv_chunk(v, gvalid, min(16, ti.n_local - c0), static_cast<uint16_t*>(a.out), a.ldo,
-                        ti.row0 + ti.t0 + c0, cg, lane);
+                        ti.row0 + ti.t0 + c0, cg, lane, a.rows_out);
           } else {  // N = M: one slot
             float v[16];
             tmem_ld16(tacc + lane_base + c0, v);

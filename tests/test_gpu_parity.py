@@ -354,7 +354,7 @@ def test_route_ties(smy):
 # ------------------------------------------------------------------ MoE layer
 
 def _layer_case(smy, fmt, E, d, f, T, k, gating="renorm_topk", shared=0, skew=0.0, seed_off=0, gate_up="auto",
-                transcode="auto"):
+                transcode="auto", variant=None):
     cfg = smy.MoEConfig(E, k, d, f, shared, gating, gpu_format(fmt), gate_up, transcode)
     encs, sws = [], []
     for e in range(E + shared):
@@ -369,7 +369,11 @@ def _layer_case(smy, fmt, E, d, f, T, k, gating="renorm_topk", shared=0, skew=0.
     x = synth.activations_bf16(synth.SEED_X, T, d)
     lg = synth.router_logits(synth.SEED_LOGITS, T, E, skew=skew)
     layer = smy.MoELayer(cfg, sws[:E], sws[E:], max_tokens=max(T, 1))
-    got = layer(dev16(x), torch.from_numpy(lg).cuda()).cpu().numpy().astype(np.float64)
+    if variant is None:
+        got = layer(dev16(x), torch.from_numpy(lg).cuda()).cpu().numpy().astype(np.float64)
+    else:
+        with layer.variant(variant, T):
+            got = layer(dev16(x), torch.from_numpy(lg).cuda()).cpu().numpy().astype(np.float64)
     mode = moe.SOFTMAX_ALL if gating == "softmax_all" else moe.RENORM_TOPK
     ref, S = moe.moe_layer(encs[:E], x, lg, k, mode, shared=encs[E:])
     return got, ref, S
@@ -415,6 +419,31 @@ def test_moe_layer_prefill_pair_kernels(smy, case):
     case = dict(case)
     got, ref, S = _layer_case(smy, F.SparseFormat(1, 2, 32), **case)
     check_tol(got, ref, S, "moe layer (pair kernels)")
+
+
+@pytest.mark.parametrize("variant", ["permute", "dense_inter"])
+@pytest.mark.parametrize("case", [
+    dict(E=4, d=512, f=512, T=512, k=2),                       # CTA-pair kernels
+    dict(E=2, d=512, f=1024, T=300, k=2, skew=2.0),            # ragged tiles, unbalanced experts
+    dict(E=8, d=256, f=512, T=100, k=2),                       # single-CTA kernels
+    dict(E=16, d=256, f=384, T=257, k=6, gating="softmax_all", shared=2, skew=1.0),
+], ids=lambda c: f"E{c['E']}-d{c['d']}-f{c['f']}-T{c['T']}-sh{c.get('shared', 0)}")
+def test_moe_layer_ablation_variants(smy, variant, case):
+    """The breakdown variants (smy_moe_set_variant) compute the same
+    layer: the materialised permutation and the token-position intermediate layout
+    against the oracle at the layer bar."""
+    case = dict(case)
+    got, ref, S = _layer_case(smy, F.SparseFormat(1, 2, 32), variant=variant, **case)
+    check_tol(got, ref, S, f"moe layer ({variant})")
+
+
+def test_moe_layer_variant_rejections(smy):
+    """A variant applies to the single-GPU interleaved layer only; unknown ids and
+    a short scratch are refused without launching."""
+    lib = smy.load()
+    assert lib.smy_moe_set_variant(7, None, 0) == 3  # SMY_E_CONFIG
+    assert lib.smy_moe_set_variant(1, None, 0) != 0  # needs scratch
+    assert lib.smy_moe_set_variant(0, None, 0) == 0
 
 
 @pytest.mark.parametrize("T", [1, 100, 600])
