@@ -340,7 +340,7 @@ smy_status samoyeds_ssmm(const smy_weight* w, const smy_weight* w2, const void* 
   const smy_weight* w1a[1] = {nw == 2 ? w2 : nullptr};
   const size_t img = (size_t)g.m_tiles * g.k_stages * g.block;
   const int cl = ssmm_pair_images_ok(w0a, nw == 2 ? w1a : nullptr, 1, img)
-                     ? ssmm_pair_cluster(nt, nw, g.ms, g.rep, g.m_tiles, n_sel)
+                     ? ssmm_pair_cluster(nt, nw, g.ms, g.rep, g.m_tiles, n_sel, 1)
                      : 0;
   if (cl) {
     a.max_tiles = ((g.m_tiles + 1) / 2) * ((n_sel + nt - 1) / nt);

@@ -107,7 +107,14 @@ int ssmm_pick_nt(int nw, int ms, int rep, int64_t tokens_per_group);
 smy_status ssmm_launch(const SsmmArgs& a, int nt, int nw, int ms, int rep, cudaStream_t s);
 // CTA-pair (cta_group::2) kernel: a.m_tiles / tile prefixes count m-tile PAIRS, tmap box = nt/2 rows
 // returns the cluster size to use (2: one MMA pair, 4: two pairs sharing weights) or 0 (single CTA)
-int ssmm_pair_cluster(int nt, int nw, int ms, int rep, int m_tiles, int64_t tokens_per_group);
+// gather: the launch reads x through SEL.  Such launches with the lane-masked
+// (1,2,V) remap and tiles of <= SMY_SINGLE_FAST_GATHER_NT tokens stay on the
+// single-CTA kernel (weight-streaming regime: its deeper weight ring and
+// precomputed-pointer gather beat the CTA pair there, profiles/r2_midrange.md)
+#ifndef SMY_SINGLE_FAST_GATHER_NT
+#define SMY_SINGLE_FAST_GATHER_NT 128
+#endif
+int ssmm_pair_cluster(int nt, int nw, int ms, int rep, int m_tiles, int64_t tokens_per_group, int gather);
 smy_status ssmm_launch_pair(const SsmmArgs& a, int nt, int nw, int ms, int cl, cudaStream_t s);
 // can one tensor map address all these images (else: single-CTA kernel)
 bool ssmm_pair_images_ok(const smy_weight* const* w0, const smy_weight* const* w1, int groups, size_t img_bytes);

@@ -287,8 +287,8 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   const size_t img_dn = (size_t)gdn.m_tiles * gdn.k_stages * gdn.block;
   const bool pair_gu_ok = ssmm_pair_images_ok(wg, nw_gu == 2 ? wu : nullptr, E, img_gu);
   const bool pair_dn_ok = ssmm_pair_images_ok(wd, nullptr, E, img_dn);
-  const int cl_gu = fused && pair_gu_ok ? ssmm_pair_cluster(nt_gu, nw_gu, ggu.ms, ggu.rep, ggu.m_tiles, tpg) : 0;
-  const int cl_dn = pair_dn_ok ? ssmm_pair_cluster(nt_dn, 1, gdn.ms, gdn.rep, gdn.m_tiles, tpg) : 0;
+  const int cl_gu = fused && pair_gu_ok ? ssmm_pair_cluster(nt_gu, nw_gu, ggu.ms, ggu.rep, ggu.m_tiles, tpg, 1) : 0;
+  const int cl_dn = pair_dn_ok ? ssmm_pair_cluster(nt_dn, 1, gdn.ms, gdn.rep, gdn.m_tiles, tpg, 0) : 0;
   const int mt_gu = cl_gu ? (ggu.m_tiles + 1) / 2 : ggu.m_tiles;
   const int mt_dn = cl_dn ? (gdn.m_tiles + 1) / 2 : gdn.m_tiles;
   // the routing scan counts tiles per expert in units of the launch's token span
@@ -452,10 +452,11 @@ smy_status moe_kernel_names(const smy_moe_config* c, int64_t T, char* gu, char* 
   const int64_t tpg_hi = tpg + (int64_t)(3.0 * sqrt((double)tpg) + 0.999);
   const int nt_gu = ssmm_pick_nt(nw_gu, ggu.ms, ggu.rep, tpg_hi);
   const int nt_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, tpg_hi);
-  const int cl_gu = fused ? ssmm_pair_cluster(nt_gu, nw_gu, ggu.ms, ggu.rep, ggu.m_tiles, tpg) : 0;
-  const int cl_dn = ssmm_pair_cluster(nt_dn, 1, gdn.ms, gdn.rep, gdn.m_tiles, tpg);
+  const int cl_gu = fused ? ssmm_pair_cluster(nt_gu, nw_gu, ggu.ms, ggu.rep, ggu.m_tiles, tpg, 1) : 0;
+  const int cl_dn = ssmm_pair_cluster(nt_dn, 1, gdn.ms, gdn.rep, gdn.m_tiles, tpg, 0);
   // the SEL-gather pair launch of the widest (1,2,V) tile runs split rings (ssmm.cu)
-  const int split_gu = cl_gu && ggu.ms == 2 && nw_gu == 1 && nt_gu == SMY_NT_WIDE && !(debug_flags() & 16384);
+  const int split_gu =
+      cl_gu && ggu.ms == 2 && nw_gu == 1 && (nt_gu == SMY_NT_WIDE || nt_gu == 128) && !(debug_flags() & 16384);
   if (cl_gu)
     snprintf(gu, len, "ssmm_pair_kernel<%d, %d, %d, %d>", nt_gu, nw_gu, ggu.ms, split_gu);
   else

@@ -35,6 +35,7 @@ extern template smy_status launch_pair_t<112, 2, 2, 0>(const SsmmArgs&, cudaStre
 extern template smy_status launch_pair_t<128, 1, 2, 0>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<SMY_NT_WIDE, 1, 2, 0>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<SMY_NT_WIDE, 1, 2, 1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<128, 1, 2, 1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<128, 1, 1, 0>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<256, 1, 1, 0>(const SsmmArgs&, cudaStream_t);
 
@@ -81,8 +82,10 @@ int ssmm_pick_nt(int nw, int ms, int rep, int64_t tpg) {
   return best > 0 ? best : largest;
 }
 
-int ssmm_pair_cluster(int nt, int nw, int ms, int rep, int m_tiles, int64_t tokens_per_group) {
+int ssmm_pair_cluster(int nt, int nw, int ms, int rep, int m_tiles, int64_t tokens_per_group, int gather) {
   if (debug_flags() & 16) return 0;  // SMY_DEBUG=16: force the single-CTA kernel
+  if (debug_flags() & 32768) gather = 0;  // SMY_DEBUG=32768: pair kernels also for narrow gather tiles
+  if (gather && ms == 2 && nw == 1 && nt <= SMY_SINGLE_FAST_GATHER_NT) return 0;
   // an odd m-tile count gives the last pair a phantom peer tile (loads repeated, stores masked)
   if (rep != 1 || m_tiles < 2 || tokens_per_group < 64) return 0;
   if (ms == 2 && !(nw == 2 ? (nt == 64 || nt == 112) : (nt == 128 || nt == SMY_NT_WIDE))) return 0;
@@ -151,10 +154,14 @@ smy_status ssmm_launch_pair(const SsmmArgs& a0, int nt, int nw, int ms, int cl, 
   if (st != SMY_OK) return st;
   if (ms == 2 && nw == 2 && nt == 64) return launch_pair_t<64, 2, 2, 0>(a, s);
   if (ms == 2 && nw == 2 && nt == 112) return launch_pair_t<112, 2, 2, 0>(a, s);
-  if (ms == 2 && nw == 1 && nt == 128) return launch_pair_t<128, 1, 2, 0>(a, s);
+  if (ms == 2 && nw == 1 && nt == 128) return a.sel_in && !(a.debug & 16384) ? launch_pair_t<128, 1, 2, 1>(a, s)
+                                                                           : launch_pair_t<128, 1, 2, 0>(a, s);
   // SEL-gathered token rows (gate/up): separate, deeper token ring
-  if (ms == 2 && nw == 1 && nt == SMY_NT_WIDE) return a.sel_in && !(a.debug & 16384) ? launch_pair_t<SMY_NT_WIDE, 1, 2, 1>(a, s)
-                                                                              : launch_pair_t<SMY_NT_WIDE, 1, 2, 0>(a, s);
+  // (SMY_DEBUG=16384: lock-step ring for gather launches too; 262144: split rings for
+  // contiguous-row launches too -- ring-structure A/B only)
+  if (ms == 2 && nw == 1 && nt == SMY_NT_WIDE)
+    return (a.sel_in && !(a.debug & 16384)) || (a.debug & 262144) ? launch_pair_t<SMY_NT_WIDE, 1, 2, 1>(a, s)
+                                                                  : launch_pair_t<SMY_NT_WIDE, 1, 2, 0>(a, s);
   if (ms == 1 && nw == 1 && nt == 128) return launch_pair_t<128, 1, 1, 0>(a, s);
   if (ms == 1 && nw == 1 && nt == 256) return launch_pair_t<256, 1, 1, 0>(a, s);
   set_last_error("ssmm: unsupported pair (nt, nw)");

@@ -5,6 +5,7 @@ namespace smy {
 template smy_status launch_pair_t<64, 2, 2, 0>(const SsmmArgs&, cudaStream_t);
 template smy_status launch_pair_t<112, 2, 2, 0>(const SsmmArgs&, cudaStream_t);
 template smy_status launch_pair_t<128, 1, 2, 0>(const SsmmArgs&, cudaStream_t);
+template smy_status launch_pair_t<128, 1, 2, 1>(const SsmmArgs&, cudaStream_t);
 template smy_status launch_pair_t<SMY_NT_WIDE, 1, 2, 0>(const SsmmArgs&, cudaStream_t);
 template smy_status launch_pair_t<SMY_NT_WIDE, 1, 2, 1>(const SsmmArgs&, cudaStream_t);
 template smy_status launch_pair_t<128, 1, 1, 0>(const SsmmArgs&, cudaStream_t);

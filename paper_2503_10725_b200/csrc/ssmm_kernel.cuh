@@ -64,6 +64,8 @@ struct Cfg {
   static_assert(NT % 16 == 0 && NT >= 16 && NT <= 256, "UMMA N");
 };
 
+// (SMY_SINGLE_FAST_GATHER_NT, internal.h: the widest token tile whose gather
+// precomputes per-thread source pointers, NT/8 of them)
 constexpr int kThreads = 352;  // warps 0-3 epilogue, 4 producer, 5 + 10 MMA, 6-9 gather
 constexpr int kGatherThreads = 128;
 
@@ -438,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
     }
   } else if (warp >= 6 && warp < 10) {
     // ================== SEL gather of token rows (warps 6-9, cp.async) ==================
-    if (gather && REP == 1 && NT <= 64) {
+    if (gather && REP == 1 && NT <= SMY_SINGLE_FAST_GATHER_NT) {
       // Thread tb owns 16-B chunk ch = tb % 16 of rows tb/16 + 8i of the tile for
       // every k-stage: sources and swizzled destinations are computed once per tile
       // (as in the pair kernel); rows past the tile's tokens are not loaded.

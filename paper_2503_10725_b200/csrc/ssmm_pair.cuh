@@ -19,6 +19,9 @@
 // `acc_full`; both epilogues arrive on the leader's `acc_empty`.
 #include "ssmm_kernel.cuh"
 
+#ifndef SMY_TOKEN_ACQ_CTA
+#define SMY_TOKEN_ACQ_CTA 0
+#endif
 #ifndef SMY_CLUSTER_ACQ_ALL
 #define SMY_CLUSTER_ACQ_ALL 0
 #endif
@@ -233,6 +236,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
   const bool gather = a.sel_in != nullptr;
   const int warp = warp_id(), lane = lane_id();
   uint8_t* zbuf = aux + 1024;  // 1 KB of zeros: the operand of the accumulator-clearing MMA
+  // SMY_DEBUG & 128: clock at which the leader's gather thread 0 issued each token slot
+  volatile unsigned long long* ts_issue = reinterpret_cast<volatile unsigned long long*>(aux + 512);
+  if (threadIdx.x < 8) ts_issue[threadIdx.x] = 0;
   // TMEM allocation first, ordered before every other shared-memory write of the
   // prologue (compute-sanitizer racecheck flagged the allocator's slot write
   // against the prologue's stores when they were unordered)
@@ -379,8 +385,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
             // include the peer's cp.async writes, made visible by its relay's release
             mbar_wait_cta(&wfull[st], (it / SW) & 1);
             if (prof) { const unsigned long long t1 = clk(); pc[0] += t1 - t0; t0 = t1; }
+#if SMY_TOKEN_ACQ_CTA
+            mbar_wait_cta(&bfull[sb], (it / SB) & 1);
+#else
             mbar_wait_acq_cluster(&bfull[sb], (it / SB) & 1);
-            if (prof) { pc[6] += clk() - t0; t0 = clk(); }  // token-ring share of the operand waits
+#endif
+            if (prof) {  // token-ring share of the operand waits; issue -> ready latency of the slot
+              const unsigned long long t1 = clk(), ts = ts_issue[sb];
+              pc[6] += t1 - t0;
+              // (the gather's generic store of ts is not ordered by its async arrive:
+              // skip the first round's unwritten slots)
+              if (ts != 0 && t1 > ts && t1 - ts < (1ull << 24)) pc[8] += t1 - ts;
+              t0 = clk();
+            }
           } else {
             mbar_wait_acq_cluster(&wfull[st], (it / SW) & 1);  // both CTAs' stage (peer bytes + relay)
           }
@@ -473,7 +490,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
           const int st = it % SB;
           unsigned long long tg0 = prof ? clk() : 0;
           mbar_wait_cta(&bempty[st], ((it / SB) & 1) ^ 1);
-          if (prof) { const unsigned long long t1 = clk(); pc[10] += t1 - tg0; tg0 = t1; }
+          if (prof) {
+            const unsigned long long t1 = clk();
+            pc[10] += t1 - tg0;
+            tg0 = t1;
+            if (tb == 0 && leader) {  // slot round trip: issue of stage it - SB -> this slot free again
+              if (it >= (uint32_t)SB) pc[9] += t1 - ts_issue[st];
+              ts_issue[st] = t1;
+            }
+          }
           const int64_t kcol0 = (int64_t)k * 128;
           const uint32_t bs = smem_u32(bsm(st)) + dst0;
           if (!(a.debug & 1)) {
@@ -642,8 +667,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
       atomicAdd(o + 0, pc[0] + pc[6]); atomicAdd(o + 1, pc[1]); atomicAdd(o + 2, pc[2]); atomicAdd(o + 6, pc[6]);
       atomicAdd(o + 7, pc[7]);
     }
-    if (warp == 6 && lane == 0) { atomicAdd(o + 10, pc[10]); atomicAdd(o + 11, pc[11]); }
-    if (warp == 0 && lane == 0) { atomicAdd(o + 3, pc[3]); atomicAdd(o + 4, pc[4]); atomicAdd(o + 8, pc[8]); atomicAdd(o + 9, pc[9]); }
+    if (warp == 6 && lane == 0) { atomicAdd(o + 10, pc[10]); atomicAdd(o + 11, pc[11]); atomicAdd(o + 9, pc[9]); }
+    if (warp == 5 && lane == 0 && SPLIT) atomicAdd(o + 12, pc[8]);
+    if (warp == 0 && lane == 0) { atomicAdd(o + 3, pc[3]); atomicAdd(o + 4, pc[4]); atomicAdd(o + 8, pc[8]); }
     if (warp == 4 && lane == 0) { atomicAdd(o + 5, pc[5]); }
   }
   if (prof) {  // CTA lifetime (ns) up to here, and the time its MMA work ended

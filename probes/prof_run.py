@@ -51,3 +51,8 @@ for name, a in zip(("gate/up", "down"), A):
                                  (en.max() - en.min()) / 1e3, (en.max() - st.min()) / 1e3))
     print("  epilogue: wait_acc_full %.1f  work %.1f (tmem_ld %.1f)   producer wait_empty %.1f"
           % tuple(a[:, i].mean() for i in (3, 4, 8, 5)))
+    if lead[:, 12].mean() > 0:
+        ks = {"mixtral": 32, "qwen2": 28, "deepseek": 16}.get(model, 1)
+        n = lead[:, 7].mean() * ks
+        print("  token slot (leader): issue -> ready seen by the MMA %.0f clk, slot round trip %.0f clk (per stage)"
+              % (lead[:, 12].mean() * 1e3 / n, lead[:, 9].mean() * 1e3 / n))

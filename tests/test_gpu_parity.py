@@ -167,7 +167,8 @@ def test_ssmm_integer_bit_exact_cfg1(smy, fmt):
 
 
 @pytest.mark.parametrize("fmt", PARITY_FORMATS, ids=str)
-@pytest.mark.parametrize("shape", [(128, 256, 64, 16), (384, 512, 300, 200), (1024, 1408, 900, 777)])
+@pytest.mark.parametrize("shape", [(128, 256, 64, 16), (384, 512, 300, 200), (1024, 1408, 900, 777),
+                                   (256, 512, 400, 110)])
 def test_ssmm_random_tolerance(smy, fmt, shape):
     rows, cols, x_rows, n_sel = shape
     if cols % 128:
@@ -414,6 +415,8 @@ def test_moe_layer_parity(smy, case):
     dict(E=4, d=512, f=512, T=512, k=2, gate_up="separate"),   # two-weight gate/up pair kernel
     dict(E=2, d=512, f=1024, T=300, k=2, skew=2.0, gate_up="separate"),
     dict(E=4, d=512, f=512, T=512, k=2, shared=2),             # shared experts as groups of the pair launches
+    dict(E=4, d=512, f=512, T=150, k=2),                       # gate/up: single-CTA NT=128 gather (mid range)
+    dict(E=8, d=256, f=768, T=380, k=2, skew=1.0),             # NT=128 gate/up, heavy experts -> 2 token tiles
 ], ids=lambda c: f"E{c['E']}-d{c['d']}-f{c['f']}-T{c['T']}-{c.get('gate_up', 'auto')}-sh{c.get('shared', 0)}")
 def test_moe_layer_prefill_pair_kernels(smy, case):
     case = dict(case)
