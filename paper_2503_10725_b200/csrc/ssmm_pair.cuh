@@ -19,6 +19,15 @@
 // `acc_full`; both epilogues arrive on the leader's `acc_empty`.
 #include "ssmm_kernel.cuh"
 
+#ifndef SMY_PAIR_W_EVICT_FIRST
+#define SMY_PAIR_W_EVICT_FIRST 0
+#endif
+#ifndef SMY_RELAY_TRYWAIT
+#define SMY_RELAY_TRYWAIT 0
+#endif
+#ifndef SMY_GATHER_EVICT_LAST
+#define SMY_GATHER_EVICT_LAST 0
+#endif
 #ifndef SMY_TOKEN_ACQ_CTA
 #define SMY_TOKEN_ACQ_CTA 0
 #endif
@@ -301,7 +310,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
       const uint32_t b_pair_bytes = gather ? 0u : 2 * (uint32_t)C::kBBytes;
       // prefill: the pairs on the same m-tile read its weights at about the same
       // time; evict_normal measured better than evict_first (fewer re-reads)
-      const uint64_t pol_w = a.weights_stream ? policy_evict_first() : policy_evict_normal();
+      const uint64_t pol_w = (a.weights_stream || SMY_PAIR_W_EVICT_FIRST) ? policy_evict_first() : policy_evict_normal();
       const uint64_t pol_x = policy_evict_last();
       const int brows = a.block >> 7;
       uint32_t it = 0;
@@ -455,7 +464,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
       for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep)
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int sb = it % SB;
-          mbar_spin(&bfull[sb], (it / SB) & 1);
+          if (SMY_RELAY_TRYWAIT)
+            mbar_wait_cta(&bfull[sb], (it / SB) & 1);
+          else
+            mbar_spin(&bfull[sb], (it / SB) & 1);
           mbar_arrive_cluster(bfull_lead + sb * 8);
         }
     }
@@ -469,6 +481,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
       constexpr int GT = pair_gather_threads(SPLIT), RS = GT / 16;
       const int tb = warp < 10 ? threadIdx.x - 6 * 32 : threadIdx.x - 15 * 32 + kGatherThreads;
       static_assert(GT % 128 == 0 && H % RS == 0, "gather mapping");
+      const uint64_t pol_g = SMY_GATHER_EVICT_LAST ? policy_evict_last() : 0;
       constexpr int NI = H / RS;
       const int r0 = tb >> 4, ch = tb & 15;
       const uint32_t dst0 = (uint32_t)((ch >> 3) * (H * 128) + r0 * 128 + (((ch & 7) ^ (r0 & 7)) << 4));
@@ -506,8 +519,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
 #pragma unroll
             for (int i = 0; i < NI; ++i)
               if ((valid >> i) & 1u)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(bs + 128u * RS * i), "l"(src[i] + kcol0)
-                             : "memory");
+              {
+                if (SMY_GATHER_EVICT_LAST)
+                  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(bs + 128u * RS * i),
+                               "l"(src[i] + kcol0), "l"(pol_g)
+                               : "memory");
+                else
+                  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(bs + 128u * RS * i), "l"(src[i] + kcol0)
+                               : "memory");
+              }
           }
           cp_async_mbar_arrive_noinc(&bfull[st]);
           if (prof) pc[11] += clk() - tg0;
