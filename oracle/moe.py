@@ -14,7 +14,9 @@ Paper:
     addition to their assigned routed experts"               (§6.2)
 Readings: R9 gate normalisation (RENORM_TOPK default, SOFTMAX_ALL preset),
 R10 top-k ties -> lower expert id, R10b a NaN logit ranks as -inf, R11 SiLU gated MLP, R12 bf16 intermediate,
-R15 shared experts weight 1.
+R15 shared experts weight 1; R15b (Qwen2-MoE's gated shared expert, beyond the
+paper's ungated "isolated shared experts") weight sigmoid(z) of a per-token
+shared-gate logit z.
 """
 from __future__ import annotations
 
@@ -91,10 +93,12 @@ def expert_ffn(wg: Encoded, wu: Encoded, wd: Encoded, x_bits: np.ndarray, sel: n
 
 
 def moe_layer(experts, x_bits: np.ndarray, logits: np.ndarray, top_k: int,
-              mode: int = RENORM_TOPK, shared=()):
-    """out[t] = sum_{(e,g) in route(t)} g * y_e[t]  (+ sum_s y_s[t]).
+              mode: int = RENORM_TOPK, shared=(), shared_logits=None):
+    """out[t] = sum_{(e,g) in route(t)} g * y_e[t]  (+ sum_s c_s[t] y_s[t]).
 
     experts: list of (wg, wu, wd) Encoded; shared: same for shared experts.
+    c_s[t] = 1 (R15), or, when shared_logits [T x len(shared)] fp32 is given,
+    c_s[t] = 1 / (1 + exp(-shared_logits[t, s])) (R15b, computed in fp64).
     Returns (out [T x d] fp64, S [T x d] error scale)."""
     x_bits = np.asarray(x_bits)
     T = x_bits.shape[0]
@@ -113,10 +117,15 @@ def moe_layer(experts, x_bits: np.ndarray, logits: np.ndarray, top_k: int,
             out[t] += g[i] * y[i]
             scale[t] += abs(g[i]) * S[i]
     all_t = np.arange(T)
-    for (wg, wu, wd) in shared:
+    for si, (wg, wu, wd) in enumerate(shared):
         y, _, S = expert_ffn(wg, wu, wd, x_bits, all_t)
-        out += y
-        scale += S
+        if shared_logits is None:
+            c = np.ones(T)
+        else:
+            z = np.asarray(shared_logits, dtype=np.float32)[:, si].astype(np.float64)
+            c = 1.0 / (1.0 + np.exp(-z))
+        out += c[:, None] * y
+        scale += np.abs(c)[:, None] * S
     return out, scale
 
 

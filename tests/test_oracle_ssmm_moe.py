@@ -304,6 +304,35 @@ def test_layer_all_tokens_one_expert_and_shared():
     assert np.allclose(out2, y + y0 + y1, rtol=1e-12, atol=1e-12)
 
 
+def test_layer_sigmoid_gated_shared_expert():
+    """Reading R15b (Qwen2-MoE's shared expert, scaled per token by the sigmoid of
+    a shared-gate logit): closed-form gates sigmoid(0) = 1/2, sigmoid(ln 3) = 3/4,
+    sigmoid(-ln 3) = 1/4, and the decomposition the bench relies on -- one shared
+    FFN of width 2f equals two width-f shared experts under the same gate, computed
+    here as the wide FFN from the decoded dense weights."""
+    fmt = F.SparseFormat(1, 2, 32)
+    E, d, f, T = 2, 64, 64, 3
+    ex = _experts(fmt, E, d, f)
+    x = synth.activations_bf16(1, T, d)
+    lg = np.zeros((T, E), dtype=np.float32)
+    lg[:, 0] = 5.0
+    y, _, _ = moe.expert_ffn(*ex[0], x, np.arange(T))
+    sh = _experts(fmt, 2, d, f, seed0=5000)
+    z = np.array([[0.0, 0.0], [np.log(3.0), np.log(3.0)], [-np.log(3.0), -np.log(3.0)]], dtype=np.float32)
+    out, S = moe.moe_layer(ex, x, lg, 1, shared=sh, shared_logits=z)
+    xf = bf16.to_f64(x)
+    g = xf @ np.vstack([F.dense_f64(sh[0][0]), F.dense_f64(sh[1][0])]).T       # [T x 2f]
+    u = xf @ np.vstack([F.dense_f64(sh[0][1]), F.dense_f64(sh[1][1])]).T
+    a = bf16.to_f64(bf16.from_f64(g / (1.0 + np.exp(-g)) * u))
+    wide = a @ np.hstack([F.dense_f64(sh[0][2]), F.dense_f64(sh[1][2])]).T      # [T x d]
+    c = np.array([0.5, 0.75, 0.25])
+    assert np.allclose(out[0], y[0] + 0.5 * wide[0], rtol=1e-12, atol=1e-12)      # z = 0 exactly
+    assert np.allclose(out, y + c[:, None] * wide, rtol=0, atol=1e-7)           # ln 3 rounded to fp32
+    out1, S1 = moe.moe_layer(ex, x, lg, 1, shared=sh)
+    assert np.allclose(out1, y + wide, rtol=1e-12, atol=1e-12)                 # ungated: weight 1 (R15)
+    assert (S <= S1 + 1e-12).all() and (S >= np.abs(out) - 1e-12).all()
+
+
 def test_ep_plan_covers_routing_once():
     E, P, T, k = 8, 4, 16, 2
     ids_r, w_r = [], []
