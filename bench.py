@@ -319,7 +319,10 @@ def run_ours(args):
     NS = args.shared
     if NS and (world > 1 or args.force_ep) and args.parallel == "ep":
         raise SystemExit("--shared: shared experts are measured on the 1-GPU / data-parallel layer")
-    cfg = P.MoEConfig(E, k, d, f, NS, gating, P.Format(*FMT), "auto", args.transcode)
+    SG = args.shared_gate
+    if SG == "sigmoid" and not NS:
+        raise SystemExit("--shared-gate sigmoid needs --shared N")
+    cfg = P.MoEConfig(E, k, d, f, NS, gating, P.Format(*FMT), "auto", args.transcode, shared_gate=SG)
     transport = None
     comm = None
     x = torch.empty(T, d, dtype=torch.int16, device=device)
@@ -360,8 +363,12 @@ def run_ours(args):
         layer = P.MoELayer(cfg, experts, shared=shared, max_tokens=T, device=device)
 
     P.synth_fill(x, synth.SEED_X + 100 * rank, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
-    lg = torch.empty(T, E, dtype=torch.float32, device=device)
+    lg = torch.empty(T, E + (NS if SG == "sigmoid" else 0), dtype=torch.float32, device=device)
     P.synth_fill(lg, synth.SEED_LOGITS + 100 * rank, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
+    if SG == "sigmoid":
+        # one shared-expert gate logit per token (Qwen2-MoE: shared_expert_gate is Linear(d, 1)),
+        # replicated into the columns of the NS width-f pieces of the wide shared FFN
+        lg[:, E:] = lg[:, E:E + 1]
     out = torch.empty(T, d, dtype=torch.float32, device=device)
     stream = torch.cuda.current_stream()
 
@@ -462,7 +469,7 @@ def run_ours(args):
         drun_ph()
         torch.cuda.synchronize()
         dpm = np.array([[dph[s][i].elapsed_time(dph[s][i + 1]) for i in range(5)] for s in range(Kd)]).mean(0)
-        ids_d = P.route(lgd, k, gating)[0].flatten().long()
+        ids_d = P.route(lgd[:, :E].contiguous(), k, gating)[0].flatten().long()
         act_d = int((torch.bincount(ids_d, minlength=E) > 0).sum().item()) + NS   # + shared experts
         kd = k + NS                                   # rows per token through the grouped launches
         gu_bytes = 2 * act_d * f * d * BYTES_PER_ELEM + Td * kd * d * 2 + Td * kd * 4 + Td * kd * f * 2
@@ -538,7 +545,7 @@ def run_ours(args):
     # ---------------- roofline of the dominant kernel (gate/up SSMM)
     hbm, bf16_burst, bf16_sust, src = peaks()
     sparse_peak = 2.0 * bf16_burst          # 2:4 sparse bf16 = 2 x dense (nominal ratio)
-    cnt = torch.bincount(P.route(lg, k, gating)[0].flatten().long(), minlength=E)
+    cnt = torch.bincount(P.route(lg[:, :E].contiguous(), k, gating)[0].flatten().long(), minlength=E)
     if world > 1:
         dist.all_reduce(cnt)                 # assignments per expert over all ranks
     cnt = cnt.cpu().numpy()
@@ -577,7 +584,7 @@ def run_ours(args):
         "metric": "moe_layer_tokens_per_s", "value": T * world / (ms * 1e-3), "unit": "tokens/s",
         "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": WORKLOAD[model] + (f"+{NS}shared" if NS else ""), "tokens_per_gpu": T, "global_tokens": T * world, "hidden": d,
+        "config": {"workload": WORKLOAD[model] + (f"+{NS}shared" if NS else "") + ("-sigmoid-gated" if SG == "sigmoid" else ""), "tokens_per_gpu": T, "global_tokens": T * world, "hidden": d,
                    "ffn": f, "experts": E, "top_k": k, "shared_experts": NS, "gating": gating, "format": "(N,M,V)=(%d,%d,%d) + 2:4" % FMT + (" (run as plain 2:4)" if cfg.kernel_config() is not cfg
                                                                else ""),
                    "parallelism": ((f"ep{world} (experts sharded; token rows / outputs over NVLink peer memory "
@@ -598,7 +605,7 @@ def run_ours(args):
         "down_ssmm_tflops": (flops_gu / 2) / (ph_ms[3] * 1e-3) / 1e12,
         "roofline": roof,
         "e2e": {"value": T * world / (ms_e2e * 1e-3), "unit": "tokens/s",
-                "h2d_bytes_per_step": T * d * 2 + T * E * 4, "d2h_bytes_per_step": T * d * (2 if e2e_bf16 else 4),
+                "h2d_bytes_per_step": T * d * 2 + T * lg.shape[1] * 4, "d2h_bytes_per_step": T * d * (2 if e2e_bf16 else 4),
                 "out_dtype": "bf16" if e2e_bf16 else "f32",
                 "overlap": "copies of steps s+1 / s-1 on separate streams beside step s (double-buffered)"},
         "decode": dec,
@@ -705,6 +712,9 @@ def main():
                     help="launch / process-group / timing path only, on CPU (gloo): prints the contract line")
     ap.add_argument("--shared", type=int, default=0,
                     help="shared experts (every token, weight 1) after the routed ones, e.g. 2 for DeepSeek-MoE")
+    ap.add_argument("--shared-gate", default="none", choices=["none", "sigmoid"],
+                    help="shared experts weighted 1 (default) or by a per-token sigmoid gate (Qwen2-MoE: "
+                         "--model qwen2 --shared 8 --shared-gate sigmoid = its width-20480 shared expert)")
     ap.add_argument("--decode-tokens", type=int, default=64, help="extra decode point on the same layer (0: off)")
     args = ap.parse_args()
     set_format(args.format)

@@ -202,6 +202,14 @@ SMY_API smy_status samoyeds_route(const float* logits, int64_t T, int32_t E, int
  * every token).  x dev bf16 [T x hidden]; logits dev fp32
  * [T x E]; out dev [T x hidden] (overwritten), fp32 or bf16 (cfg->out_dtype).  The gate/up -> down
  * intermediate is bf16 (reading R12).                                     */
+/* cfg->gating = SMY_GATE_RENORM_TOPK | SMY_GATE_SOFTMAX_ALL, optionally OR-ed
+ * with SMY_GATE_SHARED_SIGMOID when num_shared > 0 (single-GPU layer only, else
+ * SMY_E_CONFIG): the logits then have num_experts + num_shared columns and
+ * shared expert s is weighted per token by 1 / (1 + exp(-logits[t][E + s]))
+ * instead of 1 (Qwen2-MoE's gated shared expert; reading R15b --
+ * a shared FFN wider than the routed ones runs as several shared experts of
+ * the routed width with the same logit in each of their columns).          */
+#define SMY_GATE_SHARED_SIGMOID 0x10
 #define SMY_GU_SEPARATE 0
 #define SMY_GU_INTERLEAVED 1
 typedef struct {

@@ -18,6 +18,7 @@ from ._lib import check, smy_format, smy_moe_config, smy_wdesc, smy_weight, smy_
 EPI = {"compact": 0, "silu_mul": 1, "scatter_add": 2, "silu_mul_interleaved": 3}
 GATE_UP = {"separate": 0, "interleaved": 1}
 GATING = {"renorm_topk": 0, "softmax_all": 1}
+SHARED_GATE = {"none": 0, "sigmoid": 0x10}   # SMY_GATE_SHARED_SIGMOID
 PRUNE_MAGNITUDE = 1
 ASSUME_PRUNED = 2
 
@@ -213,6 +214,10 @@ class MoEConfig:
     # layer output dtype: "f32" (default) or "bf16" (fp32 accumulation in the
     # workspace, one RNE rounding at the end; single-GPU layer)
     out_dtype: str = "f32"
+    # shared experts' weight: "none" = 1 (reading R15); "sigmoid" = sigmoid of a
+    # per-token shared-gate logit, taken from logits[:, num_experts + s] (the
+    # logits then have num_experts + num_shared columns; Qwen2-MoE, reading R15b)
+    shared_gate: str = "none"
 
     def fast_format(self) -> bool:
         f = self.fmt
@@ -228,12 +233,13 @@ class MoEConfig:
         """The configuration the layer's kernels run on (after transcoding)."""
         if self.transcode == "auto" and not self.fast_format():
             return MoEConfig(self.num_experts, self.top_k, self.hidden, self.ffn, self.num_shared, self.gating,
-                             Format(2, 2, 32), self.gate_up, "off", self.out_dtype)
+                             Format(2, 2, 32), self.gate_up, "off", self.out_dtype, self.shared_gate)
         return self
 
     def c(self) -> smy_moe_config:
         return smy_moe_config(self.num_experts, self.top_k, self.hidden, self.ffn, self.num_shared,
-                              GATING[self.gating], self.fmt.c(), GATE_UP[self.resolved_gate_up()],
+                              GATING[self.gating] | SHARED_GATE[self.shared_gate], self.fmt.c(),
+                              GATE_UP[self.resolved_gate_up()],
                               {"f32": 0, "bf16": 1}[self.out_dtype])
 
 

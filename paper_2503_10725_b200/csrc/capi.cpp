@@ -391,7 +391,11 @@ smy_status samoyeds_moe_layer(const smy_moe_config* cfg, const smy_weight* exper
     return SMY_E_CONFIG;
   // shared experts run as extra groups with extra routing entries per token
   if (cfg->num_experts + cfg->num_shared > kMaxGroups || cfg->top_k + cfg->num_shared > 16) return SMY_E_CONFIG;
-  if (cfg->gating != SMY_GATE_RENORM_TOPK && cfg->gating != SMY_GATE_SOFTMAX_ALL) return SMY_E_CONFIG;
+  {
+    const int base = cfg->gating & ~SMY_GATE_SHARED_SIGMOID;
+    if (base != SMY_GATE_RENORM_TOPK && base != SMY_GATE_SOFTMAX_ALL) return SMY_E_CONFIG;
+    if ((cfg->gating & SMY_GATE_SHARED_SIGMOID) && (cfg->num_shared < 1 || comm != nullptr)) return SMY_E_CONFIG;
+  }
   if (cfg->out_dtype != SMY_F32 && cfg->out_dtype != SMY_BF16) return SMY_E_CONFIG;
   if (cfg->out_dtype == SMY_BF16 && comm != nullptr) return SMY_E_CONFIG;
   if (cfg->hidden % 128 || cfg->ffn % 128) return SMY_E_SHAPE;

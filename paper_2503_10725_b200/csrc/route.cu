@@ -68,13 +68,15 @@ __device__ __forceinline__ void topk_warp(const float* __restrict__ lg, int E, i
 // SSMM launches run shared and routed experts together.
 __device__ __forceinline__ void topk_token(const float* __restrict__ lg, int E, int k, int gating, int lane,
                                            int32_t* __restrict__ ids, float* __restrict__ w, int ns = 0) {
-  if (E <= 32) topk_warp<1>(lg, E, k, gating, lane, ids, w);
-  else if (E <= 64) topk_warp<2>(lg, E, k, gating, lane, ids, w);
-  else if (E <= 128) topk_warp<4>(lg, E, k, gating, lane, ids, w);
-  else topk_warp<8>(lg, E, k, gating, lane, ids, w);
+  const int g = gating & ~SMY_GATE_SHARED_SIGMOID;
+  if (E <= 32) topk_warp<1>(lg, E, k, g, lane, ids, w);
+  else if (E <= 64) topk_warp<2>(lg, E, k, g, lane, ids, w);
+  else if (E <= 128) topk_warp<4>(lg, E, k, g, lane, ids, w);
+  else topk_warp<8>(lg, E, k, g, lane, ids, w);
   if (lane < ns) {
     ids[k + lane] = E + lane;
-    w[k + lane] = 1.f;
+    // reading R15 (weight 1) or R15b (sigmoid of the shared expert's own logit column)
+    w[k + lane] = (gating & SMY_GATE_SHARED_SIGMOID) ? 1.f / (1.f + expf(-lg[E + lane])) : 1.f;
   }
 }
 
@@ -148,7 +150,8 @@ __global__ void route_topk_kernel(const float* __restrict__ logits, int64_t T, i
   const int64_t t = (int64_t)blockIdx.x * kRouteWarps + threadIdx.x / 32;
   if (t >= T) return;
   const int kk = k + ns;  // row stride: routed entries, then shared
-  topk_token(logits + t * E, E, k, gating, lane, ids + t * kk, w + t * kk, ns);
+  const int ld = E + ((gating & SMY_GATE_SHARED_SIGMOID) ? ns : 0);  // logits row: E router (+ ns shared-gate)
+  topk_token(logits + t * ld, E, k, gating, lane, ids + t * kk, w + t * kk, ns);
 }
 
 __global__ void route_count_kernel(const int32_t* __restrict__ ids, int64_t T, int E, int k,
@@ -176,8 +179,8 @@ __device__ __forceinline__ void small_route(const float* __restrict__ logits, in
   if (logits != nullptr) {
     // E, k here include the ns shared experts; the router covers the first E - ns
     for (int t = wp; t < T; t += kRouteWarps)
-      topk_token(logits + (int64_t)t * (E - ns), E - ns, k - ns, gating, lane, ids + (int64_t)t * k,
-                 w + (int64_t)t * k, ns);
+      topk_token(logits + (int64_t)t * ((gating & SMY_GATE_SHARED_SIGMOID) ? E : E - ns), E - ns, k - ns, gating,
+                 lane, ids + (int64_t)t * k, w + (int64_t)t * k, ns);
   }
   __syncthreads();
   build_masks(ids, T, E, k, mask);

@@ -19,6 +19,9 @@
 // `acc_full`; both epilogues arrive on the leader's `acc_empty`.
 #include "ssmm_kernel.cuh"
 
+#ifndef SMY_GATHER_SPIN
+#define SMY_GATHER_SPIN 0
+#endif
 #ifndef SMY_PAIR_W_EVICT_FIRST
 #define SMY_PAIR_W_EVICT_FIRST 0
 #endif
@@ -502,7 +505,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % SB;
           unsigned long long tg0 = prof ? clk() : 0;
-          mbar_wait_cta(&bempty[st], ((it / SB) & 1) ^ 1);
+          if (SMY_GATHER_SPIN)
+            mbar_spin(&bempty[st], ((it / SB) & 1) ^ 1);
+          else
+            mbar_wait_cta(&bempty[st], ((it / SB) & 1) ^ 1);
           if (prof) {
             const unsigned long long t1 = clk();
             pc[10] += t1 - tg0;

@@ -23,6 +23,10 @@ P.synth_fill(x, synth.SEED_X, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
 lg = torch.empty(T, E, dtype=torch.float32, device=dev)
 P.synth_fill(lg, synth.SEED_LOGITS, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
 out = torch.empty(T, d, dtype=torch.float32, device=dev)
+import contextlib
+variant = sys.argv[3] if len(sys.argv) > 3 else None
+ctx = layer.variant(variant, T) if variant else contextlib.nullcontext()
+ctx.__enter__()
 for _ in range(3):
     layer(x, lg, out)
 buf = (C.c_ulonglong * (148 * 32))()

@@ -355,8 +355,8 @@ def test_route_ties(smy):
 # ------------------------------------------------------------------ MoE layer
 
 def _layer_case(smy, fmt, E, d, f, T, k, gating="renorm_topk", shared=0, skew=0.0, seed_off=0, gate_up="auto",
-                transcode="auto", variant=None):
-    cfg = smy.MoEConfig(E, k, d, f, shared, gating, gpu_format(fmt), gate_up, transcode)
+                transcode="auto", variant=None, shared_gate="none"):
+    cfg = smy.MoEConfig(E, k, d, f, shared, gating, gpu_format(fmt), gate_up, transcode, shared_gate=shared_gate)
     encs, sws = [], []
     for e in range(E + shared):
         te, ts = [], []
@@ -368,7 +368,8 @@ def _layer_case(smy, fmt, E, d, f, T, k, gating="renorm_topk", shared=0, skew=0.
         encs.append(tuple(te))
         sws.append(tuple(ts))
     x = synth.activations_bf16(synth.SEED_X, T, d)
-    lg = synth.router_logits(synth.SEED_LOGITS, T, E, skew=skew)
+    sig = shared_gate == "sigmoid"
+    lg = synth.router_logits(synth.SEED_LOGITS, T, E + (shared if sig else 0), skew=skew)
     layer = smy.MoELayer(cfg, sws[:E], sws[E:], max_tokens=max(T, 1))
     if variant is None:
         got = layer(dev16(x), torch.from_numpy(lg).cuda()).cpu().numpy().astype(np.float64)
@@ -376,7 +377,7 @@ def _layer_case(smy, fmt, E, d, f, T, k, gating="renorm_topk", shared=0, skew=0.
         with layer.variant(variant, T):
             got = layer(dev16(x), torch.from_numpy(lg).cuda()).cpu().numpy().astype(np.float64)
     mode = moe.SOFTMAX_ALL if gating == "softmax_all" else moe.RENORM_TOPK
-    ref, S = moe.moe_layer(encs[:E], x, lg, k, mode, shared=encs[E:])
+    ref, S = moe.moe_layer(encs[:E], x, lg[:, :E], k, mode, shared=encs[E:], shared_logits=lg[:, E:] if sig else None)
     return got, ref, S
 
 
@@ -397,8 +398,14 @@ def _layer_case(smy, fmt, E, d, f, T, k, gating="renorm_topk", shared=0, skew=0.
     # routing (T <= 32), and k + shared = 9 entries per token (Qwen2-like top-8 + 1)
     dict(fmt=F.SparseFormat(1, 2, 32), E=16, d=256, f=384, T=20, k=8, gating="softmax_all", shared=1),
     dict(fmt=F.SparseFormat(1, 2, 32), E=16, d=256, f=384, T=300, k=8, gating="softmax_all", shared=1),
+    # Qwen2-MoE's sigmoid-gated shared expert (reading R15b): a width-4f shared FFN as 4
+    # shared experts under one logit per token -- decode (one-block routing) and prefill
+    dict(fmt=F.SparseFormat(1, 2, 32), E=16, d=256, f=384, T=20, k=4, gating="softmax_all", shared=4,
+         shared_gate="sigmoid"),
+    dict(fmt=F.SparseFormat(1, 2, 32), E=16, d=256, f=384, T=300, k=8, gating="softmax_all", shared=8,
+         shared_gate="sigmoid"),
 ], ids=lambda c: (f"{c['fmt']}-E{c['E']}-T{c['T']}-{c.get('gate_up', 'auto')}-{c.get('transcode', 'auto')}"
-                  f"-sh{c.get('shared', 0)}"))
+                  f"-sh{c.get('shared', 0)}{c.get('shared_gate', '')}"))
 def test_moe_layer_parity(smy, case):
     case = dict(case)
     fmt = case.pop("fmt")
