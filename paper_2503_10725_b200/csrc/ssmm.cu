@@ -168,18 +168,22 @@ smy_status ssmm_launch_pair(const SsmmArgs& a0, int nt, int nw, int ms, int cl, 
   return SMY_E_CONFIG;
 }
 
+#ifndef SMY_KSPLIT_MIN_STAGES
+#define SMY_KSPLIT_MIN_STAGES 8
+#endif
 int ssmm_pick_ksplit(int64_t tiles, int k_stages) {
   // Split K so that tiles x splits fills whole waves of the 148 SMs: among the
   // splits that keep >= 8 K-stages per piece and give >= 2 pieces per SM, take
   // the one whose last wave is fullest (work / (waves x 148)), preferring fewer
   // splits on ties (less partial-sum traffic).
   const int64_t sms = 148;
-  if (tiles >= 4 * sms || k_stages < 16) return 1;
+  constexpr int kMin = SMY_KSPLIT_MIN_STAGES;  // K-stages per piece at least
+  if (tiles >= 4 * sms || k_stages < 2 * kMin) return 1;
   int best = 1;
   double best_eff = 0.0;
-  for (int ks = 1; ks <= k_stages / 8; ++ks) {
+  for (int ks = 1; ks <= k_stages / kMin; ++ks) {
     const int64_t n = tiles * ks;
-    if (n < 2 * sms && ks < k_stages / 8) continue;
+    if (n < 2 * sms && ks < k_stages / kMin) continue;
     const int64_t waves = (n + sms - 1) / sms;
     const double eff = (double)n / (double)(waves * sms);
     if (eff > best_eff + 0.02) {

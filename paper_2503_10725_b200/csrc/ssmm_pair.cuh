@@ -250,7 +250,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
   uint8_t* zbuf = aux + 1024;  // 1 KB of zeros: the operand of the accumulator-clearing MMA
   // SMY_DEBUG & 128: clock at which the leader's gather thread 0 issued each token slot
   volatile unsigned long long* ts_issue = reinterpret_cast<volatile unsigned long long*>(aux + 512);
-  if (threadIdx.x < 8) ts_issue[threadIdx.x] = 0;
   // TMEM allocation first, ordered before every other shared-memory write of the
   // prologue (compute-sanitizer racecheck flagged the allocator's slot write
   // against the prologue's stores when they were unordered)
@@ -260,6 +259,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
     reinterpret_cast<uint32_t*>(zbuf)[threadIdx.x] = 0u;
     fence_proxy_async_smem();
   }
+  if (threadIdx.x < 8) ts_issue[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     if constexpr (SPLIT) {
       for (int s = 0; s < SW; ++s) {
