@@ -226,7 +226,12 @@ class MoEConfig:
     def resolved_gate_up(self) -> str:
         if self.gate_up != "auto":
             return self.gate_up
-        ok = self.fast_format() and self.ffn % 128 == 0
+        # (1,2,V): the interleaved weight (one SSMM, two lane-masked slots); N = M:
+        # gate and up as the two weights of one launch (two accumulators per token
+        # stage, half the SEL-gather bytes per MMA of the interleaved one-slot
+        # kernel: Mixtral (2,2,32) gate/up 2.04 -> 1.08 ms, profiles/r2_nm_formats.md)
+        f = self.fmt
+        ok = f.v % 32 == 0 and f.n == 1 and f.m == 2 and self.ffn % 128 == 0
         return "interleaved" if ok else "separate"
 
     def kernel_config(self) -> "MoEConfig":

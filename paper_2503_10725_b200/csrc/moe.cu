@@ -456,7 +456,8 @@ smy_status moe_kernel_names(const smy_moe_config* c, int64_t T, char* gu, char* 
   const int cl_dn = ssmm_pair_cluster(nt_dn, 1, gdn.ms, gdn.rep, gdn.m_tiles, tpg, 0);
   // the SEL-gather pair launch of the widest (1,2,V) tile runs split rings (ssmm.cu)
   const int split_gu =
-      cl_gu && ggu.ms == 2 && nw_gu == 1 && (nt_gu == SMY_NT_WIDE || nt_gu == 128) && !(debug_flags() & 16384);
+      cl_gu && ((ggu.ms == 2 && nw_gu == 1 && (nt_gu == SMY_NT_WIDE || nt_gu == 128) && !(debug_flags() & 16384)) ||
+                (ggu.ms == 1 && nw_gu == 2 && nt_gu == 224));
   if (cl_gu)
     snprintf(gu, len, "ssmm_pair_kernel<%d, %d, %d, %d>", nt_gu, nw_gu, ggu.ms, split_gu);
   else

@@ -36,6 +36,7 @@ extern template smy_status launch_pair_t<128, 1, 2, 0>(const SsmmArgs&, cudaStre
 extern template smy_status launch_pair_t<SMY_NT_WIDE, 1, 2, 0>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<SMY_NT_WIDE, 1, 2, 1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<128, 1, 2, 1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<224, 2, 1, 1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<128, 1, 1, 0>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<256, 1, 1, 0>(const SsmmArgs&, cudaStream_t);
 
@@ -89,7 +90,9 @@ int ssmm_pair_cluster(int nt, int nw, int ms, int rep, int m_tiles, int64_t toke
   // an odd m-tile count gives the last pair a phantom peer tile (loads repeated, stores masked)
   if (rep != 1 || m_tiles < 2 || tokens_per_group < 64) return 0;
   if (ms == 2 && !(nw == 2 ? (nt == 64 || nt == 112) : (nt == 128 || nt == SMY_NT_WIDE))) return 0;
-  if (ms == 1 && !(nw == 1 && (nt == 128 || nt == 256))) return 0;  // N == M: plain 2:4
+  // N == M (plain 2:4): one weight at 128 / 256 tokens, or gate + up (NW = 2) at 224 --
+  // two weights per token stage halve the SEL-gather bytes per MMA
+  if (ms == 1 && !((nw == 1 && (nt == 128 || nt == 256)) || (nw == 2 && nt == 224))) return 0;
   if (ms != 1 && ms != 2) return 0;
   // (4-CTA clusters sharing weight stages by multicast measured 2x slower on
   // B200 -- probes/mcast_bench.cu -- and were removed)
@@ -162,6 +165,7 @@ smy_status ssmm_launch_pair(const SsmmArgs& a0, int nt, int nw, int ms, int cl, 
   if (ms == 2 && nw == 1 && nt == SMY_NT_WIDE)
     return (a.sel_in && !(a.debug & 16384)) || (a.debug & 262144) ? launch_pair_t<SMY_NT_WIDE, 1, 2, 1>(a, s)
                                                                   : launch_pair_t<SMY_NT_WIDE, 1, 2, 0>(a, s);
+  if (ms == 1 && nw == 2 && nt == 224) return launch_pair_t<224, 2, 1, 1>(a, s);  // gather launches only
   if (ms == 1 && nw == 1 && nt == 128) return launch_pair_t<128, 1, 1, 0>(a, s);
   if (ms == 1 && nw == 1 && nt == 256) return launch_pair_t<256, 1, 1, 0>(a, s);
   set_last_error("ssmm: unsupported pair (nt, nw)");

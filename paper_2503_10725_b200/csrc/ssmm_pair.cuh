@@ -632,6 +632,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
           }
           continue;
         }
+        if constexpr (MS == 1 && NW == 2) {  // N == M, gate and up: lane = output row
+          const int64_t r0 = ti.row0 + ti.t0 + c0;
+          uint16_t* o = static_cast<uint16_t*>(a.out) + r0 * a.ldo + cr;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (j < n) *o = __bfloat16_as_ushort(__float2bfloat16_rn(silu_mul(v[0][0][j], v[1][0][j])));
+            o += a.ldo;
+          }
+          continue;
+        }
         if constexpr (MS == 1) {  // N == M compact: lane = output row, fp32 or bf16
           const int64_t r0 = ti.row0 + ti.t0 + c0;
           if (a.out_bf16) {

@@ -392,6 +392,9 @@ def _layer_case(smy, fmt, E, d, f, T, k, gating="renorm_topk", shared=0, skew=0.
     dict(fmt=F.SparseFormat(4, 8, 32), E=4, d=256, f=256, T=300, k=2, transcode="off"),   # lane-masked M=8 slots
     dict(fmt=F.SparseFormat(8, 16, 32), E=4, d=256, f=256, T=50, k=2, transcode="off"),
     dict(fmt=F.SparseFormat(2, 2, 32), E=4, d=256, f=512, T=400, k=2),                   # plain 2:4, pair kernels
+    # N = M gate + up as two weights of one pair launch (NW = 2: half the gather bytes per MMA)
+    dict(fmt=F.SparseFormat(2, 2, 32), E=4, d=512, f=512, T=600, k=2, gate_up="separate"),
+    dict(fmt=F.SparseFormat(4, 8, 32), E=4, d=256, f=512, T=500, k=2, gate_up="separate", skew=1.0),
     dict(fmt=F.SparseFormat(1, 2, 32), E=16, d=256, f=384, T=57, k=6, gating="softmax_all", shared=2,
          gate_up="separate"),
     # shared experts folded into the grouped launches: top-k fused into the one-block
