@@ -104,6 +104,9 @@ struct SsmmPlan {
 };
 // Choose the token tile for a launch given the expected tokens per group.
 int ssmm_pick_nt(int nw, int ms, int rep, int64_t tokens_per_group);
+// gathered token pools larger than this run their tiles m-tile fastest (L2 is 126 MB;
+// the weight tiles in flight and the outputs share it)
+constexpr int64_t kGatherL2Bytes = 64ll << 20;
 smy_status ssmm_launch(const SsmmArgs& a, int nt, int nw, int ms, int rep, cudaStream_t s);
 // CTA-pair (cta_group::2) kernel: a.m_tiles / tile prefixes count m-tile PAIRS, tmap box = nt/2 rows
 // returns the cluster size to use (2: one MMA pair, 4: two pairs sharing weights) or 0 (single CTA)

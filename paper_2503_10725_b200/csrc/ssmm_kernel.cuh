@@ -697,7 +697,11 @@ smy_status launch_t(const SsmmArgs& a, cudaStream_t s) {
   b.streamk = a.epi == kEpiScatter && a.k_splits <= 1 && !(a.debug & 512);
   const int grid = (b.streamk || a.max_tiles >= num_sms) ? num_sms : a.max_tiles;
   b.workers = grid;
-  b.m_fastest = a.epi == kEpiScatter && !(a.debug & 2048);
+  // m-tile fastest (concurrent tiles share the token tile in L2) for the scatter (down)
+  // launches, and for SEL-gather launches whose token pool does not fit in L2 (their
+  // n-fastest order would re-stream the gathered rows from HBM for every m-tile)
+  b.m_fastest = (a.epi == kEpiScatter || (a.sel_in != nullptr && (int64_t)a.x_rows * a.ldx * 2 > kGatherL2Bytes)) &&
+                !(a.debug & 2048);
   kern<<<grid, kThreads, C::kSmemBytes, s>>>(b);
   count_launch();
   return cuda_status(cudaGetLastError());

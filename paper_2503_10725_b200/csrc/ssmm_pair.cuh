@@ -745,7 +745,11 @@ smy_status launch_pair_t(const SsmmArgs& a, cudaStream_t s) {
   // stream-K launches use every pair: with fewer tiles than pairs the K pieces fill them
   const int pairs = (b.streamk || a.max_tiles >= num_sms / 2) ? num_sms / 2 : a.max_tiles;
   b.workers = pairs;
-  b.m_fastest = a.epi == kEpiScatter && !(a.debug & 2048);
+  // m-tile fastest (concurrent tiles share the token tile in L2) for the scatter (down)
+  // launches, and for SEL-gather launches whose token pool does not fit in L2 (their
+  // n-fastest order would re-stream the gathered rows from HBM for every m-tile)
+  b.m_fastest = (a.epi == kEpiScatter || (a.sel_in != nullptr && (int64_t)a.x_rows * a.ldx * 2 > kGatherL2Bytes)) &&
+                !(a.debug & 2048);
   kern<<<2 * pairs, pair_threads(SPLIT), C::kSmemBytes, s>>>(b);
   count_launch();
   return cuda_status(cudaGetLastError());

@@ -10,6 +10,9 @@ C[n x M] = x[sel] W^T, bf16 in, fp32 accumulate:
   ssmm (1,2,32)  our SSMM on the Samoyeds format (vector-wise + 2:4, 75 % sparse),
                  rows read through SEL  -- the paper's dual-side sparse kernel
   ssmm (1,2,16)  same at V = 16, run as its plain-2:4 transcode (the layer's path)
+  cusparselt     the vendor weight-only 2:4 kernel (cuSPARSELt through torch's
+                 to_sparse_semi_structured) on pre-gathered rows -- TIMING ONLY: torch's
+                 binding returns wrong values on this box (probes/cslt_dbg.py)
 Every kernel writes fp32 [n x M].  Timing: CUDA events around the op only,
 median of R iterations, L2 flushed (a 512 MB memset) before each.
 Useful TFLOP/s follow SURVEY §8(d): 2 * (M * N/M_fmt) * K * n for ours (the
@@ -70,6 +73,15 @@ def main():
                          float(synth.uniform_scale(np.sqrt(3.0 / K))))
             wd = wt.view(torch.bfloat16)
             sws = {name: P.compress(wt, fmt)[0] for name, fmt in fmts.items()}
+            try:
+                from torch.sparse import SparseSemiStructuredTensor, to_sparse_semi_structured
+                SparseSemiStructuredTensor._FORCE_CUTLASS = False
+                g = wd.float().view(M, K // 4, 4)
+                keep = torch.zeros_like(g, dtype=torch.bool).scatter_(-1, g.abs().topk(2, dim=-1).indices, True)
+                w24 = to_sparse_semi_structured((g * keep).view(M, K).to(torch.bfloat16))
+            except Exception as exc:  # no cuSPARSELt: the column stays empty
+                print("cusparselt unavailable:", repr(exc)[:120], file=sys.stderr)
+                w24 = None
             # V=16 has no fast kernel of its own: the library's path is its plain-2:4 transcode
             sws["ssmm (1,2,16)"] = P.transcode_24(sws["ssmm (1,2,16)"])
             for sw in sws.values():
@@ -82,17 +94,21 @@ def main():
                 r["ms"]["cublas+gather"] = timed(lambda: torch.matmul(torch.index_select(xb, 0, sel.long()), wd.t(),
                                                                       out=None), flush, args.reps)
                 r["ms"]["cublas"] = timed(lambda: torch.matmul(xs, wd.t()), flush, args.reps)
+                if w24 is not None:
+                    xst = xs.t().contiguous()
+                    r["ms"]["cusparselt"] = timed(lambda: torch.mm(w24, xst), flush, args.reps)
                 for name, sw in sws.items():
                     r["ms"][name] = timed(lambda: P.ssmm(sw, x, sel, out=out), flush, args.reps)
                 dense_flops = 2.0 * M * K * n
                 r["eff_tflops"] = {k: dense_flops / (v * 1e-3) / 1e12 for k, v in r["ms"].items()}
-                r["useful_tflops"] = {k: (dense_flops * (fmts[k].n / fmts[k].m) if k in fmts else dense_flops)
+                r["useful_tflops"] = {k: (dense_flops * (fmts[k].n / fmts[k].m) if k in fmts else
+                                          dense_flops / 2 if k == "cusparselt" else dense_flops)
                                       / (v * 1e-3) / 1e12 for k, v in r["ms"].items()}
                 r["speedup_vs_cublas_gather"] = {k: r["ms"]["cublas+gather"] / v for k, v in r["ms"].items()}
                 rows.append(r)
                 print(json.dumps({"M": M, "K": K, "n": n, **{k: round(v, 4) for k, v in r["ms"].items()}}),
                       file=sys.stderr, flush=True)
-            del sws, wt
+            del sws, wt, w24
         del x
     print(json.dumps({"_note": __doc__.strip().splitlines()[0], "device": torch.cuda.get_device_name(),
                       "rows": rows}, indent=1))
