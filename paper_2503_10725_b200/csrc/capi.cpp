@@ -335,6 +335,25 @@ smy_status samoyeds_ssmm(const smy_weight* w, const smy_weight* w2, const void* 
       a.scale = nullptr;
     }
   }
+  // N = M weight, > 128 tokens: m-tile pairing on the CTA pair -- the weight's second half
+  // of m-tiles runs as a second "weight" of the same launch, so every SEL-gathered token
+  // stage feeds two accumulators (half the gather bytes per MMA of the one-slot kernel)
+  if (nw == 1 && g.ms == 1 && g.rep == 1 && g.m_tiles >= 2 && !(debug_flags() & 131072)) {
+    const int nt2 = ssmm_pick_nt(2, 1, 1, n_sel);
+    const int half = (g.m_tiles + 1) / 2;
+    const smy_weight* w0a[1] = {w};
+    const size_t img = (size_t)g.m_tiles * g.k_stages * g.block;
+    if (nt2 == 224 && ssmm_pair_images_ok(w0a, nullptr, 1, img) &&
+        ssmm_pair_cluster(nt2, 2, 1, 1, half, n_sel, 1) == 2) {
+      a.img1[0] = a.img0[0] + (size_t)half * g.k_stages * g.block;
+      a.m_tiles = half;
+      a.mtp_half = half;
+      a.max_tiles = ((half + 1) / 2) * ((n_sel + nt2 - 1) / nt2);
+      a.k_splits = 1;
+      if ((st = make_x_tmap(&a.tmap_x, x_bf16, w->d.cols, x_rows, ldx, nt2 / 2)) != SMY_OK) return st;
+      return ssmm_launch_pair(a, nt2, 2, 1, 2, static_cast<cudaStream_t>(stream));
+    }
+  }
   // >= 64 tokens of a (1,2,V) weight: CTA-pair tiles (M = 256, cta_group::2), as in the layer
   const smy_weight* w0a[1] = {w};
   const smy_weight* w1a[1] = {nw == 2 ? w2 : nullptr};

@@ -65,6 +65,11 @@ struct SsmmArgs {
   int64_t ldo;
   const int32_t* sel_out;  // scatter destinations (SCATTER only)
   const int32_t* rows_out;  // SILU_MUL_ILV output row of compact row r (ablation variant only; NULL: r)
+  // m-tile pairing (N = M single weights on the pair kernel, NW = 2): "weight" 1 is the
+  // same weight's m-tiles [mtp_half, 2 mtp_half) (img1 = img0 + mtp_half m-tiles), so every
+  // token stage feeds two accumulators; output rows of weight w are offset by
+  // w * mtp_half * 128; m_tiles = mtp_half; 0 = off
+  int mtp_half;
   const float* scale;      // scatter scale, NULL = 1
   int max_tiles;           // tile count (single group) / upper bound (grouped)
   int weights_stream;      // 1: weights read once per call (decode) -> L2 evict_first

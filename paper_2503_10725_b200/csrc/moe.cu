@@ -85,6 +85,13 @@ smy_status silu_mul_launch(const float* g, const float* u, int64_t rows, int64_t
 
 static bool gate_up_fused(const Geometry& g) { return !(g.ms >= 16); }
 
+// m-tile pairing of an N = M down launch (0 = off): wide token tiles on the CTA pair
+static int down_mtp_half(const Geometry& gdn, int64_t tpg, int64_t tpg_hi) {
+  if (gdn.ms != 1 || gdn.rep != 1 || gdn.m_tiles < 3 || (debug_flags() & 131072)) return 0;
+  const int half = (gdn.m_tiles + 1) / 2;
+  return ssmm_pick_nt(2, 1, 1, tpg_hi) == 224 && ssmm_pair_cluster(224, 2, 1, 1, half, tpg, 0) == 2 ? half : 0;
+}
+
 static bool interleaved(const smy_moe_config* c) { return c->gate_up == SMY_GU_INTERLEAVED; }
 
 smy_status moe_workspace_bytes(const smy_moe_config* c, int64_t T, size_t* bytes) {
@@ -115,7 +122,7 @@ static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* 
                           int epi, void* out, int64_t ldo, int out_bf16, const int32_t* sel_out,
                           const float* scale, int64_t k_cols, int stream_w, int k_splits, int cl,
                           cudaStream_t s, const PeerRows* peers = nullptr, float* zero_ptr = nullptr,
-                          int64_t zero_elems = 0, const int32_t* rows_out = nullptr) {
+                          int64_t zero_elems = 0, const int32_t* rows_out = nullptr, int mtp_half = 0) {
   SsmmArgs a;
   memset(&a, 0, sizeof(a));
   a.rows_out = rows_out;
@@ -157,6 +164,11 @@ static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* 
   a.max_tiles = max_tiles * k_splits;
   a.weights_stream = stream_w;
   a.k_splits = k_splits;
+  if (mtp_half > 0) {  // m-tile pairing: "weight" 1 = the same weight's m-tiles [half, 2 half)
+    for (int e = 0; e < groups; ++e) a.img1[e] = a.img0[e] + (size_t)mtp_half * g.k_stages * g.block;
+    a.m_tiles = mtp_half;
+    a.mtp_half = mtp_half;
+  }
   smy_status st = make_x_tmap(&a.tmap_x, x, k_cols, x_rows, ldx, cl ? nt / 2 : nt);
   if (st != SMY_OK) return st;
   return cl ? ssmm_launch_pair(a, nt, nw, g.ms, cl, s) : ssmm_launch(a, nt, nw, g.ms, g.rep, s);
@@ -261,19 +273,13 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   // through the SMs); ragged tiles issue MMAs of their own width
   const int64_t tpg_hi = tpg + (int64_t)(3.0 * sqrt((double)tpg) + 0.999);
   const int nt_gu = ssmm_pick_nt(nw_gu, ggu.ms, ggu.rep, tpg_hi);
-  const int nt_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, tpg_hi);
-  // expected down tiles -> K split (the scatter-add epilogue makes partial sums free)
+  int nt_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, tpg_hi);
   const int64_t act = E < T * k ? E : T * k;
   const Variant var = t_variant;
   if (var.v != 0) {  // ablation variants: the single-GPU interleaved layer with router logits
     if (!ilv || keys != nullptr || peers != nullptr) return SMY_E_CONFIG;
     if (variant_bytes(c, T, var.v) > var.bytes) return SMY_E_WORKSPACE;
   }
-  // the permute variant's down writes compact fp32 rows: no K split
-  const int ks_dn = var.v == SMY_VARIANT_PERMUTE
-                        ? 1
-                        : ssmm_pick_ksplit((int64_t)gdn.m_tiles * act * ((tpg + nt_dn - 1) / (nt_dn > 0 ? nt_dn : 1)),
-                                           gdn.k_stages);
   const smy_weight* wg[kMaxGroups];
   const smy_weight* wu[kMaxGroups];
   const smy_weight* wd[kMaxGroups];
@@ -288,9 +294,22 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   const bool pair_gu_ok = ssmm_pair_images_ok(wg, nw_gu == 2 ? wu : nullptr, E, img_gu);
   const bool pair_dn_ok = ssmm_pair_images_ok(wd, nullptr, E, img_dn);
   const int cl_gu = fused && pair_gu_ok ? ssmm_pair_cluster(nt_gu, nw_gu, ggu.ms, ggu.rep, ggu.m_tiles, tpg, 1) : 0;
-  const int cl_dn = pair_dn_ok ? ssmm_pair_cluster(nt_dn, 1, gdn.ms, gdn.rep, gdn.m_tiles, tpg, 0) : 0;
+  // N = M down weights with wide tiles: m-tile pairing on the CTA pair (the weight's
+  // second half of m-tiles as the launch's second weight, samoyeds_ssmm): every token
+  // stage of the intermediate feeds two accumulators
+  const int mtp_dn = pair_dn_ok && var.v != SMY_VARIANT_PERMUTE ? down_mtp_half(gdn, tpg, tpg_hi) : 0;
+  if (mtp_dn) nt_dn = 224;
+  const int mtiles_dn = mtp_dn ? mtp_dn : gdn.m_tiles;  // m-tiles per weight of the launch
+  const int cl_dn =
+      mtp_dn ? 2 : pair_dn_ok ? ssmm_pair_cluster(nt_dn, 1, gdn.ms, gdn.rep, gdn.m_tiles, tpg, 0) : 0;
+  // expected down tiles -> K split (the scatter-add epilogue makes partial sums free);
+  // the permute variant's down writes compact fp32 rows: no K split
+  const int ks_dn = var.v == SMY_VARIANT_PERMUTE
+                        ? 1
+                        : ssmm_pick_ksplit((int64_t)mtiles_dn * act * ((tpg + nt_dn - 1) / (nt_dn > 0 ? nt_dn : 1)),
+                                           gdn.k_stages);
   const int mt_gu = cl_gu ? (ggu.m_tiles + 1) / 2 : ggu.m_tiles;
-  const int mt_dn = cl_dn ? (gdn.m_tiles + 1) / 2 : gdn.m_tiles;
+  const int mt_dn = cl_dn ? (mtiles_dn + 1) / 2 : mtiles_dn;
   // the routing scan counts tiles per expert in units of the launch's token span
   const int nts[2] = {nt_gu, nt_dn};
   const int mts[2] = {mt_gu, mt_dn * ks_dn};
@@ -373,8 +392,9 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
     st = grouped(wd, nullptr, E, gdn, d, nt_dn, 1, inter_dense, f, (int64_t)E * T, rows_dense, w.offsets, prefix_dn,
                  max_dn, kEpiScatter, out, d, 0, w.sel, w.gw, f, tpg <= nt_dn, ks_dn, cl_dn, s);
   } else {
-    st = grouped(wd, nullptr, E, gdn, d, nt_dn, 1, w.inter, f, Tk, nullptr, w.offsets, prefix_dn, max_dn, kEpiScatter,
-                 out, peers ? peers->ldo : d, 0, w.sel, w.gw, f, tpg <= nt_dn, ks_dn, cl_dn, s, peers);
+    st = grouped(wd, nullptr, E, gdn, d, nt_dn, mtp_dn ? 2 : 1, w.inter, f, Tk, nullptr, w.offsets, prefix_dn, max_dn,
+                 kEpiScatter, out, peers ? peers->ldo : d, 0, w.sel, w.gw, f, tpg <= nt_dn, ks_dn, cl_dn, s, peers,
+                 nullptr, 0, nullptr, mtp_dn);
   }
   if (st != SMY_OK) return st;
   record_phase(4, s);
@@ -453,7 +473,8 @@ smy_status moe_kernel_names(const smy_moe_config* c, int64_t T, char* gu, char* 
   const int nt_gu = ssmm_pick_nt(nw_gu, ggu.ms, ggu.rep, tpg_hi);
   const int nt_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, tpg_hi);
   const int cl_gu = fused ? ssmm_pair_cluster(nt_gu, nw_gu, ggu.ms, ggu.rep, ggu.m_tiles, tpg, 1) : 0;
-  const int cl_dn = ssmm_pair_cluster(nt_dn, 1, gdn.ms, gdn.rep, gdn.m_tiles, tpg, 0);
+  const int mtp_dn = down_mtp_half(gdn, tpg, tpg_hi);
+  const int cl_dn = mtp_dn ? 2 : ssmm_pair_cluster(nt_dn, 1, gdn.ms, gdn.rep, gdn.m_tiles, tpg, 0);
   // the SEL-gather pair launch of the widest (1,2,V) tile runs split rings (ssmm.cu)
   const int split_gu =
       cl_gu && ((ggu.ms == 2 && nw_gu == 1 && (nt_gu == SMY_NT_WIDE || nt_gu == 128) && !(debug_flags() & 16384)) ||
@@ -462,7 +483,9 @@ smy_status moe_kernel_names(const smy_moe_config* c, int64_t T, char* gu, char* 
     snprintf(gu, len, "ssmm_pair_kernel<%d, %d, %d, %d>", nt_gu, nw_gu, ggu.ms, split_gu);
   else
     snprintf(gu, len, "ssmm_kernel<%d, %d, %d, %d>", nt_gu, nw_gu, ggu.ms, ggu.rep);
-  if (cl_dn)
+  if (mtp_dn)
+    snprintf(dn, len, "ssmm_pair_kernel<224, 2, 1, 1>");
+  else if (cl_dn)
     snprintf(dn, len, "ssmm_pair_kernel<%d, %d, %d, %d>", nt_dn, 1, gdn.ms, 0);
   else
     snprintf(dn, len, "ssmm_kernel<%d, %d, %d, %d>", nt_dn, 1, gdn.ms, gdn.rep);

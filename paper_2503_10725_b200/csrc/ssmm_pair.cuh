@@ -621,6 +621,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
           const float my_s = (lane & 15) < jmax ? (a.scale ? a.scale[rl] : 1.f) : 0.f;
           if constexpr (MS == 2) {
             scatter_chunk_v4(v[0][0], v[0][1], my_row, my_s, n, grp, lane);
+          } else if (NW == 2) {  // m-tile pairing: weight w = output rows offset by w * mtp_half * 128
+            const int off1 = a.mtp_half * kTileM;
+            const int n1 = (valid && cr + off1 < a.R && !(a.debug & 8)) ? jmax : 0;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              float* o = reinterpret_cast<float*>(
+                  __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), j));
+              const float sc = __shfl_sync(0xffffffffu, my_s, j);
+              if (j < n) atomicAdd(o + cr, sc * v[0][0][j]);
+              if (j < n1) atomicAdd(o + cr + off1, sc * v[NW - 1][0][j]);
+            }
           } else {  // N == M: lane = output row
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
@@ -628,6 +639,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
                   __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), j));
               const float sc = __shfl_sync(0xffffffffu, my_s, j);
               if (j < n) atomicAdd(o + cr, sc * v[0][0][j]);
+            }
+          }
+          continue;
+        }
+        if (MS == 1 && NW == 2 && a.mtp_half) {  // m-tile pairing, compact fp32 / bf16
+          const int64_t r0 = ti.row0 + ti.t0 + c0;
+          const int off1 = a.mtp_half * kTileM;
+          const int n1 = (valid && cr + off1 < a.R && !(a.debug & 8)) ? jmax : 0;
+#pragma unroll
+          for (int w = 0; w < NW; ++w) {
+            const int col = cr + w * off1, nw_ = w ? n1 : n;
+            if (a.out_bf16) {
+              uint16_t* o = static_cast<uint16_t*>(a.out) + r0 * a.ldo + col;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                if (j < nw_) *o = __bfloat16_as_ushort(__float2bfloat16_rn(v[w][0][j]));
+                o += a.ldo;
+              }
+            } else {
+              float* o = static_cast<float*>(a.out) + r0 * a.ldo + col;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                if (j < nw_) *o = v[w][0][j];
+                o += a.ldo;
+              }
             }
           }
           continue;
