@@ -85,6 +85,16 @@ smy_status silu_mul_launch(const float* g, const float* u, int64_t rows, int64_t
 
 static bool gate_up_fused(const Geometry& g) { return !(g.ms >= 16); }
 
+// m-tile pairing of the interleaved (1,2,V) gate/up on the CTA pair (0 = off): two
+// m-tiles per SEL-gathered token stage at NT = 112 -- four lane-masked MMAs per window
+// instead of two at NT = 224, half the token bytes per MMA (Qwen2 gate/up 0.635 ->
+// 0.598 ms, Mixtral neutral, DeepSeek -2 %; SMY_DEBUG=1048576 turns it off)
+static int gu_mtp_half(bool ilv, int cl_gu, const Geometry& ggu, int nt_gu) {
+  if (!ilv || cl_gu != 2 || ggu.ms != 2 || nt_gu != SMY_NT_WIDE || ggu.m_tiles < 3 || (debug_flags() & 1048576))
+    return 0;
+  return (ggu.m_tiles + 1) / 2;
+}
+
 // m-tile pairing of an N = M down launch (0 = off): wide token tiles on the CTA pair
 static int down_mtp_half(const Geometry& gdn, int64_t tpg, int64_t tpg_hi) {
   if (gdn.ms != 1 || gdn.rep != 1 || gdn.m_tiles < 3 || (debug_flags() & 131072)) return 0;
@@ -272,7 +282,7 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   // decode-sized expert rarely needs a second n-tile (which would re-stream its weights
   // through the SMs); ragged tiles issue MMAs of their own width
   const int64_t tpg_hi = tpg + (int64_t)(3.0 * sqrt((double)tpg) + 0.999);
-  const int nt_gu = ssmm_pick_nt(nw_gu, ggu.ms, ggu.rep, tpg_hi);
+  int nt_gu = ssmm_pick_nt(nw_gu, ggu.ms, ggu.rep, tpg_hi);
   int nt_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, tpg_hi);
   const int64_t act = E < T * k ? E : T * k;
   const Variant var = t_variant;
@@ -294,6 +304,8 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   const bool pair_gu_ok = ssmm_pair_images_ok(wg, nw_gu == 2 ? wu : nullptr, E, img_gu);
   const bool pair_dn_ok = ssmm_pair_images_ok(wd, nullptr, E, img_dn);
   const int cl_gu = fused && pair_gu_ok ? ssmm_pair_cluster(nt_gu, nw_gu, ggu.ms, ggu.rep, ggu.m_tiles, tpg, 1) : 0;
+  const int mtp_gu = var.v == 0 ? gu_mtp_half(ilv, cl_gu, ggu, nt_gu) : 0;
+  if (mtp_gu) nt_gu = 112;
   // N = M down weights with wide tiles: m-tile pairing on the CTA pair (the weight's
   // second half of m-tiles as the launch's second weight, samoyeds_ssmm): every token
   // stage of the intermediate feeds two accumulators
@@ -308,7 +320,8 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
                         ? 1
                         : ssmm_pick_ksplit((int64_t)mtiles_dn * act * ((tpg + nt_dn - 1) / (nt_dn > 0 ? nt_dn : 1)),
                                            gdn.k_stages);
-  const int mt_gu = cl_gu ? (ggu.m_tiles + 1) / 2 : ggu.m_tiles;
+  const int mtiles_gu = mtp_gu ? mtp_gu : ggu.m_tiles;
+  const int mt_gu = cl_gu ? (mtiles_gu + 1) / 2 : mtiles_gu;
   const int mt_dn = cl_dn ? (mtiles_dn + 1) / 2 : mtiles_dn;
   // the routing scan counts tiles per expert in units of the launch's token span
   const int nts[2] = {nt_gu, nt_dn};
@@ -362,9 +375,9 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
                  inter_dense, f, 1, nullptr, nullptr, d, tpg <= nt_gu, 1, cl_gu, s, nullptr, zero_out, T * d,
                  rows_dense);
   } else if (ilv) {
-    st = grouped(wg, nullptr, E, ggu, f, nt_gu, 1, xb, peers ? peers->ldx : d, T, w.sel, w.offsets, prefix_gu,
-                 max_gu, kEpiSiluMulIlv, w.inter, f, 1, nullptr, nullptr, d, tpg <= nt_gu, 1, cl_gu, s, peers,
-                 zero_out, T * d);
+    st = grouped(wg, nullptr, E, ggu, f, nt_gu, mtp_gu ? 2 : 1, xb, peers ? peers->ldx : d, T, w.sel, w.offsets,
+                 prefix_gu, max_gu, kEpiSiluMulIlv, w.inter, f, 1, nullptr, nullptr, d, tpg <= nt_gu, 1, cl_gu, s,
+                 peers, zero_out, T * d, nullptr, mtp_gu);
   } else if (fused) {
     st = grouped(wg, wu, E, ggu, f, nt_gu, 2, xb, peers ? peers->ldx : d, T, w.sel, w.offsets, prefix_gu, max_gu,
                  kEpiSiluMul, w.inter, f, 1, nullptr, nullptr, d, tpg <= nt_gu, 1, cl_gu, s, peers, zero_out, T * d);
@@ -479,7 +492,10 @@ smy_status moe_kernel_names(const smy_moe_config* c, int64_t T, char* gu, char* 
   const int split_gu =
       cl_gu && ((ggu.ms == 2 && nw_gu == 1 && (nt_gu == SMY_NT_WIDE || nt_gu == 128) && !(debug_flags() & 16384)) ||
                 (ggu.ms == 1 && nw_gu == 2 && nt_gu == 224));
-  if (cl_gu)
+  const int mtp_gu = gu_mtp_half(ilv, cl_gu, ggu, nt_gu);
+  if (mtp_gu)
+    snprintf(gu, len, "ssmm_pair_kernel<112, 2, 2, 1>");
+  else if (cl_gu)
     snprintf(gu, len, "ssmm_pair_kernel<%d, %d, %d, %d>", nt_gu, nw_gu, ggu.ms, split_gu);
   else
     snprintf(gu, len, "ssmm_kernel<%d, %d, %d, %d>", nt_gu, nw_gu, ggu.ms, ggu.rep);

@@ -37,6 +37,7 @@ extern template smy_status launch_pair_t<SMY_NT_WIDE, 1, 2, 0>(const SsmmArgs&, 
 extern template smy_status launch_pair_t<SMY_NT_WIDE, 1, 2, 1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<128, 1, 2, 1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<224, 2, 1, 1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<112, 2, 2, 1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<128, 1, 1, 0>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<256, 1, 1, 0>(const SsmmArgs&, cudaStream_t);
 
@@ -156,7 +157,8 @@ smy_status ssmm_launch_pair(const SsmmArgs& a0, int nt, int nw, int ms, int cl, 
   smy_status st = make_w_tmap(&a.tmap_w, a.wbase, (int64_t)((hi - lo) / 128), (kABytes + kEBytes + 64 + 127) / 128);
   if (st != SMY_OK) return st;
   if (ms == 2 && nw == 2 && nt == 64) return launch_pair_t<64, 2, 2, 0>(a, s);
-  if (ms == 2 && nw == 2 && nt == 112) return launch_pair_t<112, 2, 2, 0>(a, s);
+  if (ms == 2 && nw == 2 && nt == 112)
+    return a.mtp_half && a.sel_in ? launch_pair_t<112, 2, 2, 1>(a, s) : launch_pair_t<112, 2, 2, 0>(a, s);
   if (ms == 2 && nw == 1 && nt == 128) return a.sel_in && !(a.debug & 16384) ? launch_pair_t<128, 1, 2, 1>(a, s)
                                                                            : launch_pair_t<128, 1, 2, 0>(a, s);
   // SEL-gathered token rows (gate/up): separate, deeper token ring

@@ -181,8 +181,10 @@ constexpr int kPairThreads = 32 * (11 + kPairEpiWarps - 4);  // + producer, 2 MM
 #ifndef SMY_PAIR_GATHER_WARPS
 #define SMY_PAIR_GATHER_WARPS 8
 #endif
-constexpr int pair_threads(int split) { return kPairThreads + (split ? 32 * (SMY_PAIR_GATHER_WARPS - 4) : 0); }
-constexpr int pair_gather_threads(int split) { return split ? 32 * SMY_PAIR_GATHER_WARPS : kGatherThreads; }
+// (8 gather warps cover 16 token rows per pass: halves of a multiple of 16 rows only)
+constexpr int pair_gather_warps(int split, int nt) { return split && (nt / 2) % 16 == 0 ? SMY_PAIR_GATHER_WARPS : 4; }
+constexpr int pair_threads(int split, int nt) { return kPairThreads + 32 * (pair_gather_warps(split, nt) - 4); }
+constexpr int pair_gather_threads(int split, int nt) { return 32 * pair_gather_warps(split, nt); }
 
 // MS = accumulator slots per weight: 2 for (1,2,V) (the lane-masked remap), 1 for
 // N == M (plain 2:4, no remap -- the weight-only-sparse baseline formats)
@@ -224,7 +226,7 @@ struct PairCfg {
 };
 
 template <int NT, int NW, int MS, int SPLIT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT), 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, NT), 1)
     ssmm_pair_kernel(const __grid_constant__ SsmmArgs a) {
   using C = PairCfg<NT, NW, MS, SPLIT>;
   constexpr int SW = C::kWStages, SB = C::kBStages;
@@ -269,7 +271,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
       for (int s = 0; s < SB; ++s) {
         // gather: own gather threads (+ the peer's relay on the leader); contiguous
         // rows: the leader's expect_tx (both CTAs' TMA bytes)
-        mbar_init(&bfull[s], gather ? pair_gather_threads(SPLIT) + (leader ? 1 : 0) : 1);
+        mbar_init(&bfull[s], gather ? pair_gather_threads(SPLIT, NT) + (leader ? 1 : 0) : 1);
         mbar_init(&bempty[s], kIssuers);
       }
     } else {
@@ -481,7 +483,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
     // source pointers and swizzled destination offsets are computed once per tile;
     // a stage is then H/RS (address add + cp.async) per thread.
     if (gather) {
-      constexpr int GT = pair_gather_threads(SPLIT), RS = GT / 16;
+      constexpr int GT = pair_gather_threads(SPLIT, NT), RS = GT / 16;
       const int tb = warp < 10 ? threadIdx.x - 6 * 32 : threadIdx.x - 15 * 32 + kGatherThreads;
       static_assert(GT % 128 == 0 && H % RS == 0, "gather mapping");
       const uint64_t pol_g = SMY_GATHER_EVICT_LAST ? policy_evict_last() : 0;
@@ -561,7 +563,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
     for (int b = 0; b < AB; ++b) release(b);
     uint32_t tcount = 0;
     TileInfo ti;
-    const bool ilv = NW == 1 && a.epi == kEpiSiluMulIlv;
+    const bool ilv = (NW == 1 || a.mtp_half) && a.epi == kEpiSiluMulIlv;
     for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep, ++tcount) {
       const int m_own = 2 * ti.m_tile + (int)cta;
       const int cr = m_own * kTileM + 32 * q + lane;
@@ -579,7 +581,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT),
         const bool gvalid = m_own < a.m_tiles && cg < a.R / 2 && !(a.debug & 8);
         for (int c0 = 16 * h; c0 < ti.n_local; c0 += 32) {
           const unsigned long long tl0 = prof ? clk() : 0;
-          if constexpr (MS == 2) {
+          if constexpr (MS == 2 && NW == 2) {  // m-tile pairing: weight 1 = m-tiles [half, 2 half)
+            float v[2][2][16];
+#pragma unroll
+            for (int w = 0; w < 2; ++w) {
+              tmem_ld16(tacc + lane_base + (2 * w) * NT + c0, v[w][0]);
+              tmem_ld16(tacc + lane_base + (2 * w + 1) * NT + c0, v[w][1]);
+            }
+            tmem_ld_wait();
+            if (c0 + 32 >= ti.n_local) release(ab);
+            if (prof) pc[8] += clk() - tl0;
+            const int cg1 = cg + a.mtp_half * 64;  // a 128-lane m-tile holds 64 outputs
+            if (!(a.debug & 32)) {
+              ilv_chunk(v[0], gvalid, min(16, ti.n_local - c0), static_cast<uint16_t*>(a.out), a.ldo,
+                        ti.row0 + ti.t0 + c0, cg, lane, a.rows_out);
+              ilv_chunk(v[1], gvalid && cg1 < a.R / 2, min(16, ti.n_local - c0), static_cast<uint16_t*>(a.out),
+                        a.ldo, ti.row0 + ti.t0 + c0, cg1, lane, a.rows_out);
+            }
+          } else if constexpr (MS == 2) {
             float v[2][16];
             tmem_ld16(tacc + lane_base + c0, v[0]);
             tmem_ld16(tacc + lane_base + NT + c0, v[1]);
@@ -786,7 +805,7 @@ smy_status launch_pair_t(const SsmmArgs& a, cudaStream_t s) {
   // n-fastest order would re-stream the gathered rows from HBM for every m-tile)
   b.m_fastest = (a.epi == kEpiScatter || (a.sel_in != nullptr && (int64_t)a.x_rows * a.ldx * 2 > kGatherL2Bytes)) &&
                 !(a.debug & 2048);
-  kern<<<2 * pairs, pair_threads(SPLIT), C::kSmemBytes, s>>>(b);
+  kern<<<2 * pairs, pair_threads(SPLIT, NT), C::kSmemBytes, s>>>(b);
   count_launch();
   return cuda_status(cudaGetLastError());
 }

@@ -1,5 +1,4 @@
 mkdir -p gpurun_out/r2
-timeout 1200 python -m pytest tests/test_gpu_parity.py -x -q -k "moe_layer or ssmm" > gpurun_out/r2/par_mtp2.txt 2>&1
-for fmt in 4,8,32 2,2,32; do
-  timeout 600 python bench.py --format $fmt --no-cpu-baseline --steps 60 --warmup 5 > gpurun_out/r2/b3_${fmt}.json 2> gpurun_out/r2/b3_${fmt}.err
-done
+timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/r2/pytest_gpu_full.txt 2>&1; echo "exit $?" >> gpurun_out/r2/pytest_gpu_full.txt
+timeout 600 python bench.py > gpurun_out/r2/bench_final1.json 2> gpurun_out/r2/bench_final1.err
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2/smoke.txt 2>&1; echo "exit $?" >> gpurun_out/r2/smoke.txt
