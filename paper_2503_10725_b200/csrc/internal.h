@@ -22,9 +22,11 @@ constexpr int kMaxPeers = 8;      // ranks of one NVLink/NVSwitch node (expert p
 #ifndef SMY_NT_WIDE
 #define SMY_NT_WIDE 224
 #endif
-// token-ring depth of the SEL-gather pair launches (SPLIT rings)
+// token-ring depth of the SEL-gather pair launches (SPLIT rings; capped by what fits
+// beside 3 weight slots: 7 at NT = 112 (the m-tile-paired gate/up), 5 at NT = 224;
+// 5 -> 7 at NT = 112: token-ring waits 495 k -> 391 k cycles, gate/up -2 to -3 %)
 #ifndef SMY_TOKEN_SLOTS
-#define SMY_TOKEN_SLOTS 5
+#define SMY_TOKEN_SLOTS 7
 #endif
 
 struct Geometry {
