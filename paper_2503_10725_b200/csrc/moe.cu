@@ -97,10 +97,18 @@ static int gu_mtp_half(bool ilv, int cl_gu, const Geometry& ggu, int nt_gu) {
 
 // m-tile pairing of an N = M down launch (0 = off): wide token tiles on the CTA pair
 static int down_mtp_half(const Geometry& gdn, int64_t tpg, int64_t tpg_hi) {
-  if (gdn.ms != 1 || gdn.rep != 1 || gdn.m_tiles < 3 || (debug_flags() & 131072)) return 0;
+  if (gdn.rep != 1 || gdn.m_tiles < 3 || (debug_flags() & 131072)) return 0;
   const int half = (gdn.m_tiles + 1) / 2;
-  return ssmm_pick_nt(2, 1, 1, tpg_hi) == 224 && ssmm_pair_cluster(224, 2, 1, 1, half, tpg, 0) == 2 ? half : 0;
+  if (gdn.ms == 1)
+    return ssmm_pick_nt(2, 1, 1, tpg_hi) == 224 && ssmm_pair_cluster(224, 2, 1, 1, half, tpg, 0) == 2 ? half : 0;
+  // (1,2,V) down with NT = 112, two m-tiles per token stage: measured slower (Mixtral down
+  // 0.337 -> 0.378 ms, Qwen2 0.350 -> 0.374; DeepSeek -1.7 %) -- opt-in, SMY_DEBUG=2097152
+  if (gdn.ms == 2 && (debug_flags() & 2097152))
+    return ssmm_pick_nt(1, 2, 1, tpg_hi) == SMY_NT_WIDE && ssmm_pair_cluster(112, 2, 2, 1, half, tpg, 0) == 2 ? half
+                                                                                                              : 0;
+  return 0;
 }
+static int down_mtp_nt(const Geometry& gdn) { return gdn.ms == 1 ? 224 : 112; }
 
 static bool interleaved(const smy_moe_config* c) { return c->gate_up == SMY_GU_INTERLEAVED; }
 
@@ -309,8 +317,8 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   // N = M down weights with wide tiles: m-tile pairing on the CTA pair (the weight's
   // second half of m-tiles as the launch's second weight, samoyeds_ssmm): every token
   // stage of the intermediate feeds two accumulators
-  const int mtp_dn = pair_dn_ok && var.v != SMY_VARIANT_PERMUTE ? down_mtp_half(gdn, tpg, tpg_hi) : 0;
-  if (mtp_dn) nt_dn = 224;
+  const int mtp_dn = pair_dn_ok && var.v == 0 ? down_mtp_half(gdn, tpg, tpg_hi) : 0;
+  if (mtp_dn) nt_dn = down_mtp_nt(gdn);
   const int mtiles_dn = mtp_dn ? mtp_dn : gdn.m_tiles;  // m-tiles per weight of the launch
   const int cl_dn =
       mtp_dn ? 2 : pair_dn_ok ? ssmm_pair_cluster(nt_dn, 1, gdn.ms, gdn.rep, gdn.m_tiles, tpg, 0) : 0;
@@ -499,8 +507,10 @@ smy_status moe_kernel_names(const smy_moe_config* c, int64_t T, char* gu, char* 
     snprintf(gu, len, "ssmm_pair_kernel<%d, %d, %d, %d>", nt_gu, nw_gu, ggu.ms, split_gu);
   else
     snprintf(gu, len, "ssmm_kernel<%d, %d, %d, %d>", nt_gu, nw_gu, ggu.ms, ggu.rep);
-  if (mtp_dn)
+  if (mtp_dn && gdn.ms == 1)
     snprintf(dn, len, "ssmm_pair_kernel<224, 2, 1, 1>");
+  else if (mtp_dn)
+    snprintf(dn, len, "ssmm_pair_kernel<112, 2, 2, 0>");
   else if (cl_dn)
     snprintf(dn, len, "ssmm_pair_kernel<%d, %d, %d, %d>", nt_dn, 1, gdn.ms, 0);
   else

@@ -19,6 +19,9 @@
 // `acc_full`; both epilogues arrive on the leader's `acc_empty`.
 #include "ssmm_kernel.cuh"
 
+#ifndef SMY_PAIR_MIN_WSLOTS
+#define SMY_PAIR_MIN_WSLOTS 3  // weight slots kept beside the token ring of a SPLIT launch
+#endif
 #ifndef SMY_GATHER_SPIN
 #define SMY_GATHER_SPIN 0
 #endif
@@ -215,7 +218,7 @@ struct PairCfg {
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;          // lock-step ring depth
   // split rings: 5 token slots (measured: their depth matters more than the weights'),
   // the rest of shared memory to weight slots
-  static constexpr int kBFit = (kSmemCap - 3 * kWStage) / kBStage;
+  static constexpr int kBFit = (kSmemCap - SMY_PAIR_MIN_WSLOTS * kWStage) / kBStage;
   static constexpr int kBStages = SPLIT ? (SMY_TOKEN_SLOTS < kBFit ? SMY_TOKEN_SLOTS : kBFit) : kStages;
   static constexpr int kWStagesRaw = SPLIT ? (kSmemCap - kBStages * kBStage) / kWStage : kStages;
   static constexpr int kWStages = kWStagesRaw > 8 ? 8 : kWStagesRaw;
@@ -640,6 +643,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
           const float my_s = (lane & 15) < jmax ? (a.scale ? a.scale[rl] : 1.f) : 0.f;
           if constexpr (MS == 2) {
             scatter_chunk_v4(v[0][0], v[0][1], my_row, my_s, n, grp, lane);
+            if (NW == 2 && a.mtp_half) {  // m-tile pairing: weight 1 = compressed rows + mtp_half * 128
+              const int g1 = grp + a.mtp_half * kTileM;
+              scatter_chunk_v4(v[NW - 1][0], v[NW - 1][1], my_row, my_s,
+                               (valid && g1 < a.R && !(a.debug & 8)) ? jmax : 0, g1, lane);
+            }
           } else if (NW == 2) {  // m-tile pairing: weight w = output rows offset by w * mtp_half * 128
             const int off1 = a.mtp_half * kTileM;
             const int n1 = (valid && cr + off1 < a.R && !(a.debug & 8)) ? jmax : 0;
