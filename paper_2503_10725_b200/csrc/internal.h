@@ -72,6 +72,11 @@ struct SsmmArgs {
   // token stage feeds two accumulators; output rows of weight w are offset by
   // w * mtp_half * 128; m_tiles = mtp_half; 0 = off
   int mtp_half;
+  // programmatic dependent launch: the launch may start while the previous kernel of
+  // the stream (the gate/up SSMM) still runs; its producer streams the first ring of
+  // WEIGHT stages, then waits (griddepcontrol.wait) before the dependent token loads,
+  // and the epilogue waits before its first output write (contiguous-B launches only)
+  int pdl;
   const float* scale;      // scatter scale, NULL = 1
   int max_tiles;           // tile count (single group) / upper bound (grouped)
   int weights_stream;      // 1: weights read once per call (decode) -> L2 evict_first

@@ -140,10 +140,12 @@ static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* 
                           int epi, void* out, int64_t ldo, int out_bf16, const int32_t* sel_out,
                           const float* scale, int64_t k_cols, int stream_w, int k_splits, int cl,
                           cudaStream_t s, const PeerRows* peers = nullptr, float* zero_ptr = nullptr,
-                          int64_t zero_elems = 0, const int32_t* rows_out = nullptr, int mtp_half = 0) {
+                          int64_t zero_elems = 0, const int32_t* rows_out = nullptr, int mtp_half = 0,
+                          int pdl = 0) {
   SsmmArgs a;
   memset(&a, 0, sizeof(a));
   a.rows_out = rows_out;
+  a.pdl = pdl;
   a.zero_ptr = zero_ptr;
   a.zero_elems = zero_elems;
   if (peers != nullptr) {
@@ -415,7 +417,7 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   } else {
     st = grouped(wd, nullptr, E, gdn, d, nt_dn, mtp_dn ? 2 : 1, w.inter, f, Tk, nullptr, w.offsets, prefix_dn, max_dn,
                  kEpiScatter, out, peers ? peers->ldo : d, 0, w.sel, w.gw, f, tpg <= nt_dn, ks_dn, cl_dn, s, peers,
-                 nullptr, 0, nullptr, mtp_dn);
+                 nullptr, 0, nullptr, mtp_dn, peers == nullptr && !(debug_flags() & 4194304));
   }
   if (st != SMY_OK) return st;
   record_phase(4, s);

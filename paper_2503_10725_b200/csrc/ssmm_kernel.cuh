@@ -286,6 +286,9 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
   constexpr int kIssuers = (NW == 2 || MS >= 2) ? 2 : 1;  // MMA-issuing warps
   using C = Cfg<NT, NW, MS, REP>;
   constexpr int S = C::kStages;
+  // a dependent launch (the down SSMM after gate/up, SsmmArgs::pdl) may start its
+  // prologue and weight stream on SMs this grid has left
+  if (threadIdx.x == 0) griddep_launch_dependents();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* aux = smem + S * C::kStageBytes;
@@ -333,12 +336,27 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
       const uint64_t pol_x = policy_evict_last();
       uint32_t it = 0;
       TileInfo ti;
+      // programmatic dependent launch: the first ring of stages gets its weights at once,
+      // their token loads (the previous kernel's output) wait for griddepcontrol.wait
+      const bool defer = a.pdl && !gather;
+      int npend = 0, pend_k[S], pend_row[S];
+      auto load_b = [&](int st, int k, int xrow) {
+#pragma unroll
+        for (int atom = 0; atom < 2 / REP; ++atom)
+          tma_tile2d(bsm(st) + atom * (NT * 128), &a.tmap_x, k * (128 / REP) + atom * 64, xrow, &full[st], pol_x);
+      };
+      auto flush = [&]() {
+        griddep_wait();
+        for (int i = 0; i < npend; ++i) load_b(i, pend_k[i], pend_row[i]);
+        npend = -1;
+      };
       for (int tile = tile0; decode_tile(a, NT, tile, ti); tile += tstep) {
         const uint8_t* src0 = a.img0[ti.g] + (size_t)ti.m_tile * ks * a.block;
         const uint8_t* src1 = NW == 2 ? a.img1[ti.g] + (size_t)ti.m_tile * ks * a.block : nullptr;
         const int xrow = ti.row0 + ti.t0;
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % S;
+          if (defer && npend >= 0 && it >= (uint32_t)S) flush();  // the ring is full: tokens next
           const unsigned long long t0 = prof ? clk() : 0;
           mbar_wait(&empty[st], ((it / S) & 1) ^ 1);
           if (prof) pc[5] += clk() - t0;
@@ -349,12 +367,17 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
             if (NW == 2) bulk_g2s(wsm(st, 1), src1 + (size_t)k * a.block, wbytes, &full[st], pol_w);
           }
           if (!gather) {
-#pragma unroll
-            for (int atom = 0; atom < 2 / REP; ++atom)
-              tma_tile2d(bsm(st) + atom * (NT * 128), &a.tmap_x, k * (128 / REP) + atom * 64, xrow, &full[st], pol_x);
+            if (defer && npend >= 0) {
+              pend_k[npend] = k;
+              pend_row[npend] = xrow;
+              ++npend;
+            } else {
+              load_b(st, k, xrow);
+            }
           }
         }
       }
+      if (defer && npend >= 0) flush();
     }
   } else if (warp == 5 || warp == 10) {
     // ============ MMA issuers (warps 5 and 10; whole warp, one elected lane) ============
@@ -515,6 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
     }
   } else {
     // ============ epilogue (warps 0-3): TMEM -> fused epilogue -> re-zero ============
+    if (a.pdl) griddep_wait();  // outputs (zeroed by the previous kernel) are written below
     if (a.zero_ptr != nullptr) zero_slice(a, (int64_t)blockIdx.x * 128 + threadIdx.x, (int64_t)gridDim.x * 128);
     const int q = warp;  // TMEM lane quarter
     const uint32_t lane_base = (uint32_t)(32 * q) << 16;
@@ -702,6 +726,21 @@ smy_status launch_t(const SsmmArgs& a, cudaStream_t s) {
   // n-fastest order would re-stream the gathered rows from HBM for every m-tile)
   b.m_fastest = (a.epi == kEpiScatter || (a.sel_in != nullptr && (int64_t)a.x_rows * a.ldx * 2 > kGatherL2Bytes)) &&
                 !(a.debug & 2048);
+  if (b.pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, b);
+    count_launch();
+    return cuda_status(e);
+  }
   kern<<<grid, kThreads, C::kSmemBytes, s>>>(b);
   count_launch();
   return cuda_status(cudaGetLastError());

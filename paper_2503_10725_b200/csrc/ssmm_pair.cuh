@@ -233,6 +233,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
     ssmm_pair_kernel(const __grid_constant__ SsmmArgs a) {
   using C = PairCfg<NT, NW, MS, SPLIT>;
   constexpr int SW = C::kWStages, SB = C::kBStages;
+  if (threadIdx.x == 0) griddep_launch_dependents();  // see ssmm_kernel
   constexpr int kIssuers = (NW == 2 || MS == 2) ? 2 : 1;  // MMA-issuing warps
   constexpr int H = C::kHalf;
   extern __shared__ uint8_t smem_raw[];
@@ -323,6 +324,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
       const int brows = a.block >> 7;
       uint32_t it = 0;
       TileInfo ti;
+      // programmatic dependent launch (SsmmArgs::pdl): the lock-step ring's first SW
+      // stages get their weights at once, their token halves after griddepcontrol.wait
+      const bool defer = a.pdl && !gather && !SPLIT;
+      if (a.pdl && !gather && SPLIT) griddep_wait();
+      int npend = 0, pend_k[SW], pend_row[SW];
+      auto load_b = [&](int sb, int k, int xrow) {
+#pragma unroll
+        for (int atom = 0; atom < 2; ++atom)
+          tma2d_pair(bsm(sb) + atom * (H * 128), &a.tmap_x, k * 128 + atom * 64, xrow, bfull_lead + sb * 8, pol_x);
+      };
+      auto flush = [&]() {
+        griddep_wait();
+        for (int i = 0; i < npend; ++i) load_b(i, pend_k[i], pend_row[i]);
+        npend = -1;
+      };
       for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep) {
         // an odd m-tile count leaves the last pair's peer without a tile: it loads the
         // last real tile again (valid memory) and its epilogue stores nothing
@@ -335,6 +351,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
         const int xrow = ti.row0 + ti.t0 + (int)cta * hh;
         for (int k = ti.k0; k < ti.k1; ++k, ++it) {
           const int st = it % SW;
+          if (defer && npend >= 0 && it >= (uint32_t)SW) flush();
           const unsigned long long t0 = prof ? clk() : 0;
           mbar_wait_cta(&wempty[st], ((it / SW) & 1) ^ 1);
           if (prof) pc[5] += clk() - t0;
@@ -352,12 +369,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
               mbar_wait_cta(&bempty[sb], ((it / SB) & 1) ^ 1);
               if (leader) mbar_arrive_expect_tx(&bfull[sb], b_pair_bytes);
             }
-#pragma unroll
-            for (int atom = 0; atom < 2; ++atom)
-              tma2d_pair(bsm(sb) + atom * (H * 128), &a.tmap_x, k * 128 + atom * 64, xrow, bfull_lead + sb * 8, pol_x);
+            if (defer && npend >= 0) {  // lock-step: sb == st == it for the first SW stages
+              pend_k[npend] = k;
+              pend_row[npend] = xrow;
+              ++npend;
+            } else {
+              load_b(sb, k, xrow);
+            }
           }
         }
       }
+      if (defer && npend >= 0) flush();
     }
   } else if (warp == 5 || warp == 14) {
     if (leader && (warp == 5 || kIssuers == 2)) {
@@ -552,6 +574,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
     // epilogue's dependent-latency chains.
     const int q = warp & 3;
     const int h = warp >= 10 ? 1 : 0;
+    if (a.pdl) griddep_wait();  // outputs (zeroed by the previous kernel) are written below
     if (a.zero_ptr != nullptr)
       zero_slice(a, (int64_t)blockIdx.x * 256 + (q + 4 * h) * 32 + lane, (int64_t)gridDim.x * 256);
     const uint32_t lane_base = (uint32_t)(32 * q) << 16;
@@ -813,6 +836,21 @@ smy_status launch_pair_t(const SsmmArgs& a, cudaStream_t s) {
   // n-fastest order would re-stream the gathered rows from HBM for every m-tile)
   b.m_fastest = (a.epi == kEpiScatter || (a.sel_in != nullptr && (int64_t)a.x_rows * a.ldx * 2 > kGatherL2Bytes)) &&
                 !(a.debug & 2048);
+  if (b.pdl) {  // programmatic dependent launch (SsmmArgs::pdl); cluster dims are compiled in
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(pair_threads(SPLIT, NT));
+    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, b);
+    count_launch();
+    return cuda_status(e);
+  }
   kern<<<2 * pairs, pair_threads(SPLIT, NT), C::kSmemBytes, s>>>(b);
   count_launch();
   return cuda_status(cudaGetLastError());
