@@ -5,7 +5,7 @@
 # Results under gpurun_out/cap2; probes/ncu_summary.py condenses the CSVs into
 # profiles/r2_ncu_summary.json (bench.py's roofline.traffic lookup).
 set -x
-O=gpurun_out/cap2
+O=${CAP_OUT:-gpurun_out/cap3}
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $O/smi.txt
 timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err
@@ -32,6 +32,14 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
     -k regex:ssmm -s 6 -c 2 -o $O/traffic_deepseek_4096_sh2 \
     python bench.py --model deepseek --shared 2 --steps 1 --warmup 3 --decode-tokens 0 --no-cpu-baseline --no-graph > /dev/null 2>&1
 ncu -i $O/traffic_deepseek_4096_sh2.ncu-rep --page raw --csv > $O/traffic_deepseek_4096_sh2.csv 2>/dev/null
+# ablation, N>1 formats, config-5 sweep, per-role counters
+timeout 900 python probes/ablation.py > $O/ablation.md 2> $O/ablation.err
+for fmt in 4,8,32 1,2,16 8,16,32 2,2,32; do
+  timeout 600 python bench.py --format $fmt --no-cpu-baseline --steps 60 --warmup 5 > $O/fmt_${fmt}.json 2>/dev/null
+done
+timeout 1500 python probes/sweep.py > $O/sweep.json 2> $O/sweep.err
+for m in mixtral qwen2 deepseek; do SMY_DEBUG=128 timeout 300 python probes/prof_run.py $m 4096 > $O/prof_$m.txt 2>&1; done
+timeout 600 python bench.py --model qwen2 --shared 8 --shared-gate sigmoid --decode-tokens 0 --no-cpu-baseline > $O/table_qwen2_4096_sh8sig.json 2>/dev/null
 # launch list of the default command (kernel shares of the step)
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline --decode-tokens 0 > /dev/null 2>&1

@@ -135,3 +135,28 @@ def test_moe_layer_rejects_unknown_gating_and_misaligned_out(lib):
     # samoyeds_moe_experts has no shared experts
     cfg.num_shared = 1
     assert lib.samoyeds_moe_experts(C.byref(cfg), ws, p, 16, p, p, p, p, 16, None) == 3
+
+
+@pytest.mark.parametrize("model,fmt,T,gu_expect,dn_expect", [
+    # prefill: gate/up m-tile-paired on the CTA pair (NT=112), down on the pair at NT=224
+    ("mixtral", (1, 2, 32), 4096, "ssmm_pair_kernel<112, 2, 2, 1>", "ssmm_pair_kernel<224, 1, 2, 0>"),
+    ("deepseek", (1, 2, 32), 4096, "ssmm_pair_kernel<112, 2, 2, 1>", "ssmm_pair_kernel<224, 1, 2, 0>"),
+    # mid range: <= 128-token gate/up tiles stay single-CTA, the down goes to the pair
+    ("mixtral", (1, 2, 32), 256, "ssmm_kernel<128, 1, 2, 1>", "ssmm_pair_kernel<128, 1, 2, 0>"),
+    # decode: single-CTA kernels with narrow token tiles
+    ("mixtral", (1, 2, 32), 64, "ssmm_kernel<32, 1, 2, 1>", "ssmm_kernel<32, 1, 2, 1>"),
+    ("qwen2", (1, 2, 32), 1, "ssmm_kernel<16, 1, 2, 1>", "ssmm_kernel<16, 1, 2, 1>"),
+    # N = M (and N>1 formats transcoded to it): gate + up and the m-tile-paired down at NT=224
+    ("mixtral", (4, 8, 32), 4096, "ssmm_pair_kernel<224, 2, 1, 1>", "ssmm_pair_kernel<224, 2, 1, 1>"),
+    ("mixtral", (2, 2, 32), 4096, "ssmm_pair_kernel<224, 2, 1, 1>", "ssmm_pair_kernel<224, 2, 1, 1>"),
+])
+def test_kernel_selection_rules(lib, model, fmt, T, gu_expect, dn_expect):
+    """The launch decisions of samoyeds_moe_layer (tile width, CTA pair vs single CTA,
+    m-tile pairing) as smy_moe_kernel_names reports them -- host-only."""
+    import bench
+    from paper_2503_10725_b200 import api
+    d, f, E, k, gating = bench.MODELS[model]
+    cfg = api.MoEConfig(E, k, d, f, 0, gating, api.Format(*fmt)).kernel_config().c()
+    gu, dn = C.create_string_buffer(96), C.create_string_buffer(96)
+    assert lib.smy_moe_kernel_names(C.byref(cfg), T, gu, dn, 96) == 0
+    assert (gu.value.decode(), dn.value.decode()) == (gu_expect, dn_expect)
