@@ -22,6 +22,11 @@ constexpr int kMaxPeers = 8;      // ranks of one NVLink/NVSwitch node (expert p
 #ifndef SMY_NT_WIDE
 #define SMY_NT_WIDE 224
 #endif
+// token tile of the m-tile-paired (1,2,V) gate/up on the CTA pair (two m-tiles x two
+// slots x SMY_MTP_NT accumulator columns must fit TMEM beside the E columns)
+#ifndef SMY_MTP_NT
+#define SMY_MTP_NT 112
+#endif
 // token-ring depth of the SEL-gather pair launches (SPLIT rings; capped by what fits
 // beside 3 weight slots: 7 at NT = 112 (the m-tile-paired gate/up), 5 at NT = 224;
 // 5 -> 7 at NT = 112: token-ring waits 495 k -> 391 k cycles, gate/up -2 to -3 %)

@@ -315,7 +315,7 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   const bool pair_dn_ok = ssmm_pair_images_ok(wd, nullptr, E, img_dn);
   const int cl_gu = fused && pair_gu_ok ? ssmm_pair_cluster(nt_gu, nw_gu, ggu.ms, ggu.rep, ggu.m_tiles, tpg, 1) : 0;
   const int mtp_gu = var.v == 0 ? gu_mtp_half(ilv, cl_gu, ggu, nt_gu) : 0;
-  if (mtp_gu) nt_gu = 112;
+  if (mtp_gu) nt_gu = SMY_MTP_NT;
   // N = M down weights with wide tiles: m-tile pairing on the CTA pair (the weight's
   // second half of m-tiles as the launch's second weight, samoyeds_ssmm): every token
   // stage of the intermediate feeds two accumulators
@@ -504,7 +504,7 @@ smy_status moe_kernel_names(const smy_moe_config* c, int64_t T, char* gu, char* 
                 (ggu.ms == 1 && nw_gu == 2 && nt_gu == 224));
   const int mtp_gu = gu_mtp_half(ilv, cl_gu, ggu, nt_gu);
   if (mtp_gu)
-    snprintf(gu, len, "ssmm_pair_kernel<112, 2, 2, 1>");
+    snprintf(gu, len, "ssmm_pair_kernel<%d, 2, 2, 1>", SMY_MTP_NT);
   else if (cl_gu)
     snprintf(gu, len, "ssmm_pair_kernel<%d, %d, %d, %d>", nt_gu, nw_gu, ggu.ms, split_gu);
   else

@@ -37,7 +37,7 @@ extern template smy_status launch_pair_t<SMY_NT_WIDE, 1, 2, 0>(const SsmmArgs&, 
 extern template smy_status launch_pair_t<SMY_NT_WIDE, 1, 2, 1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<128, 1, 2, 1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<224, 2, 1, 1>(const SsmmArgs&, cudaStream_t);
-extern template smy_status launch_pair_t<112, 2, 2, 1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_pair_t<SMY_MTP_NT, 2, 2, 1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<128, 1, 1, 0>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<256, 1, 1, 0>(const SsmmArgs&, cudaStream_t);
 
@@ -90,7 +90,7 @@ int ssmm_pair_cluster(int nt, int nw, int ms, int rep, int m_tiles, int64_t toke
   if (gather && ms == 2 && nw == 1 && nt <= SMY_SINGLE_FAST_GATHER_NT) return 0;
   // an odd m-tile count gives the last pair a phantom peer tile (loads repeated, stores masked)
   if (rep != 1 || m_tiles < 2 || tokens_per_group < 64) return 0;
-  if (ms == 2 && !(nw == 2 ? (nt == 64 || nt == 112) : (nt == 128 || nt == SMY_NT_WIDE))) return 0;
+  if (ms == 2 && !(nw == 2 ? (nt == 64 || nt == 112 || nt == SMY_MTP_NT) : (nt == 128 || nt == SMY_NT_WIDE))) return 0;
   // N == M (plain 2:4): one weight at 128 / 256 tokens, or gate + up (NW = 2) at 224 --
   // two weights per token stage halve the SEL-gather bytes per MMA
   if (ms == 1 && !((nw == 1 && (nt == 128 || nt == 256)) || (nw == 2 && nt == 224))) return 0;
@@ -157,8 +157,8 @@ smy_status ssmm_launch_pair(const SsmmArgs& a0, int nt, int nw, int ms, int cl, 
   smy_status st = make_w_tmap(&a.tmap_w, a.wbase, (int64_t)((hi - lo) / 128), (kABytes + kEBytes + 64 + 127) / 128);
   if (st != SMY_OK) return st;
   if (ms == 2 && nw == 2 && nt == 64) return launch_pair_t<64, 2, 2, 0>(a, s);
-  if (ms == 2 && nw == 2 && nt == 112)
-    return a.mtp_half && a.sel_in ? launch_pair_t<112, 2, 2, 1>(a, s) : launch_pair_t<112, 2, 2, 0>(a, s);
+  if (ms == 2 && nw == 2 && nt == SMY_MTP_NT && a.mtp_half && a.sel_in) return launch_pair_t<SMY_MTP_NT, 2, 2, 1>(a, s);
+  if (ms == 2 && nw == 2 && nt == 112) return launch_pair_t<112, 2, 2, 0>(a, s);
   if (ms == 2 && nw == 1 && nt == 128) return a.sel_in && !(a.debug & 16384) ? launch_pair_t<128, 1, 2, 1>(a, s)
                                                                            : launch_pair_t<128, 1, 2, 0>(a, s);
   // SEL-gathered token rows (gate/up): separate, deeper token ring
