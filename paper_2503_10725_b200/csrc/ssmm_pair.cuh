@@ -184,8 +184,12 @@ constexpr int kPairThreads = 32 * (11 + kPairEpiWarps - 4);  // + producer, 2 MM
 #ifndef SMY_PAIR_GATHER_WARPS
 #define SMY_PAIR_GATHER_WARPS 8
 #endif
-// (8 gather warps cover 16 token rows per pass: halves of a multiple of 16 rows only)
-constexpr int pair_gather_warps(int split, int nt) { return split && (nt / 2) % 16 == 0 ? SMY_PAIR_GATHER_WARPS : 4; }
+// (w gather warps cover 2w token rows per pass: 8 warps for halves of a multiple of
+// 16 rows, 7 for multiples of 14 -- the NT = 112 m-tile-paired gate/up)
+constexpr int pair_gather_warps(int split, int nt) {
+  return !split ? 4 : (nt / 2) % (2 * SMY_PAIR_GATHER_WARPS) == 0 ? SMY_PAIR_GATHER_WARPS
+                    : (SMY_PAIR_GATHER_WARPS >= 7 && (nt / 2) % 14 == 0) ? 7 : 4;
+}
 constexpr int pair_threads(int split, int nt) { return kPairThreads + 32 * (pair_gather_warps(split, nt) - 4); }
 constexpr int pair_gather_threads(int split, int nt) { return 32 * pair_gather_warps(split, nt); }
 
@@ -510,11 +514,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
     if (gather) {
       constexpr int GT = pair_gather_threads(SPLIT, NT), RS = GT / 16;
       const int tb = warp < 10 ? threadIdx.x - 6 * 32 : threadIdx.x - 15 * 32 + kGatherThreads;
-      static_assert(GT % 128 == 0 && H % RS == 0, "gather mapping");
+      static_assert(GT % 32 == 0 && H % RS == 0, "gather mapping");
       const uint64_t pol_g = SMY_GATHER_EVICT_LAST ? policy_evict_last() : 0;
       constexpr int NI = H / RS;
       const int r0 = tb >> 4, ch = tb & 15;
       const uint32_t dst0 = (uint32_t)((ch >> 3) * (H * 128) + r0 * 128 + (((ch & 7) ^ (r0 & 7)) << 4));
+      // swizzled destination of row r0 + RS*i relative to dst0 (RS % 8 == 0: the same
+      // XOR pattern for every i; RS = 14 -- 7 gather warps -- changes it per row)
+      auto dst_off = [&](int i) -> uint32_t {
+        if (RS % 8 == 0) return 128u * RS * i;
+        const int row = r0 + RS * i;
+        return (uint32_t)((ch >> 3) * (H * 128) + row * 128 + (((ch & 7) ^ (row & 7)) << 4)) - dst0;
+      };
       uint32_t it = 0;
       TileInfo ti;
       for (int tile = pair0; decode_tile(a, NT, tile, ti); tile += pstep) {
@@ -554,11 +565,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
               if ((valid >> i) & 1u)
               {
                 if (SMY_GATHER_EVICT_LAST)
-                  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(bs + 128u * RS * i),
+                  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(bs + dst_off(i)),
                                "l"(src[i] + kcol0), "l"(pol_g)
                                : "memory");
                 else
-                  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(bs + 128u * RS * i), "l"(src[i] + kcol0)
+                  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(bs + dst_off(i)), "l"(src[i] + kcol0)
                                : "memory");
               }
           }
