@@ -22,6 +22,9 @@
 #ifndef SMY_PAIR_MIN_WSLOTS
 #define SMY_PAIR_MIN_WSLOTS 3  // weight slots kept beside the token ring of a SPLIT launch
 #endif
+#ifndef SMY_PW_ACC
+#define SMY_PW_ACC 0  // per-weight accumulator hand-off of the m-tile-paired gate/up (measured slower)
+#endif
 #ifndef SMY_GATHER_SPIN
 #define SMY_GATHER_SPIN 0
 #endif
@@ -249,6 +252,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
   uint64_t* bfull = SPLIT ? wempty + 8 : wfull;        // [SB]
   uint64_t* bempty = SPLIT ? wempty + 16 : wempty;     // [SB]
   constexpr int AB = C::kAccBufs;
+  // per-weight accumulator hand-off (m-tile-paired ILV gate/up, one accumulator set):
+  // acc_full[w] / acc_empty[w] per weight, so issuer w starts its next tile as soon as
+  // both epilogues have drained weight w -- the weight-0 MMAs of tile i+1 overlap the
+  // weight-1 half of tile i's epilogue
+  const bool PW = SMY_PW_ACC && NW == 2 && MS == 2 && AB == 1 && a.mtp_half && a.epi == kEpiSiluMulIlv;
   uint64_t* acc_full = wempty + 24;    // [AB]
   uint64_t* acc_empty = acc_full + 2;  // [AB]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
@@ -290,8 +298,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
         mbar_init(&wempty[s], kIssuers);  // every issuer warp's commit
       }
     }
-    for (int b = 0; b < AB; ++b) {
-      mbar_init(&acc_full[b], kIssuers);           // every issuer warp's commit
+    for (int b = 0; b < (PW ? 2 : AB); ++b) {
+      mbar_init(&acc_full[b], PW ? 1 : kIssuers);  // every issuer warp's commit (PW: its weight's)
       mbar_init(&acc_empty[b], 2 * kPairEpiWarps);  // every epilogue warp of both CTAs
     }
     fence_mbar_init();
@@ -410,7 +418,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
         unsigned long long t0 = prof ? clk() : 0;
         const int ab = tcount % AB;
         const uint32_t tacc = tm + ab * C::kAccCols;
-        mbar_wait_cta(&acc_empty[ab], (tcount / AB) & 1);  // both epilogues have read the accumulator
+        mbar_wait_cta(&acc_empty[PW ? w : ab], (tcount / AB) & 1);  // both epilogues have read the accumulator
         if (prof) pc[1] += clk() - t0;
         tc_fence_after();
         const uint32_t nbits = __reduce_or_sync(0xffffffffu, ((uint32_t)(2 * pair_half(ti.n_local)) >> 3) << 17);
@@ -487,7 +495,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
           tc_commit2_mc_elect(&wempty[st], 0x3);
           if constexpr (SPLIT) tc_commit2_mc_elect(&bempty[sb], 0x3);
         }
-        tc_commit2_mc_elect(&acc_full[ab], 0x3);
+        tc_commit2_mc_elect(&acc_full[PW ? w : ab], 0x3);
         pc[7] += 1;
       }
       if (prof) pc[2] = clk() - tstart;
@@ -597,7 +605,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(acc_empty_leader + 8 * b);
     };
-    for (int b = 0; b < AB; ++b) release(b);
+    for (int b = 0; b < (PW ? 2 : AB); ++b) release(b);
     uint32_t tcount = 0;
     TileInfo ti;
     const bool ilv = (NW == 1 || a.mtp_half) && a.epi == kEpiSiluMulIlv;
@@ -609,6 +617,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
       unsigned long long t0 = prof ? clk() : 0;
       const int ab = tcount % AB;
       const uint32_t tacc = tmem + ab * C::kAccCols;
+      if (PW) {  // per-weight hand-off: drain weight 0, release it, then weight 1
+        const int cg = 16 * (4 * m_own + q) + (lane & 15);
+        const bool gvalid = m_own < a.m_tiles && cg < a.R / 2 && !(a.debug & 8);
+#pragma unroll 1
+        for (int w = 0; w < 2; ++w) {
+          mbar_wait_cta(&acc_full[w], tcount & 1);
+          tc_fence_after();
+          const int cgw = cg + w * a.mtp_half * 64;  // a 128-lane m-tile holds 64 outputs
+          for (int c0 = 16 * h; c0 < ti.n_local; c0 += 32) {
+            float v[2][16];
+            tmem_ld16(tacc + lane_base + (2 * w) * NT + c0, v[0]);
+            tmem_ld16(tacc + lane_base + (2 * w + 1) * NT + c0, v[1]);
+            tmem_ld_wait();
+            if (c0 + 32 >= ti.n_local) release(w);
+            if (!(a.debug & 32))
+              ilv_chunk(v, gvalid && cgw < a.R / 2, min(16, ti.n_local - c0), static_cast<uint16_t*>(a.out), a.ldo,
+                        ti.row0 + ti.t0 + c0, cgw, lane, a.rows_out);
+          }
+          if (16 * h >= ti.n_local) release(w);  // no chunk of this tile for this warp
+        }
+        if (prof) pc[4] += clk() - t0;
+        continue;
+      }
       mbar_wait_cta(&acc_full[ab], (tcount / AB) & 1);
       if (prof) { const unsigned long long t1 = clk(); pc[3] += t1 - t0; t0 = t1; }
       tc_fence_after();
