@@ -149,7 +149,8 @@ SMY_API smy_status samoyeds_interleave_gate_up(const smy_weight* gate, const smy
  *   SMY_EPI_SILU_MUL_INTERLEAVED  w = the interleaved gate/up weight [2f x d]
  *                            (samoyeds_interleave_gate_up), w2 = NULL:
  *                            out[t * ldo + o] = bf16(silu(C_gate[t,o]) * C_up[t,o])
- *                            for o < f (BF16; format (1,2,V), V % 32 == 0)
+ *                            for o < f (BF16; format (1,2,V), (N,2N,V) or
+ *                            N == M, V % 32 == 0)
  *   SMY_EPI_SCATTER_ADD      out[sel[t] * ldo + o] += scale[t] * C[t, o]  (f32;
  *                            scale NULL = 1; atomic, order not deterministic;
  *                            16-byte reductions: ldo % 4 == 0, out 16-byte
@@ -194,8 +195,10 @@ SMY_API smy_status samoyeds_route(const float* logits, int64_t T, int32_t E, int
  *          + sum_s Wd_s( silu(Wg_s x_t) * (Wu_s x_t) )
  * experts: host array [E][3] of smy_weight: (gate, up, down) when
  * cfg->gate_up == SMY_GU_SEPARATE, or (gu, unused, down) when SMY_GU_INTERLEAVED
- * (gu from samoyeds_interleave_gate_up; format (1,2,V), V % 32 == 0 -- the
- * prefill kernels read one 128-lane tile of gate+up rows per MMA); shared: host
+ * (gu from samoyeds_interleave_gate_up; format (1,2,V), (N,2N,V) or N == M,
+ * V % 32 == 0 -- the kernels read one 128-lane tile of gate+up rows per MMA;
+ * (N,2N,32) formats with N > 1 run every one-weight SSMM of the layer with the
+ * in-shared-memory row expansion of their own compressed image); shared: host
  * array [num_shared][3] in the same layout, or NULL (num_shared + top_k <= 16,
  * num_experts + num_shared <= 128); the shared experts run as extra groups of the
  * same two grouped SSMM launches (the routing appends ids E.. with weight 1 to

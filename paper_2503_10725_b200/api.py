@@ -230,8 +230,10 @@ class MoEConfig:
         # gate and up as the two weights of one launch (two accumulators per token
         # stage, half the SEL-gather bytes per MMA of the interleaved one-slot
         # kernel: Mixtral (2,2,32) gate/up 2.04 -> 1.08 ms, profiles/r2_nm_formats.md)
+        # (N,2N,V), N > 1, kept native (transcode "off"): the interleaved weight too --
+        # every one-weight SSMM of these formats runs the in-smem row expansion (§7.5)
         f = self.fmt
-        ok = f.v % 32 == 0 and f.n == 1 and f.m == 2 and self.ffn % 128 == 0
+        ok = f.v % 32 == 0 and f.m == 2 * f.n and self.ffn % 128 == 0
         return "interleaved" if ok else "separate"
 
     def kernel_config(self) -> "MoEConfig":

@@ -121,7 +121,7 @@ static smy_status check_experts(const smy_moe_config* cfg, const smy_weight* exp
   if (cfg->gate_up != SMY_GU_SEPARATE && cfg->gate_up != SMY_GU_INTERLEAVED) return SMY_E_CONFIG;
   const bool ilv = cfg->gate_up == SMY_GU_INTERLEAVED;
   if (ilv && !ilv_format(cfg->fmt)) {
-    set_last_error("SMY_GU_INTERLEAVED needs format (1,2,V) or N == M, with V % 32 == 0");
+    set_last_error("SMY_GU_INTERLEAVED needs format (1,2,V), (N,2N,V) or N == M, with V % 32 == 0");
     return SMY_E_CONFIG;
   }
   for (int e = 0; e < n; ++e)
@@ -252,7 +252,7 @@ smy_status samoyeds_ssmm(const smy_weight* w, const smy_weight* w2, const void* 
   } else if (epi == SMY_EPI_SILU_MUL_INTERLEAVED) {
     if (out_dtype != SMY_BF16) return SMY_E_CONFIG;
     if (!ilv_format(w->d.fmt)) {
-      set_last_error("SILU_MUL_INTERLEAVED needs format (1,2,V) or N == M, with V % 32 == 0");
+      set_last_error("SILU_MUL_INTERLEAVED needs format (1,2,V), (N,2N,V) or N == M, with V % 32 == 0");
       return SMY_E_CONFIG;
     }
     if (w->d.rows % 64) return SMY_E_SHAPE;
@@ -290,9 +290,11 @@ smy_status samoyeds_ssmm(const smy_weight* w, const smy_weight* w2, const void* 
     }
   }
   const int nw = epi == SMY_EPI_SILU_MUL_COMPACT ? 2 : 1;
-  const int nt = ssmm_pick_nt(nw, g.ms, g.rep, n_sel);
+  const int xp = nw == 1 && xp_on(w->d.fmt) ? 1 : 0;  // (N, 2N, 32): in-smem row expansion
+  const int nt = ssmm_pick_nt(nw, g.ms, g.rep, n_sel, xp);
   SsmmArgs a;
   memset(&a, 0, sizeof(a));
+  a.xp = xp;
   a.img0[0] = static_cast<const uint8_t*>(w->image);
   a.img1[0] = nw == 2 ? static_cast<const uint8_t*>(w2->image) : nullptr;
   a.num_groups = 1;

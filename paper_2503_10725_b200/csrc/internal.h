@@ -77,6 +77,9 @@ struct SsmmArgs {
   // token stage feeds two accumulators; output rows of weight w are offset by
   // w * mtp_half * 128; m_tiles = mtp_half; 0 = off
   int mtp_half;
+  // in-smem row expansion of an (N, 2N, 32) image, N > 1 (ssmm_kernel<..., XP = 1>): set by
+  // ssmm_launch from the format; 0 = the lane-masked M-slot remap
+  int xp;
   // programmatic dependent launch: the launch may start while the previous kernel of
   // the stream (the gate/up SSMM) still runs; its producer streams the first ring of
   // WEIGHT stages, then waits (griddepcontrol.wait) before the dependent token loads,
@@ -120,7 +123,7 @@ struct SsmmPlan {
   int nt, nw, ms, rep;
 };
 // Choose the token tile for a launch given the expected tokens per group.
-int ssmm_pick_nt(int nw, int ms, int rep, int64_t tokens_per_group);
+int ssmm_pick_nt(int nw, int ms, int rep, int64_t tokens_per_group, int xp = 0);
 // gathered token pools larger than this run their tiles m-tile fastest (L2 is 126 MB;
 // the weight tiles in flight and the outputs share it)
 constexpr int64_t kGatherL2Bytes = 64ll << 20;
@@ -157,7 +160,14 @@ constexpr int kDebugValidate = 65536;  // SMY_DEBUG bit: validate SEL in samoyed
 smy_status interleave_launch(const smy_weight* gate, const smy_weight* up, const smy_wdesc& d, const Geometry& g,
                              smy_weight* gu, cudaStream_t s);
 // formats with an interleaved gate/up epilogue: (1,2,V) and N = M (plain 2:4), V % 32 == 0
-inline bool ilv_format(const smy_format& f) { return f.v % 32 == 0 && ((f.n == 1 && f.m == 2) || f.n == f.m); }
+// formats whose SSMMs run the in-smem row expansion: N > 1, M = 2N,
+// V % 32 == 0 -- (4,8,32), (8,16,32), (2,4,32); SMY_DEBUG=8388608 keeps the M-slot remap
+constexpr int kDebugNoXp = 8388608;
+inline bool xp_format(const smy_format& f) { return f.n > 1 && f.m == 2 * f.n && f.v % 32 == 0; }
+bool xp_on(const smy_format& f);  // xp_format and not disabled by SMY_DEBUG
+inline bool ilv_format(const smy_format& f) {
+  return f.v % 32 == 0 && ((f.n == 1 && f.m == 2) || f.n == f.m || xp_format(f));
+}
 smy_status compress_launch(const smy_wdesc* d, const Geometry& g, const uint16_t* w, int64_t ldw, int flags,
                            smy_weight* out, int32_t* d_status, cudaStream_t s);
 

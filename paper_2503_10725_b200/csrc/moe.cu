@@ -160,6 +160,8 @@ static smy_status grouped(const smy_weight* const* w0, const smy_weight* const* 
     a.img1[e] = w1 ? static_cast<const uint8_t*>(w1[e]->image) : nullptr;
   }
   a.num_groups = groups;
+  // (N, 2N, 32) weights: the in-smem row expansion (single-CTA, one weight per launch)
+  a.xp = (nw == 1 && cl == 0 && mtp_half == 0 && xp_on(w0[0]->d.fmt)) ? 1 : 0;
   a.R = (int)g.R;
   a.m_out = m_out;
   a.n_fmt = g.ms == 1 ? 1 : w0[0]->d.fmt.n;
@@ -292,8 +294,10 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
   // decode-sized expert rarely needs a second n-tile (which would re-stream its weights
   // through the SMs); ragged tiles issue MMAs of their own width
   const int64_t tpg_hi = tpg + (int64_t)(3.0 * sqrt((double)tpg) + 0.999);
-  int nt_gu = ssmm_pick_nt(nw_gu, ggu.ms, ggu.rep, tpg_hi);
-  int nt_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, tpg_hi);
+  // (N, 2N, 32) formats, N > 1: one-weight launches run the in-smem row expansion
+  const int xp_gu = nw_gu == 1 && xp_on(c->fmt) ? 1 : 0, xp_dn = xp_on(c->fmt) ? 1 : 0;
+  int nt_gu = ssmm_pick_nt(nw_gu, ggu.ms, ggu.rep, tpg_hi, xp_gu);
+  int nt_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, tpg_hi, xp_dn);
   const int64_t act = E < T * k ? E : T * k;
   const Variant var = t_variant;
   if (var.v != 0) {  // ablation variants: the single-GPU interleaved layer with router logits
@@ -428,8 +432,8 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
     const smy_weight* sg[1] = {&shared[3 * i + 0]};
     const smy_weight* su[1] = {&shared[3 * i + 1]};
     const smy_weight* sd[1] = {&shared[3 * i + 2]};
-    const int nts_gu = ssmm_pick_nt(nw_gu, ggu.ms, ggu.rep, T);
-    const int nts_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, T);
+    const int nts_gu = ssmm_pick_nt(nw_gu, ggu.ms, ggu.rep, T, xp_gu);
+    const int nts_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, T, xp_dn);
     auto single = [&](const smy_weight* const* a0, const smy_weight* const* a1, const Geometry& g, int m_out, int nt,
                       int nw, const uint16_t* xx, int64_t ldx, int epi, void* o, int64_t ldo, int ob) {
       SsmmArgs a;
@@ -437,6 +441,7 @@ smy_status moe_core(const smy_moe_config* c, const smy_weight* experts, const sm
       a.img0[0] = static_cast<const uint8_t*>(a0[0]->image);
       a.img1[0] = a1 ? static_cast<const uint8_t*>(a1[0]->image) : nullptr;
       a.num_groups = 1;
+      a.xp = nw == 1 && xp_on(c->fmt) ? 1 : 0;
       a.R = (int)g.R;
       a.m_out = m_out;
       a.n_fmt = g.ms == 1 ? 1 : c->fmt.n;
@@ -493,8 +498,9 @@ smy_status moe_kernel_names(const smy_moe_config* c, int64_t T, char* gu, char* 
   const int Er = c->num_experts, kr = c->top_k;
   const int64_t tpg = Er ? (T * kr + Er - 1) / Er : 0;
   const int64_t tpg_hi = tpg + (int64_t)(3.0 * sqrt((double)tpg) + 0.999);
-  const int nt_gu = ssmm_pick_nt(nw_gu, ggu.ms, ggu.rep, tpg_hi);
-  const int nt_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, tpg_hi);
+  const int xp_gu = nw_gu == 1 && xp_on(c->fmt) ? 1 : 0, xp_dn = xp_on(c->fmt) ? 1 : 0;
+  const int nt_gu = ssmm_pick_nt(nw_gu, ggu.ms, ggu.rep, tpg_hi, xp_gu);
+  const int nt_dn = ssmm_pick_nt(1, gdn.ms, gdn.rep, tpg_hi, xp_dn);
   const int cl_gu = fused ? ssmm_pair_cluster(nt_gu, nw_gu, ggu.ms, ggu.rep, ggu.m_tiles, tpg, 1) : 0;
   const int mtp_dn = down_mtp_half(gdn, tpg, tpg_hi);
   const int cl_dn = mtp_dn ? 2 : ssmm_pair_cluster(nt_dn, 1, gdn.ms, gdn.rep, gdn.m_tiles, tpg, 0);
@@ -507,6 +513,8 @@ smy_status moe_kernel_names(const smy_moe_config* c, int64_t T, char* gu, char* 
     snprintf(gu, len, "ssmm_pair_kernel<%d, 2, 2, 1>", SMY_MTP_NT);
   else if (cl_gu)
     snprintf(gu, len, "ssmm_pair_kernel<%d, %d, %d, %d>", nt_gu, nw_gu, ggu.ms, split_gu);
+  else if (xp_gu)
+    snprintf(gu, len, "ssmm_kernel<%d, 1, 2, 1, 1>", nt_gu);
   else
     snprintf(gu, len, "ssmm_kernel<%d, %d, %d, %d>", nt_gu, nw_gu, ggu.ms, ggu.rep);
   if (mtp_dn && gdn.ms == 1)
@@ -515,6 +523,8 @@ smy_status moe_kernel_names(const smy_moe_config* c, int64_t T, char* gu, char* 
     snprintf(dn, len, "ssmm_pair_kernel<112, 2, 2, 0>");
   else if (cl_dn)
     snprintf(dn, len, "ssmm_pair_kernel<%d, %d, %d, %d>", nt_dn, 1, gdn.ms, 0);
+  else if (xp_dn)
+    snprintf(dn, len, "ssmm_kernel<%d, 1, 2, 1, 1>", nt_dn);
   else
     snprintf(dn, len, "ssmm_kernel<%d, %d, %d, %d>", nt_dn, 1, gdn.ms, gdn.rep);
   return SMY_OK;

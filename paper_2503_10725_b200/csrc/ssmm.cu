@@ -29,6 +29,10 @@ extern template smy_status launch_t<16,1,8,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<16,1,16,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<32,2,4,1>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_t<16,2,8,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<16,1,2,1,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<32,1,2,1,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<64,1,2,1,1>(const SsmmArgs&, cudaStream_t);
+extern template smy_status launch_t<128,1,2,1,1>(const SsmmArgs&, cudaStream_t);
 
 extern template smy_status launch_pair_t<64, 2, 2, 0>(const SsmmArgs&, cudaStream_t);
 extern template smy_status launch_pair_t<112, 2, 2, 0>(const SsmmArgs&, cudaStream_t);
@@ -42,7 +46,7 @@ extern template smy_status launch_pair_t<128, 1, 1, 0>(const SsmmArgs&, cudaStre
 extern template smy_status launch_pair_t<256, 1, 1, 0>(const SsmmArgs&, cudaStream_t);
 
 namespace {
-struct Entry { int nt, nw, ms, rep; smy_status (*fn)(const SsmmArgs&, cudaStream_t); };
+struct Entry { int nt, nw, ms, rep; smy_status (*fn)(const SsmmArgs&, cudaStream_t); int xp = 0; };
 const Entry kTable[] = {
     {16, 1, 2, 1, &launch_t<16,1,2,1>},
     {32, 1, 2, 1, &launch_t<32,1,2,1>},
@@ -70,14 +74,23 @@ const Entry kTable[] = {
     {16, 1, 16, 1, &launch_t<16,1,16,1>},
     {32, 2, 4, 1, &launch_t<32,2,4,1>},
     {16, 2, 8, 1, &launch_t<16,2,8,1>},
+    // (N, 2N, 32), N > 1: in-smem row expansion, two 128-row halves per m-tile
+    {16, 1, 2, 1, &launch_t<16,1,2,1,1>, 1},
+    {32, 1, 2, 1, &launch_t<32,1,2,1,1>, 1},
+    {64, 1, 2, 1, &launch_t<64,1,2,1,1>, 1},
+    {128, 1, 2, 1, &launch_t<128,1,2,1,1>, 1},
 };
 }  // namespace
 
-int ssmm_pick_nt(int nw, int ms, int rep, int64_t tpg) {
-  // candidate tile widths for this (nw, ms, rep), ascending
+bool xp_on(const smy_format& f) { return xp_format(f) && !(debug_flags() & kDebugNoXp); }
+
+int ssmm_pick_nt(int nw, int ms, int rep, int64_t tpg, int xp) {
+  // candidate tile widths for this (nw, ms, rep), ascending (xp: the expansion kernels,
+  // one weight, two halves)
+  if (xp) ms = 2;
   int best = -1, largest = -1;
   for (const Entry& e : kTable) {
-    if (e.nw != nw || e.ms != ms || e.rep != rep) continue;
+    if (e.nw != nw || e.ms != ms || e.rep != rep || e.xp != xp) continue;
     if (e.nt > largest) largest = e.nt;
     if (e.nt >= tpg && (best < 0 || e.nt < best)) best = e.nt;
   }
@@ -210,8 +223,15 @@ smy_status ssmm_launch(const SsmmArgs& a0, int nt, int nw, int ms, int rep, cuda
     ap = &dbg;
   }
   const SsmmArgs& a = *ap;
+  if (a.xp) {
+    if (nw != 1 || rep != 1 || a.m_fmt != 2 * a.n_fmt || a.n_fmt < 2) {
+      set_last_error("ssmm: the row expansion needs one (N, 2N, 32) weight, N > 1");
+      return SMY_E_CONFIG;
+    }
+    ms = 2;
+  }
   for (const Entry& e : kTable)
-    if (e.nt == nt && e.nw == nw && e.ms == ms && e.rep == rep) return e.fn(a, s);
+    if (e.nt == nt && e.nw == nw && e.ms == ms && e.rep == rep && e.xp == a.xp) return e.fn(a, s);
   set_last_error("ssmm: unsupported (nt, nw, ms, rep) combination");
   return SMY_E_CONFIG;
 }

@@ -37,11 +37,16 @@
 
 namespace smy {
 
-template <int NT, int NW, int MS, int REP>
+template <int NT, int NW, int MS, int REP, int XP = 0>
 struct Cfg {
   static constexpr int kWStride = 19456;                  // A|E|planes, 1024-aligned stride
   static constexpr int kBBytes = NT * 128 * (2 / REP);     // token tile per stage
   static constexpr int kStageBytes = NW * kWStride + kBBytes;
+  // XP (in-smem row expansion of an (N, 2N, 32) image, N > 1): ring of expanded stages,
+  // each = two 128-row A halves | their two E images | the enabled-lane masks
+  static constexpr int kXMask = 2 * kABytes + 2 * kEBytes;
+  static constexpr int kXUnit = XP ? kXMask + 1024 : 0;
+  static constexpr int kXSlots = XP ? 2 : 0;
   static constexpr int kAccCols = NW * MS * NT;
   // two accumulator sets when they fit: the epilogue drains tile i while the
   // MMAs of tile i+1 run (decode-sized tiles)
@@ -55,9 +60,9 @@ struct Cfg {
                                                         : 512;
   static constexpr int kAux = 2048;                        // barriers + gather row ids
   static constexpr int kSmemCap = 232448 - 1024 - kAux;
-  static constexpr int kStagesRaw = kSmemCap / kStageBytes;
+  static constexpr int kStagesRaw = (kSmemCap - kXSlots * kXUnit) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + kAux;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kXSlots * kXUnit + 1024 + kAux;
   static constexpr int kPlanes = MS == 1 ? 0 : MS == 2 ? 1 : MS == 4 ? 2 : MS == 8 ? 3 : 4;
   static_assert(kColsNeeded <= 512, "TMEM budget");
   static_assert(kStages >= 2, "smem budget");
@@ -68,6 +73,20 @@ struct Cfg {
 // precomputes per-thread source pointers, NT/8 of them)
 constexpr int kThreads = 352;  // warps 0-3 epilogue, 4 producer, 5 + 10 MMA, 6-9 gather
 constexpr int kGatherThreads = 128;
+// XP launches add warps 11-14: the in-smem row expansion
+constexpr int threads_of(int xp) { return xp ? 480 : kThreads; }
+
+// Expanded row (0..255 of an m-tile's 2 x 128 TMEM lanes) of logical output row o of
+// an (N, 2N, V) m-tile.  Interleaved gate/up weights (reading R20: blocks of 32 gate |
+// 32 up output rows) are laid out so that every warp's 32 lanes hold 16 gate rows and
+// the up rows of the same 16 outputs (lanes 0-15 / 16-31, the N = M epilogue pairing);
+// other weights keep o.  Either way the rows of compressed rows [32w, 32w + 32) stay in
+// [64w, 64w + 64).
+__device__ __forceinline__ int xp_pos(int o, bool ilv) {
+  if (!ilv) return o;
+  const int i = o & 31, up = (o >> 5) & 1;
+  return (o & ~63) + ((i >> 4) << 5) + (up << 4) + (i & 15);
+}
 
 struct TileInfo {
   int g, m_tile, t0, n_local, row0, k0, k1;  // k-stage range [k0, k1)
@@ -281,11 +300,18 @@ __device__ __forceinline__ void tma_tile2d(void* dst, const CUtensorMap* map, in
       : "memory");
 }
 
-template <int NT, int NW, int MS, int REP>
-__global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant__ SsmmArgs a) {
+template <int NT, int NW, int MS, int REP, int XP = 0>
+__global__ void __launch_bounds__(XP ? 480 : 352, 1) ssmm_kernel(const __grid_constant__ SsmmArgs a) {
   constexpr int kIssuers = (NW == 2 || MS >= 2) ? 2 : 1;  // MMA-issuing warps
-  using C = Cfg<NT, NW, MS, REP>;
+  using C = Cfg<NT, NW, MS, REP, XP>;
   constexpr int S = C::kStages;
+  // XP: the weight image is an (N, 2N, 32) format, N > 1.  Warps 11-14
+  // expand each compressed stage into two 128-row halves of output rows: compressed row
+  // r's window-j values / metadata move to expanded row (r / N) * 2N + idx[r][j] and the
+  // MMA of half h enables only the lanes some compressed row landed on.  Two unmasked-
+  // layout MMAs per window (as the (1,2,V) remap issues), whatever M is.
+  static_assert(!XP || (NW == 1 && MS == 2 && REP == 1), "XP: one weight, two halves");
+  constexpr int XS = C::kXSlots;
   // a dependent launch (the down SSMM after gate/up, SsmmArgs::pdl) may start its
   // prologue and weight stream on SMs this grid has left
   if (threadIdx.x == 0) griddep_launch_dependents();
@@ -296,7 +322,9 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
   uint64_t* empty = full + S;
   uint64_t* acc_full = empty + S;      // [kAccBufs]
   uint64_t* acc_empty = acc_full + 2;  // [kAccBufs]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* xfull = acc_empty + 2;     // [XS] expanded stage written (4 expander warps)
+  uint64_t* xempty = xfull + 2;        // [XS] expanded stage consumed (issuer commits)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xempty + 2);
   constexpr int AB = C::kAccBufs;
   int32_t* rows = reinterpret_cast<int32_t*>(aux + 1024);  // gather row ids of the current tile
   const bool gather = a.sel_in != nullptr;
@@ -305,11 +333,15 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], gather ? 1 + kGatherThreads : 1);
-      mbar_init(&empty[s], kIssuers);
+      mbar_init(&empty[s], kIssuers + (XP ? 4 : 0));  // XP: the expander warps also read the stage
     }
     for (int b = 0; b < AB; ++b) {
       mbar_init(&acc_full[b], kIssuers);
       mbar_init(&acc_empty[b], 4);
+    }
+    for (int x = 0; x < XS; ++x) {
+      mbar_init(&xfull[x], 4);
+      mbar_init(&xempty[x], kIssuers);
     }
     fence_mbar_init();
   }
@@ -320,6 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
   const uint32_t tmem = *tmem_slot;
   auto wsm = [&](int st, int w) { return smem + st * C::kStageBytes + w * C::kWStride; };
   auto bsm = [&](int st) { return smem + st * C::kStageBytes + NW * C::kWStride; };
+  auto xsm = [&](int x) { return smem + S * C::kStageBytes + x * C::kXUnit; };
   const int ks = a.k_stages;
   const int tile0 = blockIdx.x, tstep = gridDim.x;
   // SMY_DEBUG & 128: per-role cycle counters (same slots as the pair kernel)
@@ -330,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
   if (warp == 4) {
     // ========== producer: weight image (bulk) + contiguous token tile (2D TMA) ==========
     if (lane == 0) {
-      const uint32_t wbytes = kABytes + kEBytes + 64 * C::kPlanes;
+      const uint32_t wbytes = kABytes + kEBytes + 64 * (XP ? a.planes : C::kPlanes);
       const uint32_t stage_bytes = NW * wbytes + (gather ? 0u : (uint32_t)C::kBBytes);
       const uint64_t pol_w = a.weights_stream ? policy_evict_first() : policy_evict_normal();
       const uint64_t pol_x = policy_evict_last();
@@ -418,6 +451,28 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
         // E double-buffered in TMEM: this stage's copy does not overwrite columns
         // the previous stage's MMAs may still be reading
         const uint32_t ecol = C::kECol + (it & 1) * 8 + 4 * mi;
+        if constexpr (XP != 0) {
+          // expanded half mi of this stage: A rows, E image, enabled-lane masks
+          const int xs = it % XS;
+          t0 = prof ? clk() : 0;
+          mbar_wait(&xfull[xs], (it / XS) & 1);
+          if (prof) pc[0] += clk() - t0;
+          tc_fence_after();
+          const uint32_t xb = smem_base + S * C::kStageBytes + xs * C::kXUnit;
+          tc_cp_128x128b_elect(tm + ecol, desc_interleave(xb + 2 * kABytes + mi * kEBytes));
+#pragma unroll
+          for (int kb = 0; kb < 4; ++kb) {
+            const uint4 en = lds_v4(xb + C::kXMask + (mi * 4 + kb) * 16);
+            const uint64_t bdesc = desc_sw128(sbase + C::kWStride + (kb / 2) * (NT * 128) + (kb % 2) * 64);
+            const uint64_t adesc = desc_sw128(xb + mi * kABytes + kb * 32);
+            if (!(a.debug & 4))
+              tc_mma_sp_elect(tacc + mi * NT, adesc, bdesc, idesc | (uint32_t)(kb & 1), ~en.x, ~en.y, ~en.z, ~en.w,
+                              tm + ecol + (kb & 2));
+          }
+          tc_commit_elect(&empty[st]);
+          tc_commit_elect(&xempty[xs]);
+          continue;
+        }
         tc_cp_128x128b_elect(tm + ecol, desc_interleave(sbase + we * C::kWStride + kABytes));
         // index bit-planes of this stage (this warp's weight): LDS, no redux (see ssmm_pair.cuh)
         uint32_t pl[4][C::kPlanes > 0 ? C::kPlanes : 1][4];
@@ -460,6 +515,78 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
       pc[7] += 1;
     }
     if (prof) pc[2] = clk() - tstart;
+    }
+  } else if (warp >= 11) {
+    if constexpr (XP != 0) {
+    // ============ XP: in-smem row expansion (warps 11-14, thread = compressed row) ============
+    const int t = threadIdx.x - 11 * 32, w4 = t >> 5;
+    const int P = a.planes, N = a.n_fmt, M = a.m_fmt;
+    const bool ilvp = a.epi == kEpiSiluMulIlv;
+    const int gbase = (t / N) * M;  // first logical output row of this row's group (in the m-tile)
+    // this row's swizzled A chunk offsets and E half-word offsets (source side)
+    const uint32_t a_src = (uint32_t)((t >> 3) * 1024 + (t & 7) * 128), a_sw = (uint32_t)(t & 7);
+    const uint32_t e_src0 = kABytes + 16u * ((t & 7) + 16 * (t >> 4)) + 2u * ((t >> 3) & 1);
+    // stale rows are never enabled; start from zero values and valid (0,1) metadata anyway
+    for (int i = t; i < XS * C::kXUnit / 16; i += 128) {
+      const int off = (i * 16) % C::kXUnit;
+      const uint32_t v = off >= 2 * kABytes && off < C::kXMask ? 0x44444444u : 0u;
+      reinterpret_cast<uint4*>(xsm(0))[i] = make_uint4(v, v, v, v);
+    }
+    uint32_t it = 0;
+    TileInfo ti;
+    for (int tile = tile0; decode_tile(a, NT, tile, ti); tile += tstep) {
+      for (int k = ti.k0; k < ti.k1; ++k, ++it) {
+        const int st = it % S, xs = it % XS;
+        unsigned long long tx0 = prof ? clk() : 0;
+        mbar_wait(&full[st], (it / S) & 1);
+        if (prof) { const unsigned long long t1 = clk(); pc[8] += t1 - tx0; tx0 = t1; }
+        const uint8_t* cw = wsm(st, 0);
+        // every load of the stage first (independent), then the stores
+        uint4 av[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) av[c] = *reinterpret_cast<const uint4*>(cw + a_src + ((c ^ a_sw) << 4));
+        uint16_t ev[4][2];
+#pragma unroll
+        for (int kb = 0; kb < 4; ++kb)
+#pragma unroll
+          for (int k1 = 0; k1 < 2; ++k1) ev[kb][k1] = *reinterpret_cast<const uint16_t*>(cw + e_src0 + 128 * k1 + 4 * kb);
+        int p[4] = {0, 0, 0, 0};
+        for (int b = 0; b < P; ++b)
+#pragma unroll
+          for (int kb = 0; kb < 4; ++kb)
+            p[kb] |= (int)((*reinterpret_cast<const uint32_t*>(cw + kABytes + kEBytes + (kb * P + b) * 16 + w4 * 4) >>
+                            lane) & 1u) << b;
+        mbar_wait(&xempty[xs], ((it / XS) & 1) ^ 1);
+        if (prof) { const unsigned long long t1 = clk(); pc[9] += t1 - tx0; tx0 = t1; }
+        uint8_t* xu = xsm(xs);
+#pragma unroll
+        for (int kb = 0; kb < 4; ++kb) {
+          const int pos = xp_pos(gbase + p[kb], ilvp);  // in [64 w4, 64 w4 + 64)
+          const int h = pos >> 7, r = pos & 127;
+          uint8_t* arow = xu + h * kABytes + (r >> 3) * 1024 + (r & 7) * 128;
+          // A: the window's two 16-B chunks (128B swizzle: chunk c of row r at c ^ (r % 8))
+          *reinterpret_cast<uint4*>(arow + (((2 * kb) ^ (r & 7)) << 4)) = av[2 * kb];
+          *reinterpret_cast<uint4*>(arow + (((2 * kb + 1) ^ (r & 7)) << 4)) = av[2 * kb + 1];
+          // E: the row's 16-bit code word of each K-half (lane (row % 8) + 8 k1 + 16 (row / 16),
+          // bits 16 ((row / 8) % 2) of the window's 32-bit column)
+          uint8_t* erow = xu + 2 * kABytes + h * kEBytes + 16 * ((r & 7) + 16 * (r >> 4)) + 4 * kb + 2 * ((r >> 3) & 1);
+          *reinterpret_cast<uint16_t*>(erow) = ev[kb][0];
+          *reinterpret_cast<uint16_t*>(erow + 128) = ev[kb][1];
+          const int loc = pos - 64 * w4;
+          const uint32_t m0 = __reduce_or_sync(0xffffffffu, loc < 32 ? 1u << loc : 0u);
+          const uint32_t m1 = __reduce_or_sync(0xffffffffu, loc >= 32 ? 1u << (loc - 32) : 0u);
+          if (lane == 0)
+            *reinterpret_cast<uint2*>(xu + C::kXMask + ((w4 >> 1) * 4 + kb) * 16 + 8 * (w4 & 1)) = make_uint2(m0, m1);
+        }
+        fence_proxy_async_smem();  // generic-proxy writes -> tcgen05.cp / tcgen05.mma reads
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&xfull[xs]);
+          mbar_arrive(&empty[st]);
+        }
+        if (prof) pc[6] += clk() - tx0;
+      }
+    }
     }
   } else if (warp >= 6 && warp < 10) {
     // ================== SEL gather of token rows (warps 6-9, cp.async) ==================
@@ -562,6 +689,59 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
       mbar_wait(&acc_full[ab], (tcount / AB) & 1);
       if (prof) { const unsigned long long t1 = clk(); pc[3] += t1 - t0; t0 = t1; }
       tc_fence_after();
+      if constexpr (XP != 0) {
+        // lane l of warp q in half h = expanded row pos = 128 h + 32 q + l of the m-tile
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t tcol = tmem + lane_base + ab * C::kAccCols + h * NT;
+          if (a.epi == kEpiSiluMulIlv) {
+            // lanes 0-15 gate / 16-31 up of the same 16 outputs (xp_pos)
+            const int cg = ti.m_tile * 128 + 64 * h + 16 * q + (lane & 15);
+            for (int c0 = 0; c0 < ti.n_local; c0 += 16) {
+              float v[16];
+              tmem_ld16(tcol + c0, v);
+              tmem_ld_wait();
+              ilv_chunk_ms1(v, cg < a.m_out && !(a.debug & 8), min(16, ti.n_local - c0),
+                            static_cast<uint16_t*>(a.out), a.ldo, ti.row0 + ti.t0 + c0, cg, lane);
+            }
+            continue;
+          }
+          const int o = ti.m_tile * 256 + 128 * h + 32 * q + lane;  // output row of this lane
+          const bool ok = o < a.m_out && !(a.debug & 8);
+          for (int c0 = 0; c0 < ti.n_local; c0 += 16) {
+            float v[16];
+            tmem_ld16(tcol + c0, v);
+            tmem_ld_wait();
+            const int jmax = min(16, ti.n_local - c0);
+            if (a.epi == kEpiScatter) {
+              const int rl = ti.row0 + ti.t0 + c0 + (lane & 15);
+              float* my_row = (lane & 15) < jmax ? out_row(a, a.sel_out ? a.sel_out[rl] : rl) : nullptr;
+              const float my_s = (lane & 15) < jmax ? (a.scale ? a.scale[rl] : 1.f) : 0.f;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                float* orow = reinterpret_cast<float*>(
+                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), j));
+                const float sj = __shfl_sync(0xffffffffu, my_s, j);
+                if (ok && j < jmax) atomicAdd(orow + o, sj * v[j]);  // 32 lanes: 128 contiguous bytes
+              }
+              continue;
+            }
+            if (!ok) continue;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (j >= jmax) break;
+              const int64_t r = ti.row0 + ti.t0 + c0 + j;
+              if (a.out_bf16)
+                static_cast<uint16_t*>(a.out)[r * a.ldo + o] = __bfloat16_as_ushort(__float2bfloat16_rn(v[j]));
+              else
+                static_cast<float*>(a.out)[r * a.ldo + o] = v[j];
+            }
+          }
+        }
+        tc_fence_before();
+        zero_acc(ab);
+        if (prof) pc[4] += clk() - t0;
+        continue;
+      }
       if (NW == 1 && MS == 1 && REP == 1 && a.epi == kEpiSiluMulIlv) {
         // N = M: lanes 0-15 gate / 16-31 up of the same 16 outputs (reading R20)
         const int cg = 16 * (4 * ti.m_tile + q) + (lane & 15);
@@ -694,6 +874,7 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
     if (warp == 6 && lane == 0) { atomicAdd(o + 10, pc[10]); atomicAdd(o + 11, pc[11]); }
     if (warp == 0 && lane == 0) { atomicAdd(o + 3, pc[3]); atomicAdd(o + 4, pc[4]); }
     if (warp == 4 && lane == 0) { atomicAdd(o + 5, pc[5]); }
+    if (XP && warp == 11 && lane == 0) { atomicAdd(o + 6, pc[6]); atomicAdd(o + 8, pc[8]); atomicAdd(o + 9, pc[9]); }
   }
   __syncthreads();
   tc_fence_after();
@@ -702,12 +883,13 @@ __global__ void __launch_bounds__(kThreads, 1) ssmm_kernel(const __grid_constant
 
 // ------------------------------------------------------------------ host side
 
-template <int NT, int NW, int MS, int REP>
+template <int NT, int NW, int MS, int REP, int XP = 0>
 smy_status launch_t(const SsmmArgs& a, cudaStream_t s) {
-  using C = Cfg<NT, NW, MS, REP>;
+  using C = Cfg<NT, NW, MS, REP, XP>;
+  constexpr int kThreadsL = threads_of(XP);
   static bool configured = false;
   static int num_sms = 0;
-  auto kern = ssmm_kernel<NT, NW, MS, REP>;
+  auto kern = ssmm_kernel<NT, NW, MS, REP, XP>;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return cuda_status(e);
@@ -729,7 +911,7 @@ smy_status launch_t(const SsmmArgs& a, cudaStream_t s) {
   if (b.pdl) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(kThreadsL);
     cfg.dynamicSmemBytes = C::kSmemBytes;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
@@ -741,7 +923,7 @@ smy_status launch_t(const SsmmArgs& a, cudaStream_t s) {
     count_launch();
     return cuda_status(e);
   }
-  kern<<<grid, kThreads, C::kSmemBytes, s>>>(b);
+  kern<<<grid, kThreadsL, C::kSmemBytes, s>>>(b);
   count_launch();
   return cuda_status(cudaGetLastError());
 }

@@ -277,6 +277,58 @@ def test_ssmm_silu_mul_interleaved(smy, shape):
     check_silu_mul(got, cg, cu, OS.ssmm_abs(eg, x, sel), OS.ssmm_abs(eu, x, sel), f"silu_mul_interleaved {shape}")
 
 
+@pytest.mark.parametrize("fmt", [F.SparseFormat(4, 8, 32), F.SparseFormat(8, 16, 32), F.SparseFormat(2, 4, 32)],
+                         ids=str)
+@pytest.mark.parametrize("shape", [(256, 256, 64, 16), (384, 512, 300, 130), (640, 512, 1000, 900)])
+def test_ssmm_silu_mul_interleaved_expanded(smy, fmt, shape):
+    """(N, 2N, 32) formats, N > 1: the interleaved gate/up SSMM runs the in-smem row
+    expansion of the compressed image, held to the north-star bar
+    against the oracle's bf16 SiLU*up.  (Not bit-equal to the lane-masked M-slot
+    kernel: that one sums a group's N lanes in the epilogue, a different fp32
+    association; both are checked against the oracle.)"""
+    f, d, x_rows, n_sel = shape
+    sel = synth.selection(8, x_rows, n_sel)
+    x = synth.activations_bf16(12, x_rows, d)
+    wg, wu = synth.weight_bf16(50, f, d), synth.weight_bf16(51, f, d)
+    eg, eu = F.encode(F.prune(wg, fmt), fmt), F.encode(F.prune(wu, fmt), fmt)
+    sg, _ = smy.compress(dev16(wg), gpu_format(fmt))
+    su, _ = smy.compress(dev16(wu), gpu_format(fmt))
+    gu = smy.interleave_gate_up(sg, su)
+    st = torch.from_numpy(sel).cuda()
+    got_t = smy.ssmm(gu, dev16(x), st, epi="silu_mul_interleaved")
+    assert tuple(got_t.shape) == (n_sel, f)
+    got = bf16.to_f64(host16(got_t.view(torch.int16)))
+    cg, cu = OS.ssmm(eg, x, sel), OS.ssmm(eu, x, sel)
+    assert np.array_equal(OS.silu_mul_interleaved_bf16(OS.ssmm(F.interleave_gate_up(eg, eu), x, sel)),
+                          OS.silu_mul_bf16(cg, cu))
+    check_silu_mul(got, cg, cu, OS.ssmm_abs(eg, x, sel), OS.ssmm_abs(eu, x, sel), f"expanded silu_mul {fmt} {shape}")
+
+
+@pytest.mark.parametrize("fmt", [F.SparseFormat(4, 8, 32), F.SparseFormat(8, 16, 32), F.SparseFormat(2, 4, 32)],
+                         ids=str)
+@pytest.mark.parametrize("epi", ["compact", "scatter_add", "compact_bf16"])
+def test_ssmm_expanded_integer_exact(smy, fmt, epi):
+    """The row-expansion kernel on integer inputs (exact): compact fp32 / bf16 and the
+    weighted scatter-add, over several m-tiles with a partial last one (rows 640 ->
+    320 compressed rows), ragged token tiles and K of 5 stages."""
+    rows, cols, x_rows, n_sel = 640, 640, 500, 333
+    sel = synth.selection(21, x_rows, n_sel)
+    enc, x, sw = _ssmm_case(smy, fmt, rows, cols, x_rows, sel, integer=True)
+    st = torch.from_numpy(sel).cuda()
+    ref = OS.ssmm(enc, x, sel)
+    if epi == "scatter_add":
+        scale = np.array([2.0 ** (i % 5 - 2) for i in range(n_sel)], dtype=np.float32)
+        base = np.round(np.random.default_rng(1).standard_normal((x_rows, rows)) * 4).astype(np.float32)
+        out = torch.from_numpy(base.copy()).cuda()
+        smy.ssmm(sw, dev16(x), st, epi="scatter_add", scale=torch.from_numpy(scale).cuda(), out=out)
+        assert np.array_equal(out.cpu().numpy(), OS.scatter_add(base.astype(np.float64), ref, sel, scale))
+    elif epi == "compact_bf16":
+        got = smy.ssmm(sw, dev16(x), st, out_dtype=torch.bfloat16)
+        assert np.array_equal(host16(got.view(torch.int16)), bf16.from_f64(ref))
+    else:
+        assert np.array_equal(smy.ssmm(sw, dev16(x), st).cpu().numpy(), ref)
+
+
 @pytest.mark.parametrize("fmt", PARITY_FORMATS, ids=str)
 def test_decompress_and_transcode(smy, fmt):
     """samoyeds_decompress returns the oracle's pruned dense weight bit for bit;
@@ -389,8 +441,15 @@ def _layer_case(smy, fmt, E, d, f, T, k, gating="renorm_topk", shared=0, skew=0.
     dict(fmt=F.SparseFormat(4, 8, 32), E=4, d=256, f=256, T=64, k=2),
     dict(fmt=F.SparseFormat(8, 16, 32), E=4, d=256, f=256, T=50, k=2),
     dict(fmt=F.SparseFormat(1, 2, 32), E=8, d=256, f=512, T=100, k=2, gate_up="separate"),
-    dict(fmt=F.SparseFormat(4, 8, 32), E=4, d=256, f=256, T=300, k=2, transcode="off"),   # lane-masked M=8 slots
+    # native (N, 2N, 32) images: interleaved gate/up + down on the in-smem row expansion
+    dict(fmt=F.SparseFormat(4, 8, 32), E=4, d=256, f=256, T=300, k=2, transcode="off"),
     dict(fmt=F.SparseFormat(8, 16, 32), E=4, d=256, f=256, T=50, k=2, transcode="off"),
+    dict(fmt=F.SparseFormat(4, 8, 32), E=8, d=512, f=640, T=900, k=2, transcode="off", skew=1.0),
+    dict(fmt=F.SparseFormat(8, 16, 32), E=16, d=256, f=384, T=257, k=6, gating="softmax_all", shared=2,
+         transcode="off"),
+    dict(fmt=F.SparseFormat(4, 8, 32), E=8, d=256, f=384, T=7, k=2, transcode="off"),     # decode
+    # lane-masked M = 8 slots (separate gate + up, two-weight launch)
+    dict(fmt=F.SparseFormat(4, 8, 32), E=4, d=256, f=256, T=300, k=2, transcode="off", gate_up="separate"),
     dict(fmt=F.SparseFormat(2, 2, 32), E=4, d=256, f=512, T=400, k=2),                   # plain 2:4, pair kernels
     # N = M gate + up as two weights of one pair launch (NW = 2: half the gather bytes per MMA)
     dict(fmt=F.SparseFormat(2, 2, 32), E=4, d=512, f=512, T=600, k=2, gate_up="separate"),
