@@ -37,6 +37,10 @@
 
 namespace smy {
 
+// expanded-stage ring depth of the (N, 2N, 32) row expansion (shared-memory units of 37 KB)
+#ifndef SMY_XP_SLOTS
+#define SMY_XP_SLOTS 2
+#endif
 template <int NT, int NW, int MS, int REP, int XP = 0>
 struct Cfg {
   static constexpr int kWStride = 19456;                  // A|E|planes, 1024-aligned stride
@@ -46,7 +50,8 @@ struct Cfg {
   // each = two 128-row A halves | their two E images | the enabled-lane masks
   static constexpr int kXMask = 2 * kABytes + 2 * kEBytes;
   static constexpr int kXUnit = XP ? kXMask + 1024 : 0;
-  static constexpr int kXSlots = XP ? 2 : 0;
+  static constexpr int kXFit = (232448 - 1024 - 2048 - 2 * kStageBytes) / (kXMask + 1024);  // keep >= 2 stages
+  static constexpr int kXSlots = XP ? (SMY_XP_SLOTS < kXFit ? SMY_XP_SLOTS : kXFit) : 0;
   static constexpr int kAccCols = NW * MS * NT;
   // two accumulator sets when they fit: the epilogue drains tile i while the
   // MMAs of tile i+1 run (decode-sized tiles)
@@ -74,7 +79,13 @@ struct Cfg {
 constexpr int kThreads = 352;  // warps 0-3 epilogue, 4 producer, 5 + 10 MMA, 6-9 gather
 constexpr int kGatherThreads = 128;
 // XP launches add warps 11-14: the in-smem row expansion
-constexpr int threads_of(int xp) { return xp ? 480 : kThreads; }
+// XP expander warps 11-18 (thread = compressed row x window pair); 4 warps (all four
+// windows per thread) measured slower: decode (4,8,32) 212 K vs 146 K tokens/s
+#ifndef SMY_XP_WARPS
+#define SMY_XP_WARPS 8
+#endif
+constexpr int kXWarps = SMY_XP_WARPS;
+constexpr int threads_of(int xp) { return xp ? kThreads + 32 * kXWarps : kThreads; }
 
 // Expanded row (0..255 of an m-tile's 2 x 128 TMEM lanes) of logical output row o of
 // an (N, 2N, V) m-tile.  Interleaved gate/up weights (reading R20: blocks of 32 gate |
@@ -301,7 +312,7 @@ __device__ __forceinline__ void tma_tile2d(void* dst, const CUtensorMap* map, in
 }
 
 template <int NT, int NW, int MS, int REP, int XP = 0>
-__global__ void __launch_bounds__(XP ? 480 : 352, 1) ssmm_kernel(const __grid_constant__ SsmmArgs a) {
+__global__ void __launch_bounds__(threads_of(XP), 1) ssmm_kernel(const __grid_constant__ SsmmArgs a) {
   constexpr int kIssuers = (NW == 2 || MS >= 2) ? 2 : 1;  // MMA-issuing warps
   using C = Cfg<NT, NW, MS, REP, XP>;
   constexpr int S = C::kStages;
@@ -322,9 +333,13 @@ __global__ void __launch_bounds__(XP ? 480 : 352, 1) ssmm_kernel(const __grid_co
   uint64_t* empty = full + S;
   uint64_t* acc_full = empty + S;      // [kAccBufs]
   uint64_t* acc_empty = acc_full + 2;  // [kAccBufs]
-  uint64_t* xfull = acc_empty + 2;     // [XS] expanded stage written (4 expander warps)
-  uint64_t* xempty = xfull + 2;        // [XS] expanded stage consumed (issuer commits)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xempty + 2);
+  uint64_t* xfull = acc_empty + 2;     // [XS <= 4] expanded stage written (4 expander warps)
+  uint64_t* xempty = xfull + 4;        // [XS <= 4] expanded stage consumed (issuer commits)
+  // XP + SEL gather: the gathered token rows complete on their own barrier, so the
+  // expander (which needs only the weight block) is not held behind the gather
+  uint64_t* bfull = XP ? xempty + 4 : full;  // [S]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xempty + 4 + (XP ? 8 : 0));
+  static_assert(C::kXSlots <= 4, "XP barrier slots");
   constexpr int AB = C::kAccBufs;
   int32_t* rows = reinterpret_cast<int32_t*>(aux + 1024);  // gather row ids of the current tile
   const bool gather = a.sel_in != nullptr;
@@ -332,15 +347,16 @@ __global__ void __launch_bounds__(XP ? 480 : 352, 1) ssmm_kernel(const __grid_co
   const int warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], gather ? 1 + kGatherThreads : 1);
-      mbar_init(&empty[s], kIssuers + (XP ? 4 : 0));  // XP: the expander warps also read the stage
+      mbar_init(&full[s], gather && !XP ? 1 + kGatherThreads : 1);
+      if (XP && gather) mbar_init(&bfull[s], kGatherThreads);
+      mbar_init(&empty[s], kIssuers + (XP ? kXWarps : 0));  // XP: the expander warps also read the stage
     }
     for (int b = 0; b < AB; ++b) {
       mbar_init(&acc_full[b], kIssuers);
       mbar_init(&acc_empty[b], 4);
     }
     for (int x = 0; x < XS; ++x) {
-      mbar_init(&xfull[x], 4);
+      mbar_init(&xfull[x], kXWarps);  // every expander warp
       mbar_init(&xempty[x], kIssuers);
     }
     fence_mbar_init();
@@ -455,16 +471,21 @@ __global__ void __launch_bounds__(XP ? 480 : 352, 1) ssmm_kernel(const __grid_co
           // expanded half mi of this stage: A rows, E image, enabled-lane masks
           const int xs = it % XS;
           t0 = prof ? clk() : 0;
+          if (gather) mbar_wait(&bfull[st], (it / S) & 1);
           mbar_wait(&xfull[xs], (it / XS) & 1);
           if (prof) pc[0] += clk() - t0;
           tc_fence_after();
           const uint32_t xb = smem_base + S * C::kStageBytes + xs * C::kXUnit;
           tc_cp_128x128b_elect(tm + ecol, desc_interleave(xb + 2 * kABytes + mi * kEBytes));
+          uint4 ens[4];  // all four windows' masks first: the LDS latency off the MMA issue chain
+#pragma unroll
+          for (int kb = 0; kb < 4; ++kb) ens[kb] = lds_v4(xb + C::kXMask + (mi * 4 + kb) * 16);
 #pragma unroll
           for (int kb = 0; kb < 4; ++kb) {
-            const uint4 en = lds_v4(xb + C::kXMask + (mi * 4 + kb) * 16);
+            const uint4 en = ens[kb];
             const uint64_t bdesc = desc_sw128(sbase + C::kWStride + (kb / 2) * (NT * 128) + (kb % 2) * 64);
-            const uint64_t adesc = desc_sw128(xb + mi * kABytes + kb * 32);
+            // (SMY_DEBUG & 16777216: both halves' MMAs read half 0's A -- timing probe, results wrong)
+            const uint64_t adesc = desc_sw128(xb + ((a.debug & 16777216) ? 0 : mi) * kABytes + kb * 32);
             if (!(a.debug & 4))
               tc_mma_sp_elect(tacc + mi * NT, adesc, bdesc, idesc | (uint32_t)(kb & 1), ~en.x, ~en.y, ~en.z, ~en.w,
                               tm + ecol + (kb & 2));
@@ -519,15 +540,18 @@ __global__ void __launch_bounds__(XP ? 480 : 352, 1) ssmm_kernel(const __grid_co
   } else if (warp >= 11) {
     if constexpr (XP != 0) {
     // ============ XP: in-smem row expansion (warps 11-14, thread = compressed row) ============
-    const int t = threadIdx.x - 11 * 32, w4 = t >> 5;
+    // Thread = (compressed row t of the m-tile, window group wp): per stage it moves the
+    // row's values / metadata of windows [XW wp, XW wp + XW) from the TMA-staged compressed
+    // block to their expanded rows (all loads first, then the stores).
+    constexpr int XW = 16 / kXWarps;  // windows per thread
+    const int tt = threadIdx.x - kThreads, t = tt & 127, wp = tt >> 7, w4 = t >> 5;
     const int P = a.planes, N = a.n_fmt, M = a.m_fmt;
     const bool ilvp = a.epi == kEpiSiluMulIlv;
     const int gbase = (t / N) * M;  // first logical output row of this row's group (in the m-tile)
-    // this row's swizzled A chunk offsets and E half-word offsets (source side)
     const uint32_t a_src = (uint32_t)((t >> 3) * 1024 + (t & 7) * 128), a_sw = (uint32_t)(t & 7);
     const uint32_t e_src0 = kABytes + 16u * ((t & 7) + 16 * (t >> 4)) + 2u * ((t >> 3) & 1);
     // stale rows are never enabled; start from zero values and valid (0,1) metadata anyway
-    for (int i = t; i < XS * C::kXUnit / 16; i += 128) {
+    for (int i = tt; i < XS * C::kXUnit / 16; i += 32 * kXWarps) {
       const int off = (i * 16) % C::kXUnit;
       const uint32_t v = off >= 2 * kABytes && off < C::kXMask ? 0x44444444u : 0u;
       reinterpret_cast<uint4*>(xsm(0))[i] = make_uint4(v, v, v, v);
@@ -541,49 +565,52 @@ __global__ void __launch_bounds__(XP ? 480 : 352, 1) ssmm_kernel(const __grid_co
         mbar_wait(&full[st], (it / S) & 1);
         if (prof) { const unsigned long long t1 = clk(); pc[8] += t1 - tx0; tx0 = t1; }
         const uint8_t* cw = wsm(st, 0);
-        // every load of the stage first (independent), then the stores
-        uint4 av[8];
+        uint4 av[2 * XW];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) av[c] = *reinterpret_cast<const uint4*>(cw + a_src + ((c ^ a_sw) << 4));
-        uint16_t ev[4][2];
+        for (int c = 0; c < 2 * XW; ++c)
+          av[c] = *reinterpret_cast<const uint4*>(cw + a_src + (((2 * XW * wp + c) ^ a_sw) << 4));
+        uint16_t ev[XW][2];
+        int p[XW];
 #pragma unroll
-        for (int kb = 0; kb < 4; ++kb)
+        for (int j = 0; j < XW; ++j) {
+          const int kb = XW * wp + j;
+          p[j] = 0;
 #pragma unroll
-          for (int k1 = 0; k1 < 2; ++k1) ev[kb][k1] = *reinterpret_cast<const uint16_t*>(cw + e_src0 + 128 * k1 + 4 * kb);
-        int p[4] = {0, 0, 0, 0};
-        for (int b = 0; b < P; ++b)
-#pragma unroll
-          for (int kb = 0; kb < 4; ++kb)
-            p[kb] |= (int)((*reinterpret_cast<const uint32_t*>(cw + kABytes + kEBytes + (kb * P + b) * 16 + w4 * 4) >>
-                            lane) & 1u) << b;
+          for (int k1 = 0; k1 < 2; ++k1) ev[j][k1] = *reinterpret_cast<const uint16_t*>(cw + e_src0 + 128 * k1 + 4 * kb);
+          for (int b = 0; b < P; ++b)
+            p[j] |= (int)((*reinterpret_cast<const uint32_t*>(cw + kABytes + kEBytes + (kb * P + b) * 16 + w4 * 4) >>
+                           lane) & 1u) << b;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);  // the compressed block is read (the MMAs release B)
         mbar_wait(&xempty[xs], ((it / XS) & 1) ^ 1);
         if (prof) { const unsigned long long t1 = clk(); pc[9] += t1 - tx0; tx0 = t1; }
         uint8_t* xu = xsm(xs);
 #pragma unroll
-        for (int kb = 0; kb < 4; ++kb) {
-          const int pos = xp_pos(gbase + p[kb], ilvp);  // in [64 w4, 64 w4 + 64)
+        for (int j = 0; j < XW; ++j) {
+          const int kb = XW * wp + j;
+          const int pos = xp_pos(gbase + p[j], ilvp);  // in [64 w4, 64 w4 + 64)
           const int h = pos >> 7, r = pos & 127;
           uint8_t* arow = xu + h * kABytes + (r >> 3) * 1024 + (r & 7) * 128;
           // A: the window's two 16-B chunks (128B swizzle: chunk c of row r at c ^ (r % 8))
-          *reinterpret_cast<uint4*>(arow + (((2 * kb) ^ (r & 7)) << 4)) = av[2 * kb];
-          *reinterpret_cast<uint4*>(arow + (((2 * kb + 1) ^ (r & 7)) << 4)) = av[2 * kb + 1];
+          *reinterpret_cast<uint4*>(arow + (((2 * kb) ^ (r & 7)) << 4)) = av[2 * j];
+          *reinterpret_cast<uint4*>(arow + (((2 * kb + 1) ^ (r & 7)) << 4)) = av[2 * j + 1];
           // E: the row's 16-bit code word of each K-half (lane (row % 8) + 8 k1 + 16 (row / 16),
           // bits 16 ((row / 8) % 2) of the window's 32-bit column)
           uint8_t* erow = xu + 2 * kABytes + h * kEBytes + 16 * ((r & 7) + 16 * (r >> 4)) + 4 * kb + 2 * ((r >> 3) & 1);
-          *reinterpret_cast<uint16_t*>(erow) = ev[kb][0];
-          *reinterpret_cast<uint16_t*>(erow + 128) = ev[kb][1];
+          *reinterpret_cast<uint16_t*>(erow) = ev[j][0];
+          *reinterpret_cast<uint16_t*>(erow + 128) = ev[j][1];
           const int loc = pos - 64 * w4;
           const uint32_t m0 = __reduce_or_sync(0xffffffffu, loc < 32 ? 1u << loc : 0u);
           const uint32_t m1 = __reduce_or_sync(0xffffffffu, loc >= 32 ? 1u << (loc - 32) : 0u);
           if (lane == 0)
             *reinterpret_cast<uint2*>(xu + C::kXMask + ((w4 >> 1) * 4 + kb) * 16 + 8 * (w4 & 1)) = make_uint2(m0, m1);
         }
-        fence_proxy_async_smem();  // generic-proxy writes -> tcgen05.cp / tcgen05.mma reads
+        if (prof) { const unsigned long long t1 = clk(); pc[11] += t1 - tx0; tx0 = t1; }
+        // generic-proxy writes -> tcgen05.cp / tcgen05.mma reads (SMY_DEBUG & 33554432: skipped, timing probe)
+        if (!(a.debug & 33554432)) fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&xfull[xs]);
-          mbar_arrive(&empty[st]);
-        }
+        if (lane == 0) mbar_arrive(&xfull[xs]);
         if (prof) pc[6] += clk() - tx0;
       }
     }
@@ -626,7 +653,7 @@ __global__ void __launch_bounds__(XP ? 480 : 352, 1) ssmm_kernel(const __grid_co
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(bs + 1024u * i), "l"(src[i] + kcol0)
                              : "memory");
           }
-          cp_async_mbar_arrive_noinc(&full[st]);
+          cp_async_mbar_arrive_noinc(&bfull[st]);
           if (prof) pc[11] += clk() - tg0;
         }
       }
@@ -658,7 +685,7 @@ __global__ void __launch_bounds__(XP ? 480 : 352, 1) ssmm_kernel(const __grid_co
           }
           // the barrier completes when every gather thread's copies have landed;
           // the thread moves on to the next stage immediately
-          cp_async_mbar_arrive_noinc(&full[st]);
+          cp_async_mbar_arrive_noinc(&bfull[st]);
           if (prof) pc[11] += clk() - tg0;
         }
       }
@@ -874,7 +901,9 @@ __global__ void __launch_bounds__(XP ? 480 : 352, 1) ssmm_kernel(const __grid_co
     if (warp == 6 && lane == 0) { atomicAdd(o + 10, pc[10]); atomicAdd(o + 11, pc[11]); }
     if (warp == 0 && lane == 0) { atomicAdd(o + 3, pc[3]); atomicAdd(o + 4, pc[4]); }
     if (warp == 4 && lane == 0) { atomicAdd(o + 5, pc[5]); }
-    if (XP && warp == 11 && lane == 0) { atomicAdd(o + 6, pc[6]); atomicAdd(o + 8, pc[8]); atomicAdd(o + 9, pc[9]); }
+    if (XP && warp == 11 && lane == 0) {
+      atomicAdd(o + 6, pc[6]); atomicAdd(o + 8, pc[8]); atomicAdd(o + 9, pc[9]); atomicAdd(o + 12, pc[11]);
+    }
   }
   __syncthreads();
   tc_fence_after();

@@ -1,5 +1,5 @@
 set -x
-O=gpurun_out/s3c; mkdir -p $O
+O=${O:-gpurun_out/s3c}; mkdir -p $O
 timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -k "expanded or moe_layer_parity or scatter_add_exact or cfg1 or random_tolerance" > $O/pytest_xp.txt 2>&1; echo "rc $?" >> $O/pytest_xp.txt
 SMY_DEBUG=128 timeout 300 python probes/xp_prof.py mixtral 64 4,8,32 off > $O/prof_64.txt 2>&1
 SMY_DEBUG=128 timeout 300 python probes/xp_prof.py mixtral 4096 4,8,32 off > $O/prof_4096.txt 2>&1

@@ -42,5 +42,5 @@ for name, r in zip(("gate/up", "down"), a):
     print(f"{model} T={T} {bench.FMT} {name} (kcycles per CTA per call): tiles {m[7] * 1e3:.2f}")
     print("  MMA: total %.1f wait_full/xfull %.1f wait_acc_empty %.1f | epilogue wait %.1f work %.1f |"
           " producer wait_empty %.1f" % (m[2], m[0], m[1], m[3], m[4], m[5]))
-    print("  expander: wait_full %.1f wait_xempty %.1f work %.1f | gather wait %.1f issue %.1f"
-          % (m[8], m[9], m[6], m[10], m[11]))
+    print("  expander: wait_full %.1f wait_xempty %.1f stores %.1f fence+arrive %.1f | gather wait %.1f issue %.1f"
+          % (m[8], m[9], m[12], m[6], m[10], m[11]))

@@ -149,6 +149,9 @@ def test_moe_layer_rejects_unknown_gating_and_misaligned_out(lib):
     # N = M (and N>1 formats transcoded to it): gate + up and the m-tile-paired down at NT=224
     ("mixtral", (4, 8, 32), 4096, "ssmm_pair_kernel<224, 2, 1, 1>", "ssmm_pair_kernel<224, 2, 1, 1>"),
     ("mixtral", (2, 2, 32), 4096, "ssmm_pair_kernel<224, 2, 1, 1>", "ssmm_pair_kernel<224, 2, 1, 1>"),
+    # native (N, 2N, 32) images (transcode "off"): the in-smem row expansion (XP = 1)
+    ("mixtral", (4, 8, 32, "off"), 64, "ssmm_kernel<32, 1, 2, 1, 1>", "ssmm_kernel<32, 1, 2, 1, 1>"),
+    ("deepseek", (8, 16, 32, "off"), 4096, "ssmm_kernel<128, 1, 2, 1, 1>", "ssmm_kernel<128, 1, 2, 1, 1>"),
 ])
 def test_kernel_selection_rules(lib, model, fmt, T, gu_expect, dn_expect):
     """The launch decisions of samoyeds_moe_layer (tile width, CTA pair vs single CTA,
@@ -156,7 +159,8 @@ def test_kernel_selection_rules(lib, model, fmt, T, gu_expect, dn_expect):
     import bench
     from paper_2503_10725_b200 import api
     d, f, E, k, gating = bench.MODELS[model]
-    cfg = api.MoEConfig(E, k, d, f, 0, gating, api.Format(*fmt)).kernel_config().c()
+    tc = fmt[3] if len(fmt) > 3 else "auto"
+    cfg = api.MoEConfig(E, k, d, f, 0, gating, api.Format(*fmt[:3]), transcode=tc).kernel_config().c()
     gu, dn = C.create_string_buffer(96), C.create_string_buffer(96)
     assert lib.smy_moe_kernel_names(C.byref(cfg), T, gu, dn, 96) == 0
     assert (gu.value.decode(), dn.value.decode()) == (gu_expect, dn_expect)
