@@ -606,7 +606,7 @@ def run_ours(args):
                                    else f"dp{world} (experts replicated per GPU)"),
                    "l2": "inputs larger than L2: %.0f MB of compressed expert weights streamed per step"
                          % (3 * active * f * d * BYTES_PER_ELEM / 1e6),
-                   "weights": "random-init (counter-based synthetic), magnitude-pruned to (1,2,32)",
+                   "weights": "random-init (counter-based synthetic), magnitude-pruned to (%d,%d,%d)" % FMT,
                    "launch": ("cuda graph of the K timed layer calls (no phase-event nodes inside; per-phase "
                               "times from a second replay that records them)") if use_graph else "eager launches"},
         "layer_tflops": flops_layer / (ms * 1e-3) / 1e12,
