@@ -264,6 +264,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
   const uint32_t cta = cluster_rank();
   const bool leader = cta == 0;
   const bool gather = a.sel_in != nullptr;
+  // launches with contiguous token rows leave the gather warps 6-9 idle: they join the
+  // epilogue as a third warp per TMEM lane quadrant (the scatter-add epilogue of short-K
+  // down launches is what the MMA waits for; SMY_DEBUG & 134217728 turns it off)
+  const bool epi3 = !gather && !(a.debug & 134217728);
+  const int NHW = epi3 ? 3 : 2;  // epilogue warps per lane quadrant
   const int warp = warp_id(), lane = lane_id();
   uint8_t* zbuf = aux + 1024;  // 1 KB of zeros: the operand of the accumulator-clearing MMA
   // SMY_DEBUG & 128: clock at which the leader's gather thread 0 issued each token slot
@@ -300,7 +305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
     }
     for (int b = 0; b < (PW ? 2 : AB); ++b) {
       mbar_init(&acc_full[b], PW ? 1 : kIssuers);  // every issuer warp's commit (PW: its weight's)
-      mbar_init(&acc_empty[b], 2 * kPairEpiWarps);  // every epilogue warp of both CTAs
+      mbar_init(&acc_empty[b], 2 * 4 * NHW);  // every epilogue warp of both CTAs
     }
     fence_mbar_init();
   }
@@ -513,7 +518,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
           mbar_arrive_cluster(bfull_lead + sb * 8);
         }
     }
-  } else if ((warp >= 6 && warp < 10) || warp >= 15) {
+  } else if ((warp >= 6 && warp < 10 && !epi3) || warp >= 15) {
     // ============ SEL gather of this CTA's half of the token rows (cp.async) ============
     // Thread tb owns the 16-B chunk ch = tb % 16 of rows tb/16 + RS*i (i < H/RS,
     // RS = gather threads / 16) of the tile for every k-stage, so the row lookups,
@@ -592,10 +597,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
     // 16-column chunks (even / odd) so two warps per SM sub-partition hide the
     // epilogue's dependent-latency chains.
     const int q = warp & 3;
-    const int h = warp >= 10 ? 1 : 0;
+    const int h = warp >= 10 ? 1 : warp >= 6 ? 2 : 0;  // this warp's share of the 16-column chunks
+    const int cstep = 16 * NHW;
     if (a.pdl) griddep_wait();  // outputs (zeroed by the previous kernel) are written below
     if (a.zero_ptr != nullptr)
-      zero_slice(a, (int64_t)blockIdx.x * 256 + (q + 4 * h) * 32 + lane, (int64_t)gridDim.x * 256);
+      zero_slice(a, (int64_t)blockIdx.x * 128 * NHW + (q + 4 * h) * 32 + lane, (int64_t)gridDim.x * 128 * NHW);
     const uint32_t lane_base = (uint32_t)(32 * q) << 16;
     const uint32_t acc_empty_leader = mapa_shared(smem_u32(acc_empty), 0);
     // the accumulator is cleared by the issuer's zero MMA at the start of each tile,
@@ -625,12 +631,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
           mbar_wait_cta(&acc_full[w], tcount & 1);
           tc_fence_after();
           const int cgw = cg + w * a.mtp_half * 64;  // a 128-lane m-tile holds 64 outputs
-          for (int c0 = 16 * h; c0 < ti.n_local; c0 += 32) {
+          for (int c0 = 16 * h; c0 < ti.n_local; c0 += cstep) {
             float v[2][16];
             tmem_ld16(tacc + lane_base + (2 * w) * NT + c0, v[0]);
             tmem_ld16(tacc + lane_base + (2 * w + 1) * NT + c0, v[1]);
             tmem_ld_wait();
-            if (c0 + 32 >= ti.n_local) release(w);
+            if (c0 + cstep >= ti.n_local) release(w);
             if (!(a.debug & 32))
               ilv_chunk(v, gvalid && cgw < a.R / 2, min(16, ti.n_local - c0), static_cast<uint16_t*>(a.out), a.ldo,
                         ti.row0 + ti.t0 + c0, cgw, lane, a.rows_out);
@@ -647,7 +653,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
         // lanes 0-15 gate / 16-31 up of the same 16 output pairs (reading R20)
         const int cg = 16 * (4 * m_own + q) + (lane & 15);
         const bool gvalid = m_own < a.m_tiles && cg < a.R / 2 && !(a.debug & 8);
-        for (int c0 = 16 * h; c0 < ti.n_local; c0 += 32) {
+        for (int c0 = 16 * h; c0 < ti.n_local; c0 += cstep) {
           const unsigned long long tl0 = prof ? clk() : 0;
           if constexpr (MS == 2 && NW == 2) {  // m-tile pairing: weight 1 = m-tiles [half, 2 half)
             float v[2][2][16];
@@ -657,7 +663,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
               tmem_ld16(tacc + lane_base + (2 * w + 1) * NT + c0, v[w][1]);
             }
             tmem_ld_wait();
-            if (c0 + 32 >= ti.n_local) release(ab);
+            if (c0 + cstep >= ti.n_local) release(ab);
             if (prof) pc[8] += clk() - tl0;
             const int cg1 = cg + a.mtp_half * 64;  // a 128-lane m-tile holds 64 outputs
             if (!(a.debug & 32)) {
@@ -671,7 +677,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
             tmem_ld16(tacc + lane_base + c0, v[0]);
             tmem_ld16(tacc + lane_base + NT + c0, v[1]);
             tmem_ld_wait();
-            if (c0 + 32 >= ti.n_local) release(ab);
+            if (c0 + cstep >= ti.n_local) release(ab);
             if (prof) pc[8] += clk() - tl0;
             if (!(a.debug & 32))
               ilv_chunk(v, gvalid, min(16, ti.n_local - c0), static_cast<uint16_t*>(a.out), a.ldo,
@@ -680,7 +686,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
             float v[16];
             tmem_ld16(tacc + lane_base + c0, v);
             tmem_ld_wait();
-            if (c0 + 32 >= ti.n_local) release(ab);
+            if (c0 + cstep >= ti.n_local) release(ab);
             if (prof) pc[8] += clk() - tl0;
             if (!(a.debug & 32))
               ilv_chunk_ms1(v, gvalid, min(16, ti.n_local - c0), static_cast<uint16_t*>(a.out), a.ldo,
@@ -688,7 +694,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
           }
         }
       }
-      for (int c0 = 16 * h; !ilv && c0 < ti.n_local; c0 += 32) {
+      for (int c0 = 16 * h; !ilv && c0 < ti.n_local; c0 += cstep) {
         float v[NW][MS][16];
         const unsigned long long tl0 = prof ? clk() : 0;
 #pragma unroll
@@ -696,7 +702,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
 #pragma unroll
           for (int p = 0; p < MS; ++p) tmem_ld16(tacc + lane_base + (w * MS + p) * NT + c0, v[w][p]);
         tmem_ld_wait();
-        if (c0 + 32 >= ti.n_local) release(ab);
+        if (c0 + cstep >= ti.n_local) release(ab);
         if (prof) pc[8] += clk() - tl0;
         const int jmax = min(16, ti.n_local - c0);
         const int n = (valid && !(a.debug & 8)) ? jmax : 0;
