@@ -193,7 +193,14 @@ constexpr int pair_gather_warps(int split, int nt) {
   return !split ? 4 : (nt / 2) % (2 * SMY_PAIR_GATHER_WARPS) == 0 ? SMY_PAIR_GATHER_WARPS
                     : (SMY_PAIR_GATHER_WARPS >= 7 && (nt / 2) % 14 == 0) ? 7 : 4;
 }
-constexpr int pair_threads(int split, int nt) { return kPairThreads + 32 * (pair_gather_warps(split, nt) - 4); }
+// lock-step (SPLIT = 0) kernels carry 4 more warps (15-18): a fourth epilogue warp per
+// TMEM lane quadrant when the token rows are contiguous (the down), idle otherwise
+#ifndef SMY_PAIR_EPI4
+#define SMY_PAIR_EPI4 1
+#endif
+constexpr int pair_threads(int split, int nt) {
+  return kPairThreads + 32 * (pair_gather_warps(split, nt) - 4) + (!split && SMY_PAIR_EPI4 ? 128 : 0);
+}
 constexpr int pair_gather_threads(int split, int nt) { return 32 * pair_gather_warps(split, nt); }
 
 // MS = accumulator slots per weight: 2 for (1,2,V) (the lane-masked remap), 1 for
@@ -268,7 +275,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
   // epilogue as a third warp per TMEM lane quadrant (the scatter-add epilogue of short-K
   // down launches is what the MMA waits for; SMY_DEBUG & 134217728 turns it off)
   const bool epi3 = !gather && !(a.debug & 134217728);
-  const int NHW = epi3 ? 3 : 2;  // epilogue warps per lane quadrant
+  const bool epi4 = epi3 && !SPLIT && SMY_PAIR_EPI4;  // + warps 15-18
+  const int NHW = epi4 ? 4 : epi3 ? 3 : 2;  // epilogue warps per lane quadrant
   const int warp = warp_id(), lane = lane_id();
   uint8_t* zbuf = aux + 1024;  // 1 KB of zeros: the operand of the accumulator-clearing MMA
   // SMY_DEBUG & 128: clock at which the leader's gather thread 0 issued each token slot
@@ -518,7 +526,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
           mbar_arrive_cluster(bfull_lead + sb * 8);
         }
     }
-  } else if ((warp >= 6 && warp < 10 && !epi3) || warp >= 15) {
+  } else if (warp >= 15 && !SPLIT && !epi4) {
+    // idle: the lock-step kernel's fourth epilogue warps on a SEL-gather launch
+  } else if ((warp >= 6 && warp < 10 && !epi3) || warp >= 15 && SPLIT) {
     // ============ SEL gather of this CTA's half of the token rows (cp.async) ============
     // Thread tb owns the 16-B chunk ch = tb % 16 of rows tb/16 + RS*i (i < H/RS,
     // RS = gather threads / 16) of the tile for every k-stage, so the row lookups,
@@ -597,7 +607,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(SPLIT, 
     // 16-column chunks (even / odd) so two warps per SM sub-partition hide the
     // epilogue's dependent-latency chains.
     const int q = warp & 3;
-    const int h = warp >= 10 ? 1 : warp >= 6 ? 2 : 0;  // this warp's share of the 16-column chunks
+    const int h = warp >= 15 ? 3 : warp >= 10 ? 1 : warp >= 6 ? 2 : 0;  // this warp's share of the chunks
     const int cstep = 16 * NHW;
     if (a.pdl) griddep_wait();  // outputs (zeroed by the previous kernel) are written below
     if (a.zero_ptr != nullptr)
