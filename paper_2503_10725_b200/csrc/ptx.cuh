@@ -218,10 +218,23 @@ __device__ __forceinline__ uint64_t desc_interleave(uint32_t saddr) {
 __device__ __forceinline__ void red_add_v2(float* addr, float a, float b) {
   asm volatile("red.relaxed.gpu.global.add.v2.f32 [%0], {%1, %2};" ::"l"(addr), "f"(a), "f"(b) : "memory");
 }
+// SMY_RED_EVICT_LAST: the scatter-add reductions carry an L2 evict_last hint (the layer
+// output -- 67 MB for Mixtral T=4096 -- receives top_k contributions at different times)
+#ifndef SMY_RED_EVICT_LAST
+#define SMY_RED_EVICT_LAST 0
+#endif
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+#if SMY_RED_EVICT_LAST
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(addr), "f"(a),
+               "f"(b), "f"(c), "f"(d), "l"(pol)
+               : "memory");
+#else
   asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
                "f"(d)
                : "memory");
+#endif
 }
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
