@@ -67,7 +67,8 @@ class EPMoELayer:
         self.e_local = cfg.num_experts // world
         if len(local_experts) != self.e_local:
             raise ValueError(f"rank {rank} needs {self.e_local} local experts")
-        self.local_cfg = api.MoEConfig(self.e_local, cfg.top_k, cfg.hidden, cfg.ffn, 0, cfg.gating, cfg.fmt, cfg.gate_up)
+        self.local_cfg = api.MoEConfig(self.e_local, cfg.top_k, cfg.hidden, cfg.ffn, 0, cfg.gating, cfg.fmt, cfg.gate_up,
+                                       cfg.transcode)
         self.device = device or torch.device("cuda")
         # a rank can receive every token of every rank once
         self.experts = api.MoEExperts(self.local_cfg, local_experts, max_rows=max(1, max_tokens * world),
@@ -167,7 +168,7 @@ class PeerEPMoELayer:
         if len(local_experts) != self.e_local:
             raise ValueError(f"rank {rank} needs {self.e_local} local experts")
         self.local_cfg = api.MoEConfig(self.e_local, cfg.top_k, cfg.hidden, cfg.ffn, 0, cfg.gating, cfg.fmt,
-                                       cfg.gate_up)
+                                       cfg.gate_up, cfg.transcode)
         self.device = device or torch.device("cuda")
         self.max_tokens = max_tokens
         self.experts = api.MoEExperts(self.local_cfg, local_experts, max_rows=max(1, max_tokens * world),

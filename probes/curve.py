@@ -12,6 +12,7 @@ HBM GB/s) below the ridge, the 2:4-sparse tensor peak (2 x measured dense bf16)
 above it -- the same byte / flop formulas as bench.py.
 
     python probes/curve.py mixtral 1,2,4,...  > profiles/r2_curve_mixtral.json
+    SMY_FORMAT=4,8,32 SMY_TRANSCODE=off python probes/curve.py mixtral ...   (other formats / native images)
 """
 import json
 import os
@@ -31,11 +32,14 @@ def main():
     Ts = [int(t) for t in sys.argv[2].split(",")]
     reps = int(sys.argv[3]) if len(sys.argv) > 3 else 30
     d, f, E, k, gating = bench.MODELS[model]
+    if os.environ.get("SMY_FORMAT"):
+        bench.set_format(os.environ["SMY_FORMAT"])  # FMT and the per-element byte count
+    tc = os.environ.get("SMY_TRANSCODE", "auto")
     dev = torch.device("cuda")
     lib = P.load()
     Tmax = max(Ts)
-    layer = P.MoELayer(P.MoEConfig(E, k, d, f, 0, gating, P.Format(*bench.FMT)), bench.build_layer(P, model, dev),
-                       max_tokens=Tmax, device=dev)
+    layer = P.MoELayer(P.MoEConfig(E, k, d, f, 0, gating, P.Format(*bench.FMT), transcode=tc),
+                       bench.build_layer(P, model, dev, transcode=tc), max_tokens=Tmax, device=dev)
     x = torch.empty(Tmax, d, dtype=torch.int16, device=dev)
     P.synth_fill(x, synth.SEED_X, synth.DIST_NORMAL, float(synth.normal_scale(1.0)))
     lg = torch.empty(Tmax, E, dtype=torch.float32, device=dev)

@@ -73,11 +73,15 @@ def _ep_inproc(smy, layers, xs, lgs):
     return outs
 
 
-@pytest.mark.parametrize("world,E,k,gating", [(2, 8, 2, "renorm_topk"), (4, 8, 2, "renorm_topk"),
-                                             (4, 16, 6, "softmax_all")])
-def test_ep_layer_matches_oracle(smy, world, E, k, gating):
+@pytest.mark.parametrize("world,E,k,gating,nmv,tc", [(2, 8, 2, "renorm_topk", (1, 2, 32), "auto"),
+                                                     (4, 8, 2, "renorm_topk", (1, 2, 32), "auto"),
+                                                     (4, 16, 6, "softmax_all", (1, 2, 32), "auto"),
+                                                     # native (4,8,32) image: the row-expansion kernels
+                                                     # on the receive side (keys / values routing)
+                                                     (2, 8, 2, "renorm_topk", (4, 8, 32), "off")])
+def test_ep_layer_matches_oracle(smy, world, E, k, gating, nmv, tc):
     from paper_2503_10725_b200.ep import EPMoELayer
-    fmt = F.SparseFormat(1, 2, 32)
+    fmt = F.SparseFormat(*nmv)
     d, f, T = 256, 384, 100
     encs, sws = [], []
     for e in range(E):
@@ -86,10 +90,10 @@ def test_ep_layer_matches_oracle(smy, world, E, k, gating):
             r, c = (f, d) if i < 2 else (d, f)
             wb = synth.weight_bf16(synth.weight_seed(e, i), r, c)
             te.append(F.encode(F.prune(wb, fmt), fmt))
-            ts.append(smy.compress(dev16(wb), smy.Format(1, 2, 32))[0])
+            ts.append(smy.compress(dev16(wb), smy.Format(*nmv))[0])
         encs.append(tuple(te))
         sws.append(tuple(ts))
-    cfg = smy.MoEConfig(E, k, d, f, 0, gating, smy.Format(1, 2, 32))
+    cfg = smy.MoEConfig(E, k, d, f, 0, gating, smy.Format(*nmv), transcode=tc)
     el = E // world
     layers = [EPMoELayer(cfg, sws[r * el:(r + 1) * el], r, world, max_tokens=T) for r in range(world)]
     xs_np = [synth.activations_bf16(synth.SEED_X + 100 * r, T, d) for r in range(world)]
