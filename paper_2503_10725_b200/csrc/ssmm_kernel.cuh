@@ -37,6 +37,10 @@
 
 namespace smy {
 
+// L2 prefetch distance (stages) of the row-expansion kernels' weight stream (0 = off)
+#ifndef SMY_XP_PREFETCH
+#define SMY_XP_PREFETCH 0
+#endif
 // expanded-stage ring depth of the (N, 2N, 32) row expansion (shared-memory units of 37 KB)
 #ifndef SMY_XP_SLOTS
 #define SMY_XP_SLOTS 2
@@ -413,6 +417,12 @@ __global__ void __launch_bounds__(threads_of(XP), 1) ssmm_kernel(const __grid_co
           mbar_arrive_expect_tx(&full[st], stage_bytes - (skip_w ? NW * wbytes : 0u));
           if (!skip_w) {
             bulk_g2s(wsm(st, 0), src0 + (size_t)k * a.block, wbytes, &full[st], pol_w);
+            // XP: the expanded units leave fewer stages in flight -- pull the block
+            // SMY_XP_PREFETCH stages ahead into L2 (no shared memory needed for that)
+            if (XP && SMY_XP_PREFETCH > 0 && k + SMY_XP_PREFETCH < ti.k1)
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src0 + (size_t)(k + SMY_XP_PREFETCH) * a.block),
+                           "r"(wbytes)
+                           : "memory");
             if (NW == 2) bulk_g2s(wsm(st, 1), src1 + (size_t)k * a.block, wbytes, &full[st], pol_w);
           }
           if (!gather) {
