@@ -306,12 +306,16 @@ def test_ssmm_silu_mul_interleaved_expanded(smy, fmt, shape):
 
 @pytest.mark.parametrize("fmt", [F.SparseFormat(4, 8, 32), F.SparseFormat(8, 16, 32), F.SparseFormat(2, 4, 32)],
                          ids=str)
-@pytest.mark.parametrize("epi", ["compact", "scatter_add", "compact_bf16"])
+@pytest.mark.parametrize("epi", ["compact", "scatter_add", "compact_bf16", "compact_longk"])
 def test_ssmm_expanded_integer_exact(smy, fmt, epi):
     """The row-expansion kernel on integer inputs (exact): compact fp32 / bf16 and the
     weighted scatter-add, over several m-tiles with a partial last one (rows 640 ->
-    320 compressed rows), ragged token tiles and K of 5 stages."""
+    320 compressed rows), ragged token tiles and K of 5 stages; compact_longk: few tiles
+    and K = 2560 (20 stages), which samoyeds_ssmm runs as a split-K / stream-K
+    scatter-add into zeroed rows."""
     rows, cols, x_rows, n_sel = 640, 640, 500, 333
+    if epi == "compact_longk":
+        rows, cols, x_rows, n_sel, epi = 256, 2560, 200, 40, "compact"
     sel = synth.selection(21, x_rows, n_sel)
     enc, x, sw = _ssmm_case(smy, fmt, rows, cols, x_rows, sel, integer=True)
     st = torch.from_numpy(sel).cuda()
