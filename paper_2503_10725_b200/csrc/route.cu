@@ -228,6 +228,25 @@ __global__ void route_small_kernel(const float* __restrict__ logits, int64_t T, 
   small_route(logits, T, E, k, ns, gating, ids, w, counts, offsets, nt0, mt0, prefix0, nt1, mt1, prefix1, sel, gw);
 }
 
+// 32 < T <= 64 in ONE launch: a cluster of 8 CTAs, one warp per token (token t on CTA
+// t % 8), a cluster barrier (release / acquire at cluster scope) publishes ids / w, and
+// CTA 0 compacts (small_route without the top-k).  (4 tokens per warp for T <= 256
+// measured slower than the grid-wide top-k launch + one-block compaction.)
+constexpr int kRouteCluster = 8;
+__global__ void __cluster_dims__(kRouteCluster, 1, 1)
+    route_cluster_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int ns, int gating,
+                         int32_t* __restrict__ ids, float* __restrict__ w, int32_t* __restrict__ counts,
+                         int32_t* __restrict__ offsets, int nt0, int mt0, int32_t* __restrict__ prefix0, int nt1,
+                         int mt1, int32_t* __restrict__ prefix1, int32_t* __restrict__ sel, float* __restrict__ gw) {
+  const int wp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int ld = (gating & SMY_GATE_SHARED_SIGMOID) ? E : E - ns;  // logits row (E, k include the ns shared)
+  for (int t = (int)blockIdx.x + kRouteCluster * wp; t < T; t += kRouteCluster * kRouteWarps)
+    topk_token(logits + (int64_t)t * ld, E - ns, k - ns, gating, lane, ids + (int64_t)t * k, w + (int64_t)t * k, ns);
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (blockIdx.x != 0) return;
+  small_route(nullptr, T, E, k, ns, gating, ids, w, counts, offsets, nt0, mt0, prefix0, nt1, mt1, prefix1, sel, gw);
+}
+
 // Single block: counts, offsets, per-block bases and SSMM tile prefixes.
 __global__ void route_scan_kernel(const int32_t* __restrict__ blk_counts, int nblk, int E, int32_t* __restrict__ counts,
                                   int32_t* __restrict__ offsets, int32_t* __restrict__ blk_base, int nt0, int mt0,
@@ -321,6 +340,13 @@ smy_status route_launch(const float* logits, int64_t T, int E, int k, int gating
     // 1024-thread block doing both, top-k by argmax rounds, and one cooperative launch
     // with a grid barrier -- probes/route_ab.sh)
     const bool fused_topk = T <= 4 * kRouteWarps;
+    if (logits != nullptr && !fused_topk && T <= kRouteCluster * kRouteWarps && !(debug_flags() & 268435456)) {
+      // one launch: a cluster of 8 CTAs (SMY_DEBUG & 268435456: the two-launch path)
+      route_cluster_kernel<<<kRouteCluster, kRouteThreads, 0, s>>>(logits, T, E, k, ns, gating, ids, w, counts,
+                                                                  offsets, nt0, mt0, pre0, nt1, mt1, pre1, sel, gw);
+      count_launch();
+      return cuda_status(cudaGetLastError());
+    }
     if (logits != nullptr && !fused_topk) {
       route_topk_kernel<<<(unsigned)((T + kRouteWarps - 1) / kRouteWarps), kRouteThreads, 0, s>>>(logits, T, Er, kr,
                                                                                                  gating, ids, w, ns);
