@@ -339,7 +339,8 @@ smy_status route_launch(const float* logits, int64_t T, int E, int k, int gating
     // (16 per warp measured slower than two launches; so were, at T = 64, E = 64: one
     // 1024-thread block doing both, top-k by argmax rounds, and one cooperative launch
     // with a grid barrier -- probes/route_ab.sh)
-    const bool fused_topk = T <= 4 * kRouteWarps;
+    // (fused top-k in the one block: one token per warp; 9..64 tokens: the cluster launch)
+    const bool fused_topk = T <= ((debug_flags() & 268435456) ? 4 * kRouteWarps : kRouteWarps);
     if (logits != nullptr && !fused_topk && T <= kRouteCluster * kRouteWarps && !(debug_flags() & 268435456)) {
       // one launch: a cluster of 8 CTAs (SMY_DEBUG & 268435456: the two-launch path)
       route_cluster_kernel<<<kRouteCluster, kRouteThreads, 0, s>>>(logits, T, E, k, ns, gating, ids, w, counts,
